@@ -1,0 +1,356 @@
+#!/usr/bin/env python
+"""Benchmark of the throttLL'eM frequency-selection hot path (BASELINE.json metric: frequency
+decisions/s and GBDT grid evals/s vs roofline).
+
+One step = one decision round over the workload: K1 projection -> K2 GBDT grid -> K3 SLO scan
+(+ one NCCL all-gather of the decisions when N > 1).  Inputs are synthetic and seeded
+(paper_2408_05235_b200/workload.py), already resident in HBM when the timed region starts.
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--workload C2] [--impl ours|reference]
+
+N > 1 runs under torchrun (one process per GPU, NCCL).  Default workload C2 = BASELINE.json
+configs[1]; per-GPU work is fixed (weak scaling: rank r decides instances [r*I, (r+1)*I) of the
+same generator).  --workload C5 is the strong-scaling sweep (262,144 instances split over N).
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+from paper_2408_05235_b200 import workload as W  # noqa: E402
+
+DESCR = {
+    "C1": "BASELINE configs[0]: 1 instance, 8 running + 4 queued, 16 KV blocks/req cap, 8 freq levels, 64-iter horizon, 50-tree depth-6 GBDT",
+    "C2": "BASELINE configs[1]: 1,024 instances, batch<=64, 16 freq levels, 512-iter horizon, 200-tree depth-8 GBDT",
+    "C3": "BASELINE configs[2]: 65,536 instances, synthetic Azure-like trace, batch<=256, 32 freq levels, 1,024-iter horizon (200-tree depth-8 assumed)",
+    "C4": "BASELINE configs[3]: 4,096 TP instance states, 500-tree depth-8 GBDT (one re-decision round)",
+    "C5": "BASELINE configs[4]: 262,144 instances sharded over N GPUs (strong scaling), 200-tree depth-8",
+}
+SKIP = 64 | 1 | 2
+
+
+def env_int(k, d):
+    try:
+        return int(os.environ.get(k, d))
+    except ValueError:
+        return d
+
+
+def shard_of(cfg, rank, world):
+    """Instance range of this rank and the global instance count (paper_2408_05235_b200/shard.py)."""
+    from paper_2408_05235_b200 import shard
+    if cfg.name == "C5":            # strong scaling: fixed total
+        return (*shard.shard_range(cfg.n_inst, rank, world), cfg.n_inst)
+    return (*shard.weak_range(cfg.n_inst, rank), cfg.n_inst * world)   # weak: fixed per GPU
+
+
+class Clocks:
+    """nvidia-smi sampling during the timed region (clock line of B200_PROFILING.md)."""
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
+         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+         "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, dev_index):
+        self.dev = dev_index
+        self.p = None
+
+    def start(self):
+        try:
+            self.p = subprocess.Popen(["nvidia-smi", f"--query-gpu={self.Q}", "--format=csv,noheader,nounits",
+                                       "-lms", "100", "-i", str(self.dev)], stdout=subprocess.PIPE,
+                                      stderr=subprocess.DEVNULL, text=True)
+        except OSError:
+            self.p = None
+
+    def stop(self):
+        if self.p is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"], "samples": 0}
+        time.sleep(0.25)
+        self.p.terminate()
+        out, _ = self.p.communicate(timeout=10)
+        sm, mx, reasons = [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for line in out.strip().splitlines():
+            f = [x.strip() for x in line.split(",")]
+            if len(f) < 9:
+                continue
+            try:
+                sm.append(float(f[1]))
+                mx.append(float(f[2]))
+            except ValueError:
+                continue
+            for nm, v in zip(names, f[5:9]):
+                if v.lower() == "active":
+                    reasons.add(nm)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+def measured_peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            return json.load(f)
+    except (OSError, ValueError):
+        return {}
+
+
+def cpu_baseline(cfg, blob, inputs, budget_s=15.0):
+    """The oracle, as it stands, on this host's cores, on a bounded prefix of the workload."""
+    from oracle import oracle
+    m = oracle.Model(blob)
+    threads = os.cpu_count() or 1
+    inst = inputs["inst"]
+
+    def run(k):
+        sub = inst[:k]
+        last = int(sub[-1]["req_begin"] + sub[-1]["n_run"] + sub[-1]["n_queue"])
+        t = time.perf_counter()
+        oracle.decide(m, sub, inputs["req"][:last], inputs["t_dead"][:last], inputs["H"], inputs["freq"],
+                      inputs["tbt_slo"], want_grid=False, want_curves=False, threads=threads)
+        return time.perf_counter() - t
+
+    k = min(len(inst), max(threads, 8))
+    dt = run(k)
+    while k < len(inst) and dt < 1.0:
+        k = min(len(inst), k * 4)
+        dt = run(k)
+    if k < len(inst) and dt < budget_s:
+        k = min(len(inst), max(k, int(k * budget_s / max(dt, 1e-3))))
+        dt = run(k)
+    return {"value": k / dt, "unit": "decisions/s", "cores": threads, "kind": "oracle",
+            "sample": f"first {k} of {len(inst)} instances of {cfg.name} (all levels scanned up to the lowest "
+                      f"passing one, {threads} threads), {dt:.1f} s"}
+
+
+def bench_reference(args, cfg):
+    """--impl reference: the CPU oracle is this tier's reference arm (rank 0 only)."""
+    rank = env_int("RANK", 0)
+    if rank != 0:
+        return
+    blob = W.write_blob(W.config_ensemble(cfg))
+    per_step = {"C1": 1, "C2": 64, "C3": 16, "C4": 8, "C5": 16}[cfg.name]
+    inputs = W.config_inputs(cfg, 0, max(per_step, 1))
+    from oracle import oracle
+    m = oracle.Model(blob)
+    threads = os.cpu_count() or 1
+
+    def step():
+        oracle.decide(m, inputs["inst"], inputs["req"], inputs["t_dead"], inputs["H"], inputs["freq"],
+                      inputs["tbt_slo"], want_grid=False, want_curves=False, threads=threads)
+    for _ in range(args.warmup):
+        step()
+    t = time.perf_counter()
+    for _ in range(args.steps):
+        step()
+    dt = time.perf_counter() - t
+    v = per_step * args.steps / dt
+    line = {"impl": "reference", "metric": "frequency decisions/sec", "value": v, "unit": "decisions/s",
+            "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup, "ms_per_step": dt / args.steps * 1e3,
+            "higher_is_better": True, "scaling": "weak" if cfg.name != "C5" else "strong", "vs_baseline": None,
+            "dtype": "f32", "data": "synthetic",
+            "config": {"workload": DESCR[cfg.name], "instances_per_step": per_step},
+            "cpu_baseline": {"value": v, "unit": "decisions/s", "cores": threads, "kind": "oracle",
+                             "sample": f"first {per_step} instances of {cfg.name} per step"},
+            "e2e": {"value": v, "unit": "decisions/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=100)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--workload", default="C2", choices=sorted(DESCR))
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--e2e-steps", type=int, default=None)
+    args = ap.parse_args()
+    cfg = W.CONFIGS[args.workload]
+    if args.impl == "reference":
+        return bench_reference(args, cfg)
+
+    import torch
+    import torch.distributed as dist
+    from paper_2408_05235_b200 import runner, tp
+
+    world = env_int("WORLD_SIZE", 1)
+    rank = env_int("RANK", 0)
+    local = env_int("LOCAL_RANK", 0)
+    if world != args.gpus:
+        print(f"warning: --gpus {args.gpus} but WORLD_SIZE={world}; using WORLD_SIZE", file=sys.stderr)
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+
+    i0, i1, I_glob = shard_of(cfg, rank, world)
+    blob = W.write_blob(W.config_ensemble(cfg))
+    inputs = W.config_inputs(dataclasses_replace(cfg, I_glob), i0, i1)
+    I, R = len(inputs["inst"]), len(inputs["req"])
+    model = tp.Gbdt(blob, local)
+    info = model.info()
+    rnd = runner.Round(inputs, dev)
+    dec = torch.empty((2, max(I, 1)), dtype=torch.int32, device=dev)   # level, status rows
+    rnd.level, rnd.status = dec[0], dec[1]
+    # equal shards (C2 weak, C5 = 262144 / {1,2,4,8}): one preallocated all-gather of [2, I] rows
+    gathered = torch.empty((world * 2, max(I, 1)), dtype=torch.int32, device=dev) if world > 1 else None
+    stream = torch.cuda.current_stream(dev)
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)     # > 126 MB L2
+
+    def step(evs=None):
+        if evs:
+            evs[0].record(stream)
+        rnd.project(stream)
+        if evs:
+            evs[1].record(stream)
+        rnd.predict(model, stream)
+        if evs:
+            evs[2].record(stream)
+        rnd.select(stream)
+        if evs:
+            evs[3].record(stream)
+        if world > 1:
+            dist.all_gather_into_tensor(gathered, dec)
+        if evs:
+            evs[4].record(stream)
+
+    for _ in range(max(args.warmup, 3)):
+        step()
+    torch.cuda.synchronize(dev)
+
+    # algorithmic grid size of this rank (from K1's outputs; not timed)
+    n_h = rnd.n[:I].cpu().numpy().astype(np.int64)
+    st_h = rnd.status[:I].cpu().numpy().view(np.uint32)
+    grid = int((n_h * ((st_h & SKIP) == 0)).sum()) * rnd.F
+    padded = int((((n_h + 31) // 32) * 32 * ((st_h & SKIP) == 0)).sum()) * rnd.F
+
+    evs = [[torch.cuda.Event(enable_timing=True) for _ in range(5)] for _ in range(args.steps)]
+    clocks = Clocks(local)
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize(dev)
+    clocks.start()
+    time.sleep(0.3)
+    for k in range(args.steps):
+        flush.zero_()                      # untimed L2 flush between timed steps
+        step(evs[k])
+    torch.cuda.synchronize(dev)
+    clk = clocks.stop()
+    if world > 1:
+        dist.barrier()
+    per = np.array([[e[j].elapsed_time(e[j + 1]) for j in range(4)] for e in evs])   # ms
+    t_total = float(per.sum())
+    k_ms = per.mean(axis=0)
+    tot = torch.tensor([t_total, grid, I], dtype=torch.float64, device=dev)
+    if world > 1:
+        mx = tot.clone()
+        dist.all_reduce(mx[:1], op=dist.ReduceOp.MAX)
+        dist.all_reduce(tot[1:], op=dist.ReduceOp.SUM)
+        tot[0] = mx[0]
+    t_max_ms, grid_all, inst_all = float(tot[0]), float(tot[1]), float(tot[2])
+    sec = t_max_ms / 1e3
+    decisions_per_s = inst_all * args.steps / sec
+    grid_per_s = grid_all * args.steps / sec
+
+    # end to end through the C ABI with host buffers (pinned), copies inside the timed region
+    e2e = None
+    if True:
+        ctx = tp.Ctx(local, I, R, rnd.H, rnd.F)
+        h_inst = torch.from_numpy(inputs["inst"].view(np.uint8)).pin_memory()
+        h_req = torch.from_numpy(inputs["req"].view(np.uint8)).pin_memory()
+        h_td = torch.from_numpy(inputs["t_dead"]).pin_memory()
+        h_level = torch.empty(max(I, 1), dtype=torch.int32).pin_memory()
+        h_status = torch.empty(max(I, 1), dtype=torch.int32).pin_memory()
+        ke = args.e2e_steps or args.steps
+        for _ in range(3):
+            ctx.decide_host(model, h_inst, I, h_req, R, h_td, rnd.freq, rnd.tbt, h_level, h_status, stream)
+        torch.cuda.synchronize(dev)
+        ee = [[torch.cuda.Event(enable_timing=True) for _ in range(2)] for _ in range(ke)]
+        for k in range(ke):
+            flush.zero_()
+            ee[k][0].record(stream)
+            ctx.decide_host(model, h_inst, I, h_req, R, h_td, rnd.freq, rnd.tbt, h_level, h_status, stream)
+            ee[k][1].record(stream)
+        torch.cuda.synchronize(dev)
+        te = torch.tensor([sum(a.elapsed_time(b) for a, b in ee)], dtype=torch.float64, device=dev)
+        if world > 1:
+            dist.all_reduce(te, op=dist.ReduceOp.MAX)
+        ok = np.array_equal(h_level[:I].numpy(), dec[0, :I].cpu().numpy())
+        e2e = {"value": inst_all * ke / (float(te[0]) / 1e3), "unit": "decisions/s",
+               "h2d_bytes_per_step": int(I * 48 + R * 16 + R * 8), "d2h_bytes_per_step": int(I * 8),
+               "matches_device_path": bool(ok)}
+        ctx.free()
+
+    if rank != 0:
+        if world > 1:
+            dist.destroy_process_group()
+        return
+
+    peaks = measured_peaks()
+    smax = float(peaks.get("sm_max_mhz", 1965.0))
+    # K2 roofline: shared-memory load bandwidth, 128 B/clk/SM (B200_PROFILING / B300_MICROARCH
+    # LDS crossbar) x 148 SMs x max SM clock.  Algorithmic bytes per grid point: T*(D+1) 4-byte
+    # node/leaf words.
+    sms = torch.cuda.get_device_properties(dev).multi_processor_count
+    per_pt = info.n_trees * (info.depth + 1) * 4
+    k2_s = k_ms[1] / 1e3
+    achieved = grid * per_pt / k2_s / 1e9          # this rank's K2, GB/s
+    peak = sms * 128 * smax * 1e6 / 1e9
+    traffic = None
+    try:
+        with open(os.path.join(ROOT, "profiles", "k2_traffic.json")) as f:
+            tj = json.load(f)
+        if tj.get("workload") == cfg.name:
+            traffic = tj.get("dram_bytes_per_launch")
+    except (OSError, ValueError):
+        pass
+    roof = {"bound": "smem", "kernel": "k2_gbdt", "achieved": achieved, "peak": peak, "unit": "GB/s",
+            "frac": achieved / peak, "traffic": traffic,
+            "peak_basis": f"{sms} SMs x 128 B/clk (LDS) x sm_max_mhz {smax:.0f} (MEASURED_PEAKS.json clock)",
+            "frac_at_observed_clock": (achieved / (sms * 128 * clk["sm_mhz"] * 1e6 / 1e9)) if clk["sm_mhz"] else None,
+            "bytes_per_grid_point": per_pt, "grid_points_per_launch": grid, "padded_grid_points": padded}
+    cpu = None
+    if world == 1 and not args.no_cpu_baseline:
+        cpu = cpu_baseline(cfg, blob, inputs)
+    line = {
+        "metric": "frequency decisions/sec", "value": decisions_per_s, "unit": "decisions/s",
+        "n_gpus": world, "steps": args.steps, "warmup": max(args.warmup, 3), "ms_per_step": t_max_ms / args.steps,
+        "higher_is_better": True, "scaling": "strong" if cfg.name == "C5" else "weak", "vs_baseline": None,
+        "dtype": "f32", "data": "synthetic",
+        "config": {"workload": DESCR[cfg.name], "name": cfg.name, "instances_per_gpu": I,
+                   "global_instances": int(inst_all), "H": cfg.H, "F": cfg.F, "trees": info.n_trees,
+                   "depth": info.depth, "parallelism": f"instance-sharded x{world}" + (" + NCCL all-gather" if world > 1 else ""),
+                   "l2": "flushed between timed steps (256 MiB device write, untimed)"},
+        "grid_evals_per_sec": grid_per_s,
+        "per_kernel_ms": {"k1_project": k_ms[0], "k2_gbdt": k_ms[1], "k3_select": k_ms[2],
+                          "gather": k_ms[3]},
+        "roofline": roof,
+        "cpu_baseline": cpu,
+        "e2e": e2e,
+        "gpu_launches": 3 * args.steps,
+        "clocks": clk,
+        "paper_context": "paper controller on host CPU (A100 box): projection <2 ms, model ~3 ms per call, "
+                         "scheduler+throttle 35 ms per decision (P:466, P:495, P:557)",
+    }
+    print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+def dataclasses_replace(cfg, n_inst):
+    import dataclasses
+    return dataclasses.replace(cfg, n_inst=n_inst)
+
+
+if __name__ == "__main__":
+    main()

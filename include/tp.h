@@ -1,0 +1,216 @@
+/*
+ * tp.h -- C ABI of libtp: throttLL'eM's per-iteration GPU-frequency-selection hot path
+ * (arXiv 2408.05235, "SLO-aware GPU Frequency Scaling for Energy Efficient LLM Inference
+ * Serving"), implemented as hand-written sm_100a CUDA kernels.
+ *
+ * Citations: P:L = line L of the paper text; readings A-n of ambiguous passages are
+ * listed in DESIGN.md §3.
+ *
+ * The path, per serving instance (one LLM engine with its Scoreboard):
+ *   tp_project      K1  Eq. 1-2 projection of batch size B[m] and KV blocks KV[m] for the future
+ *                       iterations m = 1..H (m = 1 is the iteration about to run, reading A-1),
+ *                       with FIFO admission of queued requests by check 1 + batch cap.
+ *   tp_predict_ips  K2  the GBDT performance model M(tp, B[m], KV[m], f) -> IPS on
+ *                       the full (instance x frequency x iteration m <= n) grid.
+ *   tp_select_freq  K3  T' = 1/IPS, T_R = cumulative sum (Eq. 3), TBT check
+ *                        and Eq. 4 deadlines, lowest passing frequency.
+ *
+ * General conventions (all calls):
+ *   - Pointers marked [dev] are device pointers, [host] host pointers; all are owned by the
+ *     caller.  The library never frees caller memory; only tp_gbdt_load / tp_ctx_create allocate.
+ *   - Kernels are enqueued on `stream` (a cudaStream_t; NULL = legacy default stream) and the
+ *     call returns after enqueue.  No call allocates or synchronises except the two creators,
+ *     tp_gbdt_free / tp_ctx_free, and tp_decide_host (which only enqueues copies on `stream`).
+ *   - Host-detectable argument errors return TP_EINVAL and enqueue nothing: NULL pointers with
+ *     n_inst > 0, n_inst < 0, H outside [1, 16384], F outside [1, 32], non-finite, non-positive
+ *     or non-ascending frequencies, tbt_slo outside [2^-17, 16] s.
+ *   - Device-detected errors in ONE instance's data never fail the batch: the instance gets
+ *     status TP_ST_BAD_INPUT, level F-1, n = n_adm = 0 and zero curves.  Bad data is any of:
+ *     N < 1, tp < 1, tp >= 2^24, n_run < 0, n_queue < 0, kv_cap < 0, max_batch < 0,
+ *     req_begin < 0, req_begin + n_run + n_queue > n_req; any entry with a < 0, q < 1, r < 1,
+ *     a >= 2^24, q >= 2^24, or l = r - a outside [1, H] (reading A-3; l <= 0 is a length
+ *     overrun the caller fixes); a queued entry with a != 0; or a total footprint
+ *     sum_e ceil((a_e + l_e - 1 + q_e) / N) >= 2^24 (keeps KV exact as an fp32 feature).
+ *   - Launch failures return TP_ECUDA; malformed model blobs TP_EFORMAT.
+ *   - Calls on different streams may run concurrently; a tp_gbdt handle is immutable and may be
+ *     shared by any number of concurrent calls on its device.
+ */
+#ifndef TP_H
+#define TP_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define TP_ABI_VERSION 1
+
+/* ---- return codes ---- */
+enum {
+    TP_OK = 0,
+    TP_EINVAL = -1,   /* bad argument, nothing enqueued */
+    TP_ENOMEM = -2,   /* device / host allocation failed (creators only) */
+    TP_ECUDA = -3,    /* a CUDA call or launch failed */
+    TP_EFORMAT = -4,  /* malformed or unsupported model blob */
+    TP_ENOTIMPL = -5
+};
+
+/* ---- per-instance status bits (uint32, OR-ed) ---- */
+enum {
+    TP_ST_EMPTY = 1,          /* n = 0: nothing scheduled; level 0 (reading A-15) */
+    TP_ST_BYPASS_LOST = 2,    /* a "lost" request is scheduled -> max frequency */
+    TP_ST_INFEASIBLE = 4,     /* no level meets the SLOs -> level F-1 (reading A-14) */
+    TP_ST_KV_OVER = 8,        /* running requests alone exceed kv_cap somewhere */
+    TP_ST_QUEUE_BLOCKED = 16, /* a queued request failed check 1 / batch cap; FIFO stop */
+    TP_ST_IPS_CLAMPED = 32,   /* a model output was clamped to [2^-4, 2^17] (reading A-8) */
+    TP_ST_BAD_INPUT = 64      /* invalid instance data (see conventions) */
+};
+/* level precedence: BAD_INPUT (F-1) > EMPTY (0) > BYPASS_LOST (F-1) > lowest passing level >
+ * INFEASIBLE (F-1). */
+
+#define TP_REQ_LOST 1u        /* tp_req.flags bit 0: request marked "lost" */
+
+/* Instance header, 48 bytes, little-endian, 8-byte aligned.  One per serving instance. */
+typedef struct tp_inst {
+    int64_t k;          /* current iteration k (informational; requests carry a = k - s_i) */
+    double t_cur;       /* current time t_cur in seconds (Eq. 4) */
+    int32_t req_begin;  /* index of this instance's first request in the request array */
+    int32_t n_run;      /* running (scheduled) requests, stored first */
+    int32_t n_queue;    /* queued requests, stored next in FIFO order */
+    int32_t N;          /* tokens per KV block ("compile time parameter"; reading A-4) */
+    int32_t kv_cap;     /* KV-cache capacity in blocks (check 1) */
+    int32_t max_batch;  /* engine batch-size cap (admission reading A-2) */
+    int32_t tp;         /* engine size / tensor-parallel degree: model feature 0 */
+    int32_t _pad;       /* must be ignored */
+} tp_inst;
+
+/* Scoreboard entry, 16 bytes.  Running entries: a = k - s_i >= 0 iterations since it
+ * was scheduled; queued entries: a = 0 (virtual append at s = k).  q = |q_i| prompt
+ * tokens, r = r^_i predicted generation length (already conservatively adjusted).
+ * The entry completes at iteration s_i + r^_i, i.e. at l = r - a. */
+typedef struct tp_req {
+    int32_t a, q, r;
+    uint32_t flags;     /* bit 0: TP_REQ_LOST */
+} tp_req;
+
+typedef struct tp_gbdt tp_gbdt;   /* opaque, immutable model on one device */
+
+typedef struct tp_gbdt_info {
+    int32_t n_trees;      /* T */
+    int32_t depth;        /* D: trees are stored complete to this depth */
+    int32_t n_cuts[4];    /* distinct thresholds per feature [tp, batch, kv, freq] */
+    float base_score;
+    int32_t _pad;
+    int64_t device_bytes; /* bytes of device memory held by the handle */
+    int64_t node_bytes;   /* bytes of the node arrays (T * 2^(D+1) * 4) */
+} tp_gbdt_info;
+
+/*
+ * Model blob v1 (little-endian; host memory, caller keeps ownership):
+ *   char magic[4] = "TPGB"; u32 version = 1; u32 n_features = 4 (order [tp, batch, kv_blocks,
+ *   freq_mhz]); u32 n_trees; u32 max_depth (<= 12); f32 base_score;
+ *   per tree: u32 n_nodes (1..8192) then n_nodes x {i32 feature (-1 = leaf), f32 threshold,
+ *   i32 left, i32 right, f32 leaf_value}; node 0 is the root.
+ * Semantics (XGBoost convention, reading A-7): at a split go left iff
+ *   x[feature] < threshold; M(x) = base_score + sum over trees, in tree order, of the leaf
+ *   reached, accumulated in fp32 one tree at a time.
+ * Rejected with TP_EFORMAT: bad magic/version/size, a node index out of range, a cycle or a
+ * shared or unreachable node, depth > max_depth, feature outside [-1, 3], a non-finite
+ * threshold, a non-finite leaf or |leaf| > 2^60, a non-finite base, or more than 32767 distinct
+ * thresholds on one feature.
+ * tp_gbdt_load copies the normalised model to `device` (synchronously) and returns a handle.
+ */
+int tp_gbdt_load(const void* host_blob, size_t nbytes, int device, tp_gbdt** out);
+int tp_gbdt_free(tp_gbdt* m);
+int tp_gbdt_get_info(const tp_gbdt* m, tp_gbdt_info* out);
+
+/*
+ * K1 -- projection (Eq. 1-2) and FIFO admission (check 1 + batch cap, P:506-507,
+ * P:755; reading A-2).
+ *   inst    [dev] n_inst headers.            req  [dev] n_req entries (running then queued
+ *                                                 per instance, at inst.req_begin).
+ *   B, KV   [dev] out, int32 [n_inst][H]: B[i][m-1] = number of scheduled requests active at
+ *           iteration m, KV[i][m-1] = sum of their Eq. 1 block counts
+ *           ceil((a + m - 1 + q) / N) (0 beyond each request's l); zero for m > n.
+ *           "Scheduled" = running + admitted queued.
+ *   n       [dev] out, int32 [n_inst]: horizon = max l over scheduled requests (0 if none).
+ *   n_adm   [dev] out, int32 [n_inst]: queued requests admitted (a FIFO prefix).
+ *   status  [dev] out, uint32 [n_inst]: written (not OR-ed) with BAD_INPUT, EMPTY,
+ *           BYPASS_LOST, KV_OVER, QUEUE_BLOCKED.
+ * Admission: queued c (in order) is admitted iff B[1] + 1 <= max_batch and
+ *   max_m (KV[m] + ceil((m - 1 + q_c) / N) [m <= r_c]) <= kv_cap; the first failure stops the
+ *   queue and sets QUEUE_BLOCKED.
+ */
+int tp_project(const tp_inst* inst, int32_t n_inst, const tp_req* req, int32_t n_req, int32_t H,
+               int32_t* B, int32_t* KV, int32_t* n, int32_t* n_adm, uint32_t* status, void* stream);
+
+/*
+ * K2 -- GBDT IPS model on the grid.  For every instance i not flagged
+ * BAD_INPUT / EMPTY / BYPASS_LOST in status[i], every level u < F and every m = 1..n[i]:
+ *   raw = M(tp_i, B[i][m-1], KV[i][m-1], freq_mhz[u])      (features as fp32)
+ *   ips[(i*F + u)*H + m-1] = clamp(raw)  with NaN -> 2^-4, then [2^-4, 2^17] (reading A-8),
+ * OR-ing TP_ST_IPS_CLAMPED into status[i] if any value was changed by the clamp.
+ * Entries with m > n[i] and skipped instances are not written.
+ *   freq_mhz [host] F levels, strictly ascending, finite, > 0 (reading A-19).
+ *   ips      [dev] out, fp32 [n_inst][F][H].
+ */
+int tp_predict_ips(const tp_gbdt* m, const tp_inst* inst, int32_t n_inst, const int32_t* B,
+                   const int32_t* KV, const int32_t* n, int32_t H, const float* freq_mhz, int32_t F,
+                   float* ips, uint32_t* status, void* stream);
+
+/*
+ * K3 -- SLO scan and frequency choice (Eq. 3-4; throttle P:550-557).
+ * For each instance not flagged BAD_INPUT / EMPTY / BYPASS_LOST and each level u:
+ *   T'[m] = fl32(1 / ips[m])                                       (reading A-9)
+ *   T_R[l] = sum_{m <= l} T'[m], exactly, as int64 ticks of 2^-40 s  (Eq. 3, reading A-10)
+ *   pass_u = T_R[n] <= n * tbt_slo                                  (TBT, tie passes)
+ *            and T_R[l_j] < fl64(t_dead_j - t_cur) for every scheduled request j
+ *                                                                   (Eq. 4 strict, A-12)
+ *   level[i] = min{u : pass_u}, else F-1 with INFEASIBLE.  BAD_INPUT -> F-1, EMPTY -> 0,
+ *   BYPASS_LOST -> F-1.
+ *   req, t_dead [dev] the same request array as tp_project; t_dead fp64 seconds per entry.
+ *   n, n_adm    [dev] from tp_project.   ips [dev] from tp_predict_ips.
+ *   level       [dev] out, int32 [n_inst], an index into the frequency list.
+ *   status      [dev] in/out: INFEASIBLE is OR-ed in.
+ *   tr_ticks    [dev] optional out, int64 [n_inst][F][H] (m <= n, evaluated instances), or NULL.
+ */
+int tp_select_freq(const tp_inst* inst, int32_t n_inst, const tp_req* req, int32_t n_req,
+                   const double* t_dead, const int32_t* n, const int32_t* n_adm, const float* ips,
+                   int32_t H, int32_t F, float tbt_slo, int32_t* level, uint32_t* status,
+                   int64_t* tr_ticks, void* stream);
+
+/*
+ * Convenience: one decision round with library-owned scratch.
+ * tp_ctx_create allocates, on `device`, B/KV/n/n_adm (n_inst_max x H), the ips grid
+ * (n_inst_max x F_max x H) and staging for up to n_req_max requests.
+ */
+typedef struct tp_ctx tp_ctx;
+int tp_ctx_create(int device, int32_t n_inst_max, int32_t n_req_max, int32_t H, int32_t F_max,
+                  tp_ctx** out);
+int tp_ctx_free(tp_ctx* c);
+
+/* K1 -> K2 -> K3 on device-resident inputs; level/status [dev] out. */
+int tp_decide(tp_ctx* c, const tp_gbdt* m, const tp_inst* inst, int32_t n_inst, const tp_req* req,
+              int32_t n_req, const double* t_dead, const float* freq_mhz, int32_t F, float tbt_slo,
+              int32_t* level, uint32_t* status, void* stream);
+
+/* Same with HOST inputs/outputs: enqueues host->device copies of inst/req/t_dead, the three
+ * kernels and device->host copies of level/status, all on `stream`.  Outputs are valid after
+ * the stream is synchronised.  Use pinned host memory for asynchronous copies. */
+int tp_decide_host(tp_ctx* c, const tp_gbdt* m, const tp_inst* h_inst, int32_t n_inst,
+                   const tp_req* h_req, int32_t n_req, const double* h_t_dead,
+                   const float* freq_mhz, int32_t F, float tbt_slo, int32_t* h_level,
+                   uint32_t* h_status, void* stream);
+
+/* Device pointers of the context's scratch (for inspection / tests); any out may be NULL. */
+int tp_ctx_buffers(tp_ctx* c, int32_t** B, int32_t** KV, int32_t** n, int32_t** n_adm, float** ips);
+
+const char* tp_strerror(int code);
+int tp_abi_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* TP_H */

@@ -1,0 +1,189 @@
+// libtp C ABI entry points (include/tp.h): host-side argument validation and launches.
+#include <cmath>
+#include <cstring>
+#include <new>
+
+#include "tp_internal.cuh"
+
+namespace {
+
+bool freq_ok(const float* f, int32_t F) {
+    if (!f || F < 1 || F > tp::kMaxF) return false;
+    for (int u = 0; u < F; ++u) {
+        if (!std::isfinite(f[u]) || !(f[u] > 0.f)) return false;
+        if (u > 0 && !(f[u] > f[u - 1])) return false;
+    }
+    return true;
+}
+
+bool tbt_ok(float t) { return t >= 0x1p-17f && t <= 16.0f; }
+
+bool H_ok(int32_t H) { return H >= 1 && H <= tp::kMaxH; }
+
+cudaStream_t S(void* s) { return reinterpret_cast<cudaStream_t>(s); }
+
+}  // namespace
+
+struct tp_ctx {
+    int device;
+    int32_t n_inst_max, n_req_max, H, F_max;
+    int32_t *B, *KV, *n, *n_adm, *level;
+    uint32_t* status;
+    float* ips;
+    tp_inst* inst;
+    tp_req* req;
+    double* t_dead;
+};
+
+extern "C" {
+
+const char* tp_strerror(int code) {
+    switch (code) {
+        case TP_OK: return "ok";
+        case TP_EINVAL: return "invalid argument";
+        case TP_ENOMEM: return "out of memory";
+        case TP_ECUDA: return "CUDA error";
+        case TP_EFORMAT: return "malformed or unsupported model blob";
+        case TP_ENOTIMPL: return "not implemented";
+        default: return "unknown error";
+    }
+}
+
+int tp_abi_version(void) { return TP_ABI_VERSION; }
+
+int tp_project(const tp_inst* inst, int32_t n_inst, const tp_req* req, int32_t n_req, int32_t H, int32_t* B,
+               int32_t* KV, int32_t* n, int32_t* n_adm, uint32_t* status, void* stream) {
+    if (n_inst < 0 || n_req < 0 || !H_ok(H)) return TP_EINVAL;
+    if (n_inst > 0 && (!inst || !B || !KV || !n || !n_adm || !status || (n_req > 0 && !req))) return TP_EINVAL;
+    return tp::launch_project(inst, n_inst, req, n_req, H, B, KV, n, n_adm, status, S(stream));
+}
+
+int tp_predict_ips(const tp_gbdt* m, const tp_inst* inst, int32_t n_inst, const int32_t* B, const int32_t* KV,
+                   const int32_t* n, int32_t H, const float* freq_mhz, int32_t F, float* ips, uint32_t* status,
+                   void* stream) {
+    if (!m || n_inst < 0 || !H_ok(H) || !freq_ok(freq_mhz, F)) return TP_EINVAL;
+    if (n_inst > 0 && (!inst || !B || !KV || !n || !ips || !status)) return TP_EINVAL;
+    tp::K2Params p;
+    std::memset(&p, 0, sizeof(p));
+    p.words = m->m.d_words;
+    p.cuts = m->m.d_cuts;
+    for (int f = 0; f < 5; ++f) p.cut_off[f] = m->m.cut_off[f];
+    p.n_trees = m->m.n_trees;
+    p.depth = m->m.depth;
+    p.base = m->m.base;
+    p.inst = inst;
+    p.B = B;
+    p.KV = KV;
+    p.n = n;
+    p.status = status;
+    p.ips = ips;
+    p.n_inst = n_inst;
+    p.H = H;
+    p.F = F;
+    for (int u = 0; u < F; ++u) p.freq[u] = freq_mhz[u];
+    return tp::launch_gbdt(p, S(stream));
+}
+
+int tp_select_freq(const tp_inst* inst, int32_t n_inst, const tp_req* req, int32_t n_req, const double* t_dead,
+                   const int32_t* n, const int32_t* n_adm, const float* ips, int32_t H, int32_t F, float tbt_slo,
+                   int32_t* level, uint32_t* status, int64_t* tr_ticks, void* stream) {
+    if (n_inst < 0 || n_req < 0 || !H_ok(H) || F < 1 || F > tp::kMaxF || !tbt_ok(tbt_slo)) return TP_EINVAL;
+    if (n_inst > 0 && (!inst || !n || !n_adm || !ips || !level || !status || (n_req > 0 && (!req || !t_dead))))
+        return TP_EINVAL;
+    const int64_t tbt_ticks = (int64_t)((double)tbt_slo * 0x1p40);   // exact: tbt_slo >= 2^-17
+    return tp::launch_select(inst, n_inst, req, n_req, t_dead, n, n_adm, ips, H, F, tbt_ticks, level, status,
+                             tr_ticks, S(stream));
+}
+
+int tp_ctx_create(int device, int32_t n_inst_max, int32_t n_req_max, int32_t H, int32_t F_max, tp_ctx** out) {
+    if (!out || n_inst_max < 0 || n_req_max < 0 || !H_ok(H) || F_max < 1 || F_max > tp::kMaxF) return TP_EINVAL;
+    *out = nullptr;
+    tp_ctx* c = new (std::nothrow) tp_ctx();
+    if (!c) return TP_ENOMEM;
+    std::memset(c, 0, sizeof(*c));
+    c->device = device;
+    c->n_inst_max = n_inst_max;
+    c->n_req_max = n_req_max;
+    c->H = H;
+    c->F_max = F_max;
+    int prev = 0;
+    cudaGetDevice(&prev);
+    if (cudaSetDevice(device) != cudaSuccess) {
+        delete c;
+        return TP_ECUDA;
+    }
+    const size_t I = (size_t)(n_inst_max > 0 ? n_inst_max : 1), R = (size_t)(n_req_max > 0 ? n_req_max : 1);
+    bool ok = cudaMalloc(&c->B, I * H * 4) == cudaSuccess && cudaMalloc(&c->KV, I * H * 4) == cudaSuccess &&
+              cudaMalloc(&c->n, I * 4) == cudaSuccess && cudaMalloc(&c->n_adm, I * 4) == cudaSuccess &&
+              cudaMalloc(&c->level, I * 4) == cudaSuccess && cudaMalloc(&c->status, I * 4) == cudaSuccess &&
+              cudaMalloc(&c->ips, I * F_max * H * 4) == cudaSuccess &&
+              cudaMalloc(&c->inst, I * sizeof(tp_inst)) == cudaSuccess &&
+              cudaMalloc(&c->req, R * sizeof(tp_req)) == cudaSuccess &&
+              cudaMalloc(&c->t_dead, R * sizeof(double)) == cudaSuccess;
+    cudaSetDevice(prev);
+    if (!ok) {
+        tp_ctx_free(c);
+        return TP_ENOMEM;
+    }
+    *out = c;
+    return TP_OK;
+}
+
+int tp_ctx_free(tp_ctx* c) {
+    if (!c) return TP_OK;
+    int prev = 0;
+    cudaGetDevice(&prev);
+    cudaSetDevice(c->device);
+    void* ptrs[] = {c->B, c->KV, c->n, c->n_adm, c->level, c->status, c->ips, c->inst, c->req, c->t_dead};
+    for (void* p : ptrs)
+        if (p) cudaFree(p);
+    cudaSetDevice(prev);
+    delete c;
+    return TP_OK;
+}
+
+int tp_ctx_buffers(tp_ctx* c, int32_t** B, int32_t** KV, int32_t** n, int32_t** n_adm, float** ips) {
+    if (!c) return TP_EINVAL;
+    if (B) *B = c->B;
+    if (KV) *KV = c->KV;
+    if (n) *n = c->n;
+    if (n_adm) *n_adm = c->n_adm;
+    if (ips) *ips = c->ips;
+    return TP_OK;
+}
+
+int tp_decide(tp_ctx* c, const tp_gbdt* m, const tp_inst* inst, int32_t n_inst, const tp_req* req, int32_t n_req,
+              const double* t_dead, const float* freq_mhz, int32_t F, float tbt_slo, int32_t* level,
+              uint32_t* status, void* stream) {
+    if (!c || !m || n_inst < 0 || n_inst > c->n_inst_max || F > c->F_max || !freq_ok(freq_mhz, F) ||
+        !tbt_ok(tbt_slo))
+        return TP_EINVAL;
+    int rc = tp_project(inst, n_inst, req, n_req, c->H, c->B, c->KV, c->n, c->n_adm, status, stream);
+    if (rc) return rc;
+    rc = tp_predict_ips(m, inst, n_inst, c->B, c->KV, c->n, c->H, freq_mhz, F, c->ips, status, stream);
+    if (rc) return rc;
+    return tp_select_freq(inst, n_inst, req, n_req, t_dead, c->n, c->n_adm, c->ips, c->H, F, tbt_slo, level, status,
+                          nullptr, stream);
+}
+
+int tp_decide_host(tp_ctx* c, const tp_gbdt* m, const tp_inst* h_inst, int32_t n_inst, const tp_req* h_req,
+                   int32_t n_req, const double* h_t_dead, const float* freq_mhz, int32_t F, float tbt_slo,
+                   int32_t* h_level, uint32_t* h_status, void* stream) {
+    if (!c || !m || n_inst < 0 || n_inst > c->n_inst_max || n_req < 0 || n_req > c->n_req_max) return TP_EINVAL;
+    if (n_inst > 0 && (!h_inst || !h_level || !h_status || (n_req > 0 && (!h_req || !h_t_dead)))) return TP_EINVAL;
+    if (!freq_ok(freq_mhz, F) || F > c->F_max || !tbt_ok(tbt_slo)) return TP_EINVAL;
+    cudaStream_t s = S(stream);
+    if (cudaMemcpyAsync(c->inst, h_inst, (size_t)n_inst * sizeof(tp_inst), cudaMemcpyHostToDevice, s) ||
+        cudaMemcpyAsync(c->req, h_req, (size_t)n_req * sizeof(tp_req), cudaMemcpyHostToDevice, s) ||
+        cudaMemcpyAsync(c->t_dead, h_t_dead, (size_t)n_req * sizeof(double), cudaMemcpyHostToDevice, s))
+        return TP_ECUDA;
+    int rc = tp_decide(c, m, c->inst, n_inst, c->req, n_req, c->t_dead, freq_mhz, F, tbt_slo, c->level, c->status,
+                       stream);
+    if (rc) return rc;
+    if (cudaMemcpyAsync(h_level, c->level, (size_t)n_inst * 4, cudaMemcpyDeviceToHost, s) ||
+        cudaMemcpyAsync(h_status, c->status, (size_t)n_inst * 4, cudaMemcpyDeviceToHost, s))
+        return TP_ECUDA;
+    return TP_OK;
+}
+
+}  // extern "C"

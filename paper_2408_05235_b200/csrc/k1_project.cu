@@ -1,0 +1,213 @@
+// K1 -- KV usage & batch-size projection (PAPER §4.2, Eq. 1-2) with the FIFO
+// admission gate (check 1 + batch cap, §4.3.2, one request at a time P:755).
+//
+// One CTA per instance.  Instead of evaluating Eq. 1 for every (request, m) pair, every request
+// contributes O(l/N) integer events to two difference arrays in shared memory:
+//   B : +1 at m = 1, -1 at m = l + 1
+//   KV: +ceil((a + q) / N) at m = 1, +1 at every m in [2, l] where the request's token count
+//       a + q + m - 1 crosses a block boundary ((a + q + m - 2) % N == 0), and -ceil((a+q+l-1)/N)
+//       at m = l + 1
+// and a block-wide inclusive scan turns them into B[m], KV[m] (equal to Eq. 1-2 exactly; pinned by
+// tests/test_gpu_parity.py against the oracle's direct Eq. 1 sums).  HBM traffic: 16 B per request
+// read + 8 B per (instance, m <= H) written.
+#include "tp_internal.cuh"
+
+namespace tp {
+namespace {
+
+constexpr int kThreads = 256;
+constexpr int kWarps = kThreads / 32;
+
+__device__ __forceinline__ int64_t block_sum64(int64_t v, int64_t* red) {
+    for (int o = 16; o; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
+    __syncthreads();
+    if (l == 0) red[w] = v;
+    __syncthreads();
+    int64_t s = 0;
+#pragma unroll
+    for (int i = 0; i < kWarps; ++i) s += red[i];
+    return s;
+}
+
+__device__ __forceinline__ int block_max(int v, int* red) {
+    v = __reduce_max_sync(0xffffffffu, v);
+    const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
+    __syncthreads();
+    if (l == 0) red[w] = v;
+    __syncthreads();
+    int s = red[0];
+#pragma unroll
+    for (int i = 1; i < kWarps; ++i) s = max(s, red[i]);
+    return s;
+}
+
+__global__ void __launch_bounds__(kThreads)
+k1_project(const tp_inst* __restrict__ inst, const int4* __restrict__ req, int32_t n_req, int32_t H,
+           int32_t* __restrict__ Bout, int32_t* __restrict__ KVout, int32_t* __restrict__ nout,
+           int32_t* __restrict__ nadm_out, uint32_t* __restrict__ status) {
+    extern __shared__ int smem[];
+    int* sB = smem;               // index m in [1, H + 1]
+    int* sKV = smem + (H + 2);
+    __shared__ int64_t red64[kWarps];
+    __shared__ int redi[kWarps];
+    __shared__ int s_admit;
+
+    const int i = blockIdx.x;
+    const int tid = threadIdx.x;
+    const tp_inst in = inst[i];
+    const int64_t rb = in.req_begin;
+    const int nr = in.n_run, nq = in.n_queue, N = in.N;
+
+    for (int m = tid; m < H + 2; m += kThreads) sB[m] = sKV[m] = 0;
+
+    // ---- validation (include/tp.h conventions) ----
+    bool bad = N < 1 || in.tp < 1 || (int64_t)in.tp >= kFeatLimit || nr < 0 || nq < 0 || in.kv_cap < 0 ||
+               in.max_batch < 0 || rb < 0 || rb + (int64_t)nr + nq > (int64_t)n_req;
+    int64_t foot = 0;
+    if (!bad) {
+        for (int e = tid; e < nr + nq; e += kThreads) {
+            const int4 r = __ldg(&req[rb + e]);
+            const int64_t l = (int64_t)r.z - r.x;
+            const bool eb = r.x < 0 || r.y < 1 || r.z < 1 || r.x >= kFeatLimit || r.y >= kFeatLimit || l < 1 ||
+                            l > H || (e >= nr && r.x != 0);
+            bad |= eb;
+            if (!eb) foot += ((int64_t)r.x + l - 1 + r.y + N - 1) / N;
+        }
+    }
+    bad = __syncthreads_or(bad);
+    if (!bad) bad = block_sum64(foot, red64) >= kFeatLimit;
+    if (bad) {
+        for (int m = tid; m < H; m += kThreads) {
+            Bout[(int64_t)i * H + m] = 0;
+            KVout[(int64_t)i * H + m] = 0;
+        }
+        if (tid == 0) {
+            nout[i] = 0;
+            nadm_out[i] = 0;
+            status[i] = TP_ST_BAD_INPUT;
+        }
+        return;
+    }
+
+    // ---- running requests -> event histograms (Eq. 1 increments) ----
+    int nloc = 0;
+    bool lost = false;
+    for (int e = tid; e < nr; e += kThreads) {
+        const int4 r = __ldg(&req[rb + e]);
+        const int a = r.x, q = r.y, l = r.z - r.x;
+        nloc = max(nloc, l);
+        lost |= (r.w & TP_REQ_LOST) != 0;
+        const int aq = a + q;
+        atomicAdd(&sB[1], 1);
+        atomicAdd(&sB[l + 1], -1);
+        atomicAdd(&sKV[1], (aq - 1) / N + 1);                           // ceil(aq / N), aq >= 1
+        for (int64_t m = 2 + (int64_t)((N - aq % N) % N); m <= l; m += N) atomicAdd(&sKV[m], 1);
+        atomicAdd(&sKV[l + 1], -((aq + l - 2) / N + 1));                // -ceil((aq + l - 1) / N)
+    }
+    lost = __syncthreads_or(lost);
+
+    // ---- inclusive scans: thread t owns the contiguous segment [lo, hi) of m ----
+    const int S = (H + kThreads - 1) / kThreads;
+    const int lo = 1 + tid * S, hi = min(lo + S, H + 1);
+    {
+        int sb = 0, skv = 0;
+        for (int m = lo; m < hi; ++m) {
+            sb += sB[m];
+            skv += sKV[m];
+        }
+        // exclusive block scan of the (sb, skv) pairs
+        int xb = sb, xkv = skv;
+        const int lane = tid & 31, w = tid >> 5;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const int yb = __shfl_up_sync(0xffffffffu, xb, o), ykv = __shfl_up_sync(0xffffffffu, xkv, o);
+            if (lane >= o) {
+                xb += yb;
+                xkv += ykv;
+            }
+        }
+        __shared__ int wb[kWarps], wkv[kWarps];
+        if (lane == 31) {
+            wb[w] = xb;
+            wkv[w] = xkv;
+        }
+        __syncthreads();
+        int pb = xb - sb, pkv = xkv - skv;
+        for (int k = 0; k < w; ++k) {
+            pb += wb[k];
+            pkv += wkv[k];
+        }
+        for (int m = lo; m < hi; ++m) {
+            pb += sB[m];
+            pkv += sKV[m];
+            sB[m] = pb;
+            sKV[m] = pkv;
+        }
+    }
+    __syncthreads();
+
+    int kvmax = 0;
+    for (int m = lo; m < hi; ++m) kvmax = max(kvmax, sKV[m]);
+    uint32_t st = block_max(kvmax, redi) > in.kv_cap ? TP_ST_KV_OVER : 0u;
+
+    // ---- FIFO gate: queued c admitted iff B[1]+1 <= max_batch and max_m KV + KV_c <= kv_cap ----
+    int n_adm = 0;
+    for (int c = 0; c < nq; ++c) {
+        const int4 r = __ldg(&req[rb + nr + c]);
+        const int q = r.y, lc = r.z;
+        int mx = 0;
+        for (int m = lo; m < hi; ++m) mx = max(mx, sKV[m] + (m <= lc ? (m + q - 2) / N + 1 : 0));
+        mx = block_max(mx, redi);
+        if (tid == 0) s_admit = (sB[1] + 1 <= in.max_batch) && (mx <= in.kv_cap);
+        __syncthreads();
+        const int admit = s_admit;
+        if (!admit) {
+            st |= TP_ST_QUEUE_BLOCKED;
+            break;
+        }
+        for (int m = lo; m < min(hi, lc + 1); ++m) {
+            sKV[m] += (m + q - 2) / N + 1;
+            sB[m] += 1;
+        }
+        nloc = max(nloc, lc);
+        lost |= (r.w & TP_REQ_LOST) != 0;
+        ++n_adm;
+        __syncthreads();
+    }
+    const int n = block_max(nloc, redi);
+
+    for (int m = tid; m < H; m += kThreads) {
+        Bout[(int64_t)i * H + m] = sB[m + 1];
+        KVout[(int64_t)i * H + m] = sKV[m + 1];
+    }
+    if (tid == 0) {
+        if (n == 0) st |= TP_ST_EMPTY;
+        else if (lost) st |= TP_ST_BYPASS_LOST;
+        nout[i] = n;
+        nadm_out[i] = n_adm;
+        status[i] = st;
+    }
+}
+
+}  // namespace
+
+int launch_project(const tp_inst* inst, int32_t n_inst, const tp_req* req, int32_t n_req, int32_t H,
+                   int32_t* B, int32_t* KV, int32_t* n, int32_t* n_adm, uint32_t* status, cudaStream_t s) {
+    if (n_inst == 0) return TP_OK;
+    const size_t smem = (size_t)2 * (H + 2) * sizeof(int);
+    int dev = 0;
+    if (cudaGetDevice(&dev) != cudaSuccess) return TP_ECUDA;
+    static bool attr_done[64] = {};
+    if (dev < 64 && !attr_done[dev]) {
+        if (cudaFuncSetAttribute(k1_project, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 2 * (kMaxH + 2) * (int)sizeof(int)) != cudaSuccess)
+            return TP_ECUDA;
+        attr_done[dev] = true;
+    }
+    k1_project<<<n_inst, kThreads, smem, s>>>(inst, reinterpret_cast<const int4*>(req), n_req, H, B, KV, n,
+                                                n_adm, status);
+    return cudaPeekAtLastError() == cudaSuccess ? TP_OK : TP_ECUDA;
+}
+
+}  // namespace tp

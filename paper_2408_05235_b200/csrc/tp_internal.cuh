@@ -1,0 +1,69 @@
+// Internal declarations shared by libtp's translation units (not part of the C ABI).
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "tp.h"
+
+namespace tp {
+
+constexpr int kMaxF = 32;
+constexpr int kMaxH = 16384;
+constexpr int kMaxDepth = 12;
+constexpr int kMaxCuts = 32767;            // ranks must fit 15 bits (K2 word encoding)
+constexpr int64_t kFeatLimit = 1LL << 24;  // integer features exact in fp32
+
+// Device-resident, normalised ensemble (built by tp_gbdt_load, model.cu).
+//
+// Node words: tree t occupies words[t * (2 << D) .. (t + 1) * (2 << D)), a complete binary heap
+// with 1-based index: internal node idx in [1, 2^D), leaf idx in [2^D, 2^(D+1)), children of idx at
+// 2*idx (left, x < thr) and 2*idx + 1.  word 0 is unused.
+//   internal word = ((0xFFFF - j) << 16) | sel(f)
+//     f   = split feature, j = index of the threshold among feature f's sorted distinct cuts;
+//     sel = PRMT selector moving rank_f (16 bits at byte 2f of the 8-byte feature pair) into the
+//           upper half: bytes (b1, b1, b0, b1) with b0 = 2f, b1 = 2f + 1.
+//     K2 computes r = prmt(xlo, xhi, word) = rank_f << 16 | junk (junk <= 0x7F7F) and
+//     go_right = carry_out(r + word)  <=>  rank_f + 0xFFFF - j >= 0x10000  <=>  rank_f > j
+//                                      <=>  x_f >= cut_j  (rank = #cuts <= x).
+//   leaf word = bit pattern of the fp32 leaf value.
+// Shallow leaves are replicated down to depth D (exactly equivalent).
+struct Model {
+    int device = 0;
+    int32_t n_trees = 0, depth = 0;
+    float base = 0.f;
+    int32_t n_cuts[4] = {0, 0, 0, 0};
+    uint32_t* d_words = nullptr;   // n_trees * (2 << depth)
+    float* d_cuts = nullptr;       // concatenated sorted cuts, feature order
+    int32_t cut_off[5] = {0, 0, 0, 0, 0};
+    int64_t device_bytes = 0;
+};
+
+struct K2Params {
+    const uint32_t* words;
+    const float* cuts;
+    int32_t cut_off[5];
+    int32_t n_trees, depth;
+    float base;
+    const tp_inst* inst;
+    const int32_t* B;
+    const int32_t* KV;
+    const int32_t* n;
+    uint32_t* status;
+    float* ips;
+    int32_t n_inst, H, F;
+    float freq[kMaxF];
+};
+
+int launch_project(const tp_inst* inst, int32_t n_inst, const tp_req* req, int32_t n_req, int32_t H,
+                   int32_t* B, int32_t* KV, int32_t* n, int32_t* n_adm, uint32_t* status, cudaStream_t s);
+int launch_gbdt(const K2Params& p, cudaStream_t s);
+int launch_select(const tp_inst* inst, int32_t n_inst, const tp_req* req, int32_t n_req, const double* t_dead,
+                  const int32_t* n, const int32_t* n_adm, const float* ips, int32_t H, int32_t F,
+                  int64_t tbt_ticks, int32_t* level, uint32_t* status, int64_t* tr, cudaStream_t s);
+
+}  // namespace tp
+
+struct tp_gbdt {
+    tp::Model m;
+};

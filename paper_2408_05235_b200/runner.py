@@ -1,0 +1,74 @@
+"""Device-memory plumbing around the C ABI: upload a round's inputs once, run K1 -> K2 -> K3.
+
+torch provides device memory and streams only; all arithmetic happens in libtp's kernels.
+"""
+from __future__ import annotations
+
+import numpy as np
+import torch
+
+from . import tp
+from . import workload as W
+
+
+def to_device_bytes(a: np.ndarray, device) -> torch.Tensor:
+    """A structured / plain numpy array as a raw uint8 device tensor (same bytes)."""
+    a = np.ascontiguousarray(a)
+    t = torch.from_numpy(a.view(np.uint8).reshape(-1)) if a.size else torch.zeros(16, dtype=torch.uint8)
+    return t.to(device)
+
+
+class Round:
+    """One decision round's device buffers (inputs + K1/K2/K3 outputs)."""
+
+    def __init__(self, inputs: dict, device="cuda:0", want_tr=False):
+        dev = torch.device(device)
+        self.device = dev
+        inst, req, t_dead = inputs["inst"], inputs["req"], inputs["t_dead"]
+        self.I, self.R, self.H = len(inst), len(req), int(inputs["H"])
+        self.freq = np.asarray(inputs["freq"], dtype=np.float32)
+        self.F = len(self.freq)
+        self.tbt = np.float32(inputs["tbt_slo"])
+        assert inst.dtype == W.INST_DTYPE and req.dtype == W.REQ_DTYPE
+        self.inst = to_device_bytes(inst, dev)
+        self.req = to_device_bytes(req, dev)
+        self.t_dead = torch.from_numpy(np.ascontiguousarray(t_dead, np.float64)).to(dev) if self.R else \
+            torch.zeros(1, dtype=torch.float64, device=dev)
+        I, H, F = max(self.I, 1), self.H, self.F
+        self.B = torch.empty((I, H), dtype=torch.int32, device=dev)
+        self.KV = torch.empty((I, H), dtype=torch.int32, device=dev)
+        self.n = torch.empty(I, dtype=torch.int32, device=dev)
+        self.n_adm = torch.empty(I, dtype=torch.int32, device=dev)
+        self.status = torch.empty(I, dtype=torch.int32, device=dev)
+        self.level = torch.empty(I, dtype=torch.int32, device=dev)
+        self.ips = torch.zeros((I, F, H), dtype=torch.float32, device=dev)
+        self.tr = torch.zeros((I, F, H), dtype=torch.int64, device=dev) if want_tr else None
+
+    def project(self, stream=None):
+        tp.tp_project(self.inst, self.I, self.req, self.R, self.H, self.B, self.KV, self.n, self.n_adm, self.status,
+                      stream)
+
+    def predict(self, model, stream=None):
+        tp.tp_predict_ips(model, self.inst, self.I, self.B, self.KV, self.n, self.H, self.freq, self.ips, self.status,
+                          stream)
+
+    def select(self, stream=None):
+        tp.tp_select_freq(self.inst, self.I, self.req, self.R, self.t_dead, self.n, self.n_adm, self.ips, self.H,
+                          self.F, self.tbt, self.level, self.status, self.tr, stream)
+
+    def run(self, model, stream=None):
+        self.project(stream)
+        self.predict(model, stream)
+        self.select(stream)
+
+    def results(self, idx=None) -> dict:
+        """Outputs copied to the host; ``idx`` selects instances (all by default, rows in idx order)."""
+        torch.cuda.synchronize(self.device)
+        I = self.I
+        sel = slice(0, I) if idx is None else torch.as_tensor(np.asarray(idx), device=self.device, dtype=torch.long)
+        get = lambda t: t[sel].cpu().numpy()   # noqa: E731
+        out = dict(B=get(self.B), KV=get(self.KV), n=get(self.n), n_adm=get(self.n_adm),
+                   status=get(self.status).view(np.uint32), level=get(self.level), ips=get(self.ips))
+        if self.tr is not None:
+            out["tr"] = get(self.tr)
+        return out

@@ -1,0 +1,265 @@
+"""GPU parity: the CUDA path (through the C ABI) vs the CPU oracle, element by element.
+
+Bar: B, KV, n, n_adm, status, level bit-exact (integer work); ips bit-exact (the
+kernel forms the same fp32 sums in the same tree order; north_star's 1e-5 relative tolerance is
+therefore met with margin 0); T_R ticks bit-exact (exact integer sums).
+"""
+from __future__ import annotations
+
+import dataclasses
+
+import numpy as np
+import pytest
+
+import cases
+from paper_2408_05235_b200 import workload as W
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+SKIP = 64 | 1 | 2   # BAD_INPUT | EMPTY | BYPASS_LOST: no grid evaluated
+
+
+@pytest.fixture(scope="module")
+def gpu():
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    import __graft_entry__
+    __graft_entry__.build_lib()
+    from paper_2408_05235_b200 import runner, tp
+    return tp, runner
+
+
+def run_gpu(gpu, blob, inputs, want_tr=True, idx=None):
+    tp, runner = gpu
+    model = tp.Gbdt(blob, 0)
+    r = runner.Round(inputs, "cuda:0", want_tr=want_tr)
+    r.run(model)
+    out = r.results(idx)
+    del r
+    model.free()
+    return out
+
+
+def run_oracle(oracle_mod, blob, inputs, want_tr=True, threads=8, want_grid=True):
+    return oracle_mod.decide(oracle_mod.Model(blob), inputs["inst"], inputs["req"], inputs["t_dead"], inputs["H"],
+                             inputs["freq"], inputs["tbt_slo"], want_grid=want_grid, want_tr=want_tr, threads=threads)
+
+
+def assert_parity(got, ref, idx=None, grid=True, tr=True, compact=False):
+    """ref: oracle outputs for instances idx (default all); got: GPU outputs for all instances,
+    or (compact) only for idx, in idx order."""
+    idx = np.arange(len(ref["level"])) if idx is None or compact else np.asarray(idx)
+    for k in ["level", "n", "n_adm"]:
+        assert np.array_equal(got[k][idx].astype(np.int64), ref[k].astype(np.int64)), k
+    assert np.array_equal(got["status"][idx].astype(np.uint32), ref["status"].astype(np.uint32)), "status"
+    for k in ["B", "KV"]:
+        if k in ref:
+            assert np.array_equal(got[k][idx], ref[k]), k
+    if grid and "ips" in ref:
+        for j, i in enumerate(idx):
+            if ref["status"][j] & SKIP:
+                continue
+            n = int(ref["n"][j])
+            g, r = got["ips"][i, :, :n], ref["ips"][j, :, :n]
+            assert np.array_equal(g.view(np.uint32), r.view(np.uint32)), f"ips instance {i}"
+            if tr and "tr" in ref and "tr" in got:
+                assert np.array_equal(got["tr"][i, :, :n], ref["tr"][j, :, :n]), f"T_R instance {i}"
+
+
+# ------------------------------------------------------------------ hand-worked W1
+
+@pytest.mark.parametrize("case", [d["case"] for d in cases.load_w1()["decisions"]])
+def test_w1(gpu, oracle_mod, case):
+    d = [x for x in cases.load_w1()["decisions"] if x["case"] == case][0]
+    ens, inst, req, td, H, freq, tbt = cases.w1_inputs(d)
+    inputs = dict(inst=inst, req=req, t_dead=td, H=H, freq=freq, tbt_slo=tbt)
+    blob = W.write_blob(ens)
+    got = run_gpu(gpu, blob, inputs)
+    assert int(got["level"][0]) == d["level"] and int(got["status"][0]) == d["status"]
+    assert_parity(got, run_oracle(oracle_mod, blob, inputs))
+
+
+# ------------------------------------------------------------------ brute-force scale random cases
+
+def test_tiny_random(gpu, oracle_mod):
+    rng = np.random.default_rng(11)
+    for trial in range(150):
+        ens, inst, req, td, H, freq, tbt = cases.random_tiny_case(rng)
+        inputs = dict(inst=inst, req=req, t_dead=td, H=H, freq=freq, tbt_slo=tbt)
+        blob = W.write_blob(ens)
+        assert_parity(run_gpu(gpu, blob, inputs), run_oracle(oracle_mod, blob, inputs, threads=1))
+
+
+# ------------------------------------------------------------------ parity configs (several tiles + ragged tails)
+
+@pytest.mark.parametrize("name", ["P1", "P2"])
+def test_parity_configs(gpu, oracle_mod, name):
+    cfg = W.CONFIGS[name]
+    blob = W.write_blob(W.config_ensemble(cfg))
+    inputs = W.config_inputs(cfg)
+    assert_parity(run_gpu(gpu, blob, inputs), run_oracle(oracle_mod, blob, inputs))
+
+
+def test_c1_sweep_10k(gpu, oracle_mod):
+    """BASELINE configs[0] shape, 10^4 instances (one seeded block per 1024)."""
+    cfg = dataclasses.replace(W.CONFIGS["C1"], n_inst=10000)
+    blob = W.write_blob(W.config_ensemble(cfg))
+    inputs = W.config_inputs(cfg)
+    got = run_gpu(gpu, blob, inputs)
+    ref = run_oracle(oracle_mod, blob, inputs)
+    assert_parity(got, ref)
+    assert len(np.unique(ref["level"])) >= 4          # decisions spread over levels
+
+
+def test_c2_full(gpu, oracle_mod):
+    """BASELINE configs[1] at full size: every decision; full grids on a stratified eighth."""
+    cfg = W.CONFIGS["C2"]
+    blob = W.write_blob(W.config_ensemble(cfg))
+    inputs = W.config_inputs(cfg)
+    got = run_gpu(gpu, blob, inputs, want_tr=False)
+    ref = run_oracle(oracle_mod, blob, inputs, want_grid=False, want_tr=False)
+    assert_parity(got, ref, grid=False)
+    sub = np.arange(0, cfg.n_inst, 8)
+    sub_in = _subset(inputs, sub)
+    assert_parity(got, run_oracle(oracle_mod, blob, sub_in, want_tr=False), idx=sub, tr=False)
+
+
+def _subset(inputs, idx):
+    inst = inputs["inst"][idx].copy()
+    reqs, deads, off = [], [], 0
+    for k, i in enumerate(idx):
+        b = int(inputs["inst"][i]["req_begin"])
+        e = b + int(inputs["inst"][i]["n_run"]) + int(inputs["inst"][i]["n_queue"])
+        reqs.append(inputs["req"][b:e]); deads.append(inputs["t_dead"][b:e])
+        inst[k]["req_begin"] = off
+        off += e - b
+    return dict(inputs, inst=inst, req=np.concatenate(reqs), t_dead=np.concatenate(deads))
+
+
+@pytest.mark.parametrize("name,stride", [("C3", 1024), ("C4", 256)])
+def test_full_size_sampled(gpu, oracle_mod, name, stride):
+    """BASELINE configs[2]/[3] at full size on the GPU; the oracle recomputes a stratified sample."""
+    cfg = W.CONFIGS[name]
+    blob = W.write_blob(W.config_ensemble(cfg))
+    inputs = W.config_inputs(cfg)
+    sub = np.arange(3, cfg.n_inst, stride)
+    got = run_gpu(gpu, blob, inputs, want_tr=False, idx=sub)
+    assert_parity(got, run_oracle(oracle_mod, blob, _subset(inputs, sub), want_tr=False), idx=sub, tr=False,
+                  compact=True)
+
+
+# ------------------------------------------------------------------ edge cases
+
+def test_empty_batch(gpu, oracle_mod):
+    cfg = W.CONFIGS["P1"]
+    blob = W.write_blob(W.config_ensemble(cfg))
+    inputs = dict(W.config_inputs(cfg), inst=np.zeros(0, W.INST_DTYPE), req=np.zeros(0, W.REQ_DTYPE),
+                  t_dead=np.zeros(0))
+    got = run_gpu(gpu, blob, inputs)
+    assert got["level"].shape == (0,)
+
+
+@pytest.mark.parametrize("F,H,N,depth,n_trees", [(1, 1, 1, 0, 3), (32, 37, 1, 3, 9), (3, 300, 2, 12, 4),
+                                                 (17, 65, 128, 1, 0), (32, 1024, 64, 8, 33), (2, 33, 3, 5, 120)])
+def test_shapes(gpu, oracle_mod, F, H, N, depth, n_trees):
+    """Degenerate and maximal shapes: F = 1 / 32, H = 1 (one iteration), N = 1 (a block per
+    token), depth 0 (stumps-free constant trees) and 12 (deepest), zero trees, ragged tails."""
+    cfg = dataclasses.replace(W.CONFIGS["P1"], n_inst=70, H=H, F=F, N=N, n_trees=n_trees, depth=depth,
+                              seed=3000 + F + H)
+    ens = W.gen_ensemble(n_trees, depth, 7 + depth, W.freq_levels(F), b_max=40, kv_max=4000, ragged=True)
+    blob = W.write_blob(ens)
+    inputs = W.config_inputs(cfg)
+    assert_parity(run_gpu(gpu, blob, inputs), run_oracle(oracle_mod, blob, inputs))
+
+
+def test_many_thresholds(gpu, oracle_mod):
+    """> 255 distinct thresholds per feature (16-bit ranks) and thresholds equal to feature values."""
+    rng = np.random.default_rng(5)
+    freq = W.freq_levels(12)
+    trees = []
+    for t in range(40):
+        nodes = []
+
+        def build(d):
+            idx = len(nodes)
+            nodes.append(W.Node(-1))
+            if d < 7:
+                f = int(rng.choice([1, 2, 3], p=[0.3, 0.5, 0.2]))
+                thr = [0, float(rng.integers(0, 70)), float(rng.integers(0, 6000)) + rng.choice([0, 0.25]),
+                       float(rng.choice(freq))][f]
+                nodes[idx] = W.Node(f, float(np.float32(thr)))
+                nodes[idx].left = build(d + 1)
+                nodes[idx].right = build(d + 1)
+            else:
+                nodes[idx].leaf = float(np.float32(rng.uniform(0.1, 3.0)))
+            return idx
+        build(0)
+        trees.append(nodes)
+    ens = W.Ensemble(trees, 1.0, 7)
+    blob = W.write_blob(ens)
+    tp, _ = gpu
+    info = tp.Gbdt(blob, 0).info()
+    assert info.n_cuts[2] > 255
+    cfg = dataclasses.replace(W.CONFIGS["P2"], n_inst=50, F=12, seed=91)
+    inputs = W.config_inputs(cfg)
+    assert_parity(run_gpu(gpu, blob, inputs), run_oracle(oracle_mod, blob, inputs))
+
+
+def test_clamp_and_bad_input(gpu, oracle_mod):
+    ens = cases.ensemble_from_nodes([{"feature": 1, "threshold": 2.0, "left": 1, "right": 2},
+                                     {"feature": -1, "leaf": -5.0}, {"feature": -1, "leaf": 1e9}])
+    inst, req, td = cases.make_instances([dict(N=16, running=[(0, 5, 3, 0, 1e9), (0, 5, 1, 0, 1e9)]),
+                                          dict(N=16, running=[(0, 5, 9, 0, 100.0)]),
+                                          dict(N=0, running=[(0, 5, 3, 0, 100.0)]),
+                                          dict(N=16, queued=[(5, 4, 0, 100.0)]),
+                                          dict(N=16)], 4)
+    req = req.copy()
+    req[4]["a"] = 2          # queued entry with a != 0 -> BAD_INPUT
+    inputs = dict(inst=inst, req=req, t_dead=td, H=4, freq=np.array([1000.0, 1200.0], np.float32), tbt_slo=16.0)
+    blob = W.write_blob(ens)
+    got = run_gpu(gpu, blob, inputs)
+    assert_parity(got, run_oracle(oracle_mod, blob, inputs))
+    assert got["status"][0] & 32 and got["status"].tolist()[1:] == [64, 64, 64, 1]
+
+
+def test_decide_entry_points_agree(gpu, oracle_mod):
+    """tp_decide (device) and tp_decide_host (host buffers, e2e path) == the three calls."""
+    tp, runner = gpu
+    cfg = W.CONFIGS["P2"]
+    blob = W.write_blob(W.config_ensemble(cfg))
+    inputs = W.config_inputs(cfg)
+    ref = run_oracle(oracle_mod, blob, inputs, want_grid=False, want_tr=False)
+    model = tp.Gbdt(blob, 0)
+    I, R = len(inputs["inst"]), len(inputs["req"])
+    ctx = tp.Ctx(0, I, R, inputs["H"], len(inputs["freq"]))
+    r = runner.Round(inputs, "cuda:0")
+    ctx.decide(model, r.inst, I, r.req, R, r.t_dead, inputs["freq"], inputs["tbt_slo"], r.level, r.status)
+    torch.cuda.synchronize()
+    assert np.array_equal(r.level.cpu().numpy(), ref["level"])
+    assert np.array_equal(r.status.cpu().numpy().view(np.uint32), ref["status"])
+    h_level = torch.zeros(I, dtype=torch.int32).pin_memory()
+    h_status = torch.zeros(I, dtype=torch.int32).pin_memory()
+    ctx.decide_host(model, inputs["inst"], I, inputs["req"], R, inputs["t_dead"], inputs["freq"], inputs["tbt_slo"],
+                    h_level, h_status)
+    torch.cuda.synchronize()
+    assert np.array_equal(h_level.numpy(), ref["level"])
+    assert np.array_equal(h_status.numpy().view(np.uint32), ref["status"])
+
+
+def test_concurrent_streams_share_model(gpu, oracle_mod):
+    """One immutable model handle used by two rounds on two streams at once."""
+    tp, runner = gpu
+    cfg = W.CONFIGS["P1"]
+    blob = W.write_blob(W.config_ensemble(cfg))
+    a_in = W.config_inputs(cfg)
+    b_in = W.config_inputs(dataclasses.replace(cfg, seed=4242))
+    model = tp.Gbdt(blob, 0)
+    ra, rb = runner.Round(a_in, "cuda:0"), runner.Round(b_in, "cuda:0")
+    sa, sb = torch.cuda.Stream(), torch.cuda.Stream()
+    for _ in range(3):
+        ra.run(model, sa)
+        rb.run(model, sb)
+    torch.cuda.synchronize()
+    assert_parity(ra.results(), run_oracle(oracle_mod, blob, a_in), tr=False)
+    assert_parity(rb.results(), run_oracle(oracle_mod, blob, b_in), tr=False)
