@@ -40,7 +40,9 @@ __device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
 }
 __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
     uint32_t done;
+    uint32_t polls = 0;
     do {
+        if (++polls == (1u << 28)) __trap();   // a lost TMA completion must fail, never hang the GPU
         asm volatile(
             "{\n\t.reg .pred p;\n\t"
             "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
@@ -94,7 +96,7 @@ k2_gbdt(const __grid_constant__ K2Params p, int TC, int nchunks) {
     __shared__ int s_start_i;
     __shared__ uint32_t s_rf[kMaxF];
 
-    constexpr int TW = 2 << D;    // words per tree
+    constexpr int TW = (2 << D) < 4 ? 4 : (2 << D);    // words per tree (>= 16 B for TMA)
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int G = (p.F + RU - 1) / RU;
     const int I = p.n_inst;
@@ -177,7 +179,7 @@ k2_gbdt(const __grid_constant__ K2Params p, int TC, int nchunks) {
         float acc[RU];
         if (active) {
             int64_t ti;
-            while (t >= pc + (ti = tiles_of(p.n, p.status, ci, G))) {
+            while (t >= pc + (ti = tiles_of(p.n, p.status, ci, G)) && ci < I - 1) {
                 pc += ti;
                 ++ci;
             }
@@ -253,7 +255,7 @@ k2_gbdt(const __grid_constant__ K2Params p, int TC, int nchunks) {
 
 template <int D, int RU>
 int launch_d(const K2Params& p, cudaStream_t s) {
-    const int TW = 2 << D;
+    const int TW = (2 << D) < 4 ? 4 : (2 << D);
     const int tree_bytes = TW * 4;
     int TC = std::max(1, std::min(std::max(p.n_trees, 1), kChunkBytes / tree_bytes));
     const int nchunks = p.n_trees == 0 ? 0 : (p.n_trees + TC - 1) / TC;

@@ -117,7 +117,7 @@ extern "C" int tp_gbdt_load(const void* host_blob, size_t nbytes, int device, tp
         if ((int)cuts[f].size() > tp::kMaxCuts) return TP_EFORMAT;
     }
 
-    const size_t words_per_tree = (size_t)2 << D;
+    const size_t words_per_tree = std::max<size_t>(4, (size_t)2 << D);   // >= 16 B: TMA size/alignment unit
     std::vector<uint32_t> words(std::max<size_t>(1, nt * words_per_tree), 0u);
     for (uint32_t t = 0; t < nt; ++t) fill(trees[t], 0, 1u, 0, D, cuts, &words[t * words_per_tree]);
     std::vector<float> allc;
@@ -179,6 +179,6 @@ extern "C" int tp_gbdt_get_info(const tp_gbdt* h, tp_gbdt_info* out) {
     for (int f = 0; f < 4; ++f) out->n_cuts[f] = h->m.n_cuts[f];
     out->base_score = h->m.base;
     out->device_bytes = h->m.device_bytes;
-    out->node_bytes = (int64_t)h->m.n_trees * ((int64_t)2 << h->m.depth) * 4;
+    out->node_bytes = (int64_t)h->m.n_trees * std::max<int64_t>(4, (int64_t)2 << h->m.depth) * 4;
     return TP_OK;
 }

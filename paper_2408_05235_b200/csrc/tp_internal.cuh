@@ -16,7 +16,7 @@ constexpr int64_t kFeatLimit = 1LL << 24;  // integer features exact in fp32
 
 // Device-resident, normalised ensemble (built by tp_gbdt_load, model.cu).
 //
-// Node words: tree t occupies words[t * (2 << D) .. (t + 1) * (2 << D)), a complete binary heap
+// Node words: tree t occupies words[t * TW .. (t + 1) * TW), TW = max(4, 2 << D), a complete binary heap
 // with 1-based index: internal node idx in [1, 2^D), leaf idx in [2^D, 2^(D+1)), children of idx at
 // 2*idx (left, x < thr) and 2*idx + 1.  word 0 is unused.
 //   internal word = ((0xFFFF - j) << 16) | sel(f)
