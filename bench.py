@@ -174,6 +174,8 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--e2e-steps", type=int, default=None)
+    ap.add_argument("--k2", default="runs", choices=["runs", "direct"],
+                    help="K2 variant: run-compressed (default) or one evaluation per grid point")
     args = ap.parse_args()
     cfg = W.CONFIGS[args.workload]
     if args.impl == "reference":
@@ -188,10 +190,28 @@ def main():
     local = env_int("LOCAL_RANK", 0)
     if world != args.gpus:
         print(f"warning: --gpus {args.gpus} but WORLD_SIZE={world}; using WORLD_SIZE", file=sys.stderr)
+    # TP_BENCH_DIST_TEST=1 (test aid only): several ranks on ONE GPU over gloo, to exercise the
+    # multi-rank code path on a 1-GPU box; real runs use one GPU per rank and NCCL.
+    dist_test = os.environ.get("TP_BENCH_DIST_TEST") == "1"
+    if dist_test:
+        local = 0
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     if world > 1:
-        dist.init_process_group("nccl", device_id=dev)
+        if dist_test:
+            dist.init_process_group("gloo")
+        else:
+            dist.init_process_group("nccl", device_id=dev)
+
+    def _coll(t, fn):
+        if not dist_test:
+            return fn(t)
+        c = t.cpu()
+        fn(c)
+        t.copy_(c)
+
+    def all_reduce(t, op):
+        _coll(t, lambda x: dist.all_reduce(x, op=op))
 
     i0, i1, I_glob = shard_of(cfg, rank, world)
     blob = W.write_blob(W.config_ensemble(cfg))
@@ -199,7 +219,7 @@ def main():
     I, R = len(inputs["inst"]), len(inputs["req"])
     model = tp.Gbdt(blob, local)
     info = model.info()
-    rnd = runner.Round(inputs, dev)
+    rnd = runner.Round(inputs, dev, k2_mode=args.k2)
     dec = torch.empty((2, max(I, 1)), dtype=torch.int32, device=dev)   # level, status rows
     rnd.level, rnd.status = dec[0], dec[1]
     # equal shards (C2 weak, C5 = 262144 / {1,2,4,8}): one preallocated all-gather of [2, I] rows
@@ -220,7 +240,12 @@ def main():
         if evs:
             evs[3].record(stream)
         if world > 1:
-            dist.all_gather_into_tensor(gathered, dec)
+            if dist_test:
+                g = torch.empty(gathered.shape, dtype=gathered.dtype)
+                dist.all_gather_into_tensor(g, dec.cpu())
+                gathered.copy_(g)
+            else:
+                dist.all_gather_into_tensor(gathered, dec)
         if evs:
             evs[4].record(stream)
 
@@ -233,6 +258,7 @@ def main():
     st_h = rnd.status[:I].cpu().numpy().view(np.uint32)
     grid = int((n_h * ((st_h & SKIP) == 0)).sum()) * rnd.F
     padded = int((((n_h + 31) // 32) * 32 * ((st_h & SKIP) == 0)).sum()) * rnd.F
+    evaluated = tp.runs_total(rnd.work, I, rnd.H) * rnd.F if args.k2 == "runs" else grid
 
     evs = [[torch.cuda.Event(enable_timing=True) for _ in range(5)] for _ in range(args.steps)]
     clocks = Clocks(local)
@@ -251,12 +277,28 @@ def main():
     per = np.array([[e[j].elapsed_time(e[j + 1]) for j in range(4)] for e in evs])   # ms
     t_total = float(per.sum())
     k_ms = per.mean(axis=0)
+    # the north_star's direct K2 (one descent per grid point), timed on the same inputs for reference
+    d_ms = None
+    if args.k2 == "runs":
+        rd = runner.Round(inputs, dev, k2_mode="direct")
+        rd.project(stream)
+        rd.predict(model, stream)
+        de = [[torch.cuda.Event(enable_timing=True) for _ in range(2)] for _ in range(5)]
+        for a, b in de:
+            flush.zero_()
+            a.record(stream)
+            rd.predict(model, stream)
+            b.record(stream)
+        torch.cuda.synchronize(dev)
+        d_ms = float(np.median([a.elapsed_time(b) for a, b in de]))
+        del rd
     tot = torch.tensor([t_total, grid, I], dtype=torch.float64, device=dev)
     if world > 1:
-        mx = tot.clone()
-        dist.all_reduce(mx[:1], op=dist.ReduceOp.MAX)
-        dist.all_reduce(tot[1:], op=dist.ReduceOp.SUM)
-        tot[0] = mx[0]
+        mx = tot[:1].clone()
+        sm = tot[1:].clone()
+        all_reduce(mx, dist.ReduceOp.MAX)
+        all_reduce(sm, dist.ReduceOp.SUM)
+        tot = torch.cat([mx, sm])
     t_max_ms, grid_all, inst_all = float(tot[0]), float(tot[1]), float(tot[2])
     sec = t_max_ms / 1e3
     decisions_per_s = inst_all * args.steps / sec
@@ -284,7 +326,7 @@ def main():
         torch.cuda.synchronize(dev)
         te = torch.tensor([sum(a.elapsed_time(b) for a, b in ee)], dtype=torch.float64, device=dev)
         if world > 1:
-            dist.all_reduce(te, op=dist.ReduceOp.MAX)
+            all_reduce(te, dist.ReduceOp.MAX)
         ok = np.array_equal(h_level[:I].numpy(), dec[0, :I].cpu().numpy())
         e2e = {"value": inst_all * ke / (float(te[0]) / 1e3), "unit": "decisions/s",
                "h2d_bytes_per_step": int(I * 48 + R * 16 + R * 8), "d2h_bytes_per_step": int(I * 8),
@@ -304,7 +346,7 @@ def main():
     sms = torch.cuda.get_device_properties(dev).multi_processor_count
     per_pt = info.n_trees * (info.depth + 1) * 4
     k2_s = k_ms[1] / 1e3
-    achieved = grid * per_pt / k2_s / 1e9          # this rank's K2, GB/s
+    achieved = evaluated * per_pt / k2_s / 1e9     # this rank's K2 (incl. the run pre-pass), GB/s
     peak = sms * 128 * smax * 1e6 / 1e9
     traffic = None
     try:
@@ -314,11 +356,17 @@ def main():
             traffic = tj.get("dram_bytes_per_launch")
     except (OSError, ValueError):
         pass
-    roof = {"bound": "smem", "kernel": "k2_gbdt", "achieved": achieved, "peak": peak, "unit": "GB/s",
+    roof = {"bound": "smem", "kernel": "k2_gbdt" + ("<runs> (+ k2_runs pre-pass)" if args.k2 == "runs" else ""),
+            "achieved": achieved, "peak": peak, "unit": "GB/s",
             "frac": achieved / peak, "traffic": traffic,
             "peak_basis": f"{sms} SMs x 128 B/clk (LDS) x sm_max_mhz {smax:.0f} (MEASURED_PEAKS.json clock)",
             "frac_at_observed_clock": (achieved / (sms * 128 * clk["sm_mhz"] * 1e6 / 1e9)) if clk["sm_mhz"] else None,
-            "bytes_per_grid_point": per_pt, "grid_points_per_launch": grid, "padded_grid_points": padded}
+            "bytes_per_evaluated_row": per_pt, "evaluated_rows_per_launch": evaluated,
+            "grid_points_per_launch": grid, "padded_grid_points": padded}
+    if d_ms is not None:
+        da = grid * per_pt / (d_ms / 1e3) / 1e9
+        roof["direct_k2"] = {"ms": d_ms, "achieved": da, "frac": da / peak,
+                             "note": "tp_predict_ips (one descent per grid point) on the same inputs"}
     cpu = None
     if world == 1 and not args.no_cpu_baseline:
         cpu = cpu_baseline(cfg, blob, inputs)
@@ -330,7 +378,7 @@ def main():
         "config": {"workload": DESCR[cfg.name], "name": cfg.name, "instances_per_gpu": I,
                    "global_instances": int(inst_all), "H": cfg.H, "F": cfg.F, "trees": info.n_trees,
                    "depth": info.depth, "parallelism": f"instance-sharded x{world}" + (" + NCCL all-gather" if world > 1 else ""),
-                   "l2": "flushed between timed steps (256 MiB device write, untimed)"},
+                   "l2": "flushed between timed steps (256 MiB device write, untimed)", "k2": args.k2},
         "grid_evals_per_sec": grid_per_s,
         "per_kernel_ms": {"k1_project": k_ms[0], "k2_gbdt": k_ms[1], "k3_select": k_ms[2],
                           "gather": k_ms[3]},

@@ -161,6 +161,27 @@ int tp_predict_ips(const tp_gbdt* m, const tp_inst* inst, int32_t n_inst, const 
                    float* ips, uint32_t* status, void* stream);
 
 /*
+ * K2, run-compressed (same outputs, bit for bit, as tp_predict_ips).  M depends on the iteration
+ * m only through the features (B[m], KV[m]) and, for a given ensemble, only through their ranks
+ * among the ensemble's thresholds; consecutive iterations with equal ranks ("runs", typically
+ * 5-10 iterations long: KV grows by about B/N blocks per iteration) therefore share one IPS value
+ * exactly.  A first kernel builds each instance's runs, the ensemble is evaluated once per
+ * (run, level), and the value is written to every iteration of the run.
+ *   workspace [dev] scratch of at least tp_predict_ips_workspace_size(n_inst, H) bytes, owned by
+ *             the caller, not used concurrently by another call.
+ * Other arguments, outputs and errors: as tp_predict_ips.
+ */
+size_t tp_predict_ips_workspace_size(int32_t n_inst, int32_t H);
+int tp_predict_ips_runs(const tp_gbdt* m, const tp_inst* inst, int32_t n_inst, const int32_t* B,
+                        const int32_t* KV, const int32_t* n, int32_t H, const float* freq_mhz,
+                        int32_t F, float* ips, uint32_t* status, void* workspace,
+                        size_t workspace_bytes, void* stream);
+
+/* Diagnostics (synchronous, not for the hot path): total number of runs the last
+ * tp_predict_ips_runs call on `workspace` evaluated (per level). */
+int tp_runs_total(const void* workspace, int32_t n_inst, int32_t H, int64_t* total);
+
+/*
  * K3 -- SLO scan and frequency choice (Eq. 3-4; throttle P:550-557).
  * For each instance not flagged BAD_INPUT / EMPTY / BYPASS_LOST and each level u:
  *   T'[m] = fl32(1 / ips[m])                                       (reading A-9)
@@ -184,7 +205,7 @@ int tp_select_freq(const tp_inst* inst, int32_t n_inst, const tp_req* req, int32
 /*
  * Convenience: one decision round with library-owned scratch.
  * tp_ctx_create allocates, on `device`, B/KV/n/n_adm (n_inst_max x H), the ips grid
- * (n_inst_max x F_max x H) and staging for up to n_req_max requests.
+ * (n_inst_max x F_max x H), the run workspace and staging for up to n_req_max requests.
  */
 typedef struct tp_ctx tp_ctx;
 int tp_ctx_create(int device, int32_t n_inst_max, int32_t n_req_max, int32_t H, int32_t F_max,
@@ -203,6 +224,10 @@ int tp_decide_host(tp_ctx* c, const tp_gbdt* m, const tp_inst* h_inst, int32_t n
                    const tp_req* h_req, int32_t n_req, const double* h_t_dead,
                    const float* freq_mhz, int32_t F, float tbt_slo, int32_t* h_level,
                    uint32_t* h_status, void* stream);
+
+/* Which K2 variant tp_decide / tp_decide_host use (default TP_K2_RUNS). */
+enum { TP_K2_DIRECT = 0, TP_K2_RUNS = 1 };
+int tp_ctx_set_k2_mode(tp_ctx* c, int mode);
 
 /* Device pointers of the context's scratch (for inspection / tests); any out may be NULL. */
 int tp_ctx_buffers(tp_ctx* c, int32_t** B, int32_t** KV, int32_t** n, int32_t** n_adm, float** ips);

@@ -30,6 +30,9 @@ struct tp_ctx {
     int32_t *B, *KV, *n, *n_adm, *level;
     uint32_t* status;
     float* ips;
+    void* work;
+    size_t work_bytes;
+    int k2_mode;
     tp_inst* inst;
     tp_req* req;
     double* t_dead;
@@ -81,7 +84,55 @@ int tp_predict_ips(const tp_gbdt* m, const tp_inst* inst, int32_t n_inst, const 
     p.H = H;
     p.F = F;
     for (int u = 0; u < F; ++u) p.freq[u] = freq_mhz[u];
-    return tp::launch_gbdt(p, S(stream));
+    return tp::launch_gbdt(p, false, S(stream));
+}
+
+size_t tp_predict_ips_workspace_size(int32_t n_inst, int32_t H) {
+    if (n_inst < 0 || !H_ok(H)) return 0;
+    return tp::runs_workspace_bytes(n_inst, H);
+}
+
+int tp_predict_ips_runs(const tp_gbdt* m, const tp_inst* inst, int32_t n_inst, const int32_t* B, const int32_t* KV,
+                        const int32_t* n, int32_t H, const float* freq_mhz, int32_t F, float* ips, uint32_t* status,
+                        void* workspace, size_t workspace_bytes, void* stream) {
+    if (!m || n_inst < 0 || !H_ok(H) || !freq_ok(freq_mhz, F)) return TP_EINVAL;
+    if (n_inst > 0 && (!inst || !B || !KV || !n || !ips || !status || !workspace)) return TP_EINVAL;
+    if (n_inst > 0 && workspace_bytes < tp::runs_workspace_bytes(n_inst, H)) return TP_EINVAL;
+    tp::K2Params p;
+    std::memset(&p, 0, sizeof(p));
+    p.words = m->m.d_words;
+    p.cuts = m->m.d_cuts;
+    for (int f = 0; f < 5; ++f) p.cut_off[f] = m->m.cut_off[f];
+    p.n_trees = m->m.n_trees;
+    p.depth = m->m.depth;
+    p.base = m->m.base;
+    p.inst = inst;
+    p.B = B;
+    p.KV = KV;
+    p.n = n;
+    p.status = status;
+    p.ips = ips;
+    p.n_inst = n_inst;
+    p.H = H;
+    p.F = F;
+    for (int u = 0; u < F; ++u) p.freq[u] = freq_mhz[u];
+    if (n_inst > 0) tp::runs_workspace_carve(workspace, n_inst, H, p);
+    return tp::launch_gbdt(p, true, S(stream));
+}
+
+int tp_runs_total(const void* workspace, int32_t n_inst, int32_t H, int64_t* total) {
+    if (!workspace || !total || n_inst < 0 || !H_ok(H)) return TP_EINVAL;
+    *total = 0;
+    if (n_inst == 0) return TP_OK;
+    tp::K2Params p;
+    std::memset(&p, 0, sizeof(p));
+    tp::runs_workspace_carve(const_cast<void*>(workspace), n_inst, H, p);
+    int32_t* h = new (std::nothrow) int32_t[n_inst];
+    if (!h) return TP_ENOMEM;
+    const bool ok = cudaMemcpy(h, p.run_h, (size_t)n_inst * 4, cudaMemcpyDeviceToHost) == cudaSuccess;
+    for (int32_t i = 0; ok && i < n_inst; ++i) *total += h[i];
+    delete[] h;
+    return ok ? TP_OK : TP_ECUDA;
 }
 
 int tp_select_freq(const tp_inst* inst, int32_t n_inst, const tp_req* req, int32_t n_req, const double* t_dead,
@@ -106,6 +157,7 @@ int tp_ctx_create(int device, int32_t n_inst_max, int32_t n_req_max, int32_t H, 
     c->n_req_max = n_req_max;
     c->H = H;
     c->F_max = F_max;
+    c->k2_mode = TP_K2_RUNS;
     int prev = 0;
     cudaGetDevice(&prev);
     if (cudaSetDevice(device) != cudaSuccess) {
@@ -117,6 +169,7 @@ int tp_ctx_create(int device, int32_t n_inst_max, int32_t n_req_max, int32_t H, 
               cudaMalloc(&c->n, I * 4) == cudaSuccess && cudaMalloc(&c->n_adm, I * 4) == cudaSuccess &&
               cudaMalloc(&c->level, I * 4) == cudaSuccess && cudaMalloc(&c->status, I * 4) == cudaSuccess &&
               cudaMalloc(&c->ips, I * F_max * H * 4) == cudaSuccess &&
+              cudaMalloc(&c->work, c->work_bytes = tp::runs_workspace_bytes((int32_t)I, H)) == cudaSuccess &&
               cudaMalloc(&c->inst, I * sizeof(tp_inst)) == cudaSuccess &&
               cudaMalloc(&c->req, R * sizeof(tp_req)) == cudaSuccess &&
               cudaMalloc(&c->t_dead, R * sizeof(double)) == cudaSuccess;
@@ -134,11 +187,17 @@ int tp_ctx_free(tp_ctx* c) {
     int prev = 0;
     cudaGetDevice(&prev);
     cudaSetDevice(c->device);
-    void* ptrs[] = {c->B, c->KV, c->n, c->n_adm, c->level, c->status, c->ips, c->inst, c->req, c->t_dead};
+    void* ptrs[] = {c->B, c->KV, c->n, c->n_adm, c->level, c->status, c->ips, c->work, c->inst, c->req, c->t_dead};
     for (void* p : ptrs)
         if (p) cudaFree(p);
     cudaSetDevice(prev);
     delete c;
+    return TP_OK;
+}
+
+int tp_ctx_set_k2_mode(tp_ctx* c, int mode) {
+    if (!c || (mode != TP_K2_DIRECT && mode != TP_K2_RUNS)) return TP_EINVAL;
+    c->k2_mode = mode;
     return TP_OK;
 }
 
@@ -160,7 +219,10 @@ int tp_decide(tp_ctx* c, const tp_gbdt* m, const tp_inst* inst, int32_t n_inst, 
         return TP_EINVAL;
     int rc = tp_project(inst, n_inst, req, n_req, c->H, c->B, c->KV, c->n, c->n_adm, status, stream);
     if (rc) return rc;
-    rc = tp_predict_ips(m, inst, n_inst, c->B, c->KV, c->n, c->H, freq_mhz, F, c->ips, status, stream);
+    rc = c->k2_mode == TP_K2_RUNS
+             ? tp_predict_ips_runs(m, inst, n_inst, c->B, c->KV, c->n, c->H, freq_mhz, F, c->ips, status, c->work,
+                                   c->work_bytes, stream)
+             : tp_predict_ips(m, inst, n_inst, c->B, c->KV, c->n, c->H, freq_mhz, F, c->ips, status, stream);
     if (rc) return rc;
     return tp_select_freq(inst, n_inst, req, n_req, t_dead, c->n, c->n_adm, c->ips, c->H, F, tbt_slo, level, status,
                           nullptr, stream);

@@ -17,15 +17,17 @@
 //  * Persistent-style grid (#SMs x occupancy CTAs); tiles are split evenly over CTAs by a
 //    per-CTA scan of the per-instance tile counts.
 #include <algorithm>
+#include <cstdlib>
 
 #include "tp_internal.cuh"
 
 namespace tp {
 namespace {
 
-constexpr int kThreads = 256;
-constexpr int kWarps = kThreads / 32;
-constexpr int kChunkBytes = 48 * 1024;
+constexpr int kMaxThreads = 384;        // CTA size is a launch parameter (256 or 384 threads)
+constexpr int kMaxWarps = kMaxThreads / 32;
+constexpr int kDefaultThreads = 384;
+constexpr int kDefaultChunkBytes = 48 * 1024;
 constexpr uint32_t kSkip = TP_ST_BAD_INPUT | TP_ST_EMPTY | TP_ST_BYPASS_LOST;
 
 __device__ __forceinline__ uint32_t smem_addr(const void* p) {
@@ -59,6 +61,12 @@ __device__ __forceinline__ void tma_load(void* dst, const void* src, uint32_t by
                  : "memory");
 }
 
+__device__ __forceinline__ uint32_t prmt(uint32_t lo, uint32_t hi, uint32_t sel) {
+    uint32_t r;
+    asm("prmt.b32 %0, %1, %2, %3;" : "=r"(r) : "r"(lo), "r"(hi), "r"(sel));
+    return r;
+}
+
 // One tree level: idx' = 2*idx + go_right, go_right = carry_out(prmt(xlo, xhi, w) + w).
 __device__ __forceinline__ uint32_t descend(uint32_t idx, uint32_t w, uint32_t xlo, uint32_t xhi) {
     uint32_t out;
@@ -68,6 +76,18 @@ __device__ __forceinline__ uint32_t descend(uint32_t idx, uint32_t w, uint32_t x
         "addc.u32 %0, %4, %4;\n\t}"
         : "=r"(out)
         : "r"(xlo), "r"(xhi), "r"(w), "r"(idx));
+    return out;
+}
+
+// Same step with the doubled index given: returns base2 + go_right (base2 = 2 * idx).
+__device__ __forceinline__ uint32_t step_from(uint32_t base2, uint32_t w, uint32_t xlo, uint32_t xhi) {
+    uint32_t out;
+    asm("{\n\t.reg .b32 pr, t;\n\t"
+        "prmt.b32 pr, %1, %2, %3;\n\t"
+        "add.cc.u32 t, pr, %3;\n\t"
+        "addc.u32 %0, %4, 0;\n\t}"
+        : "=r"(out)
+        : "r"(xlo), "r"(xhi), "r"(w), "r"(base2));
     return out;
 }
 
@@ -81,25 +101,95 @@ __device__ __forceinline__ uint32_t rank_of(const float* __restrict__ c, int cnt
     return (uint32_t)lo;
 }
 
-__device__ __forceinline__ int64_t tiles_of(const int32_t* __restrict__ n, const uint32_t* __restrict__ st,
-                                            int i, int G) {
-    return (st[i] & kSkip) ? 0 : (int64_t)((n[i] + 31) >> 5) * G;
+// Work units of instance i.  Direct mode: one unit = one warp tile = 32 consecutive iterations x
+// RU levels, ceil(n/32) * G units.  Run mode: one unit = one lane task = one run x RU levels,
+// h * G units, packed 32 per warp tile across instance boundaries (no padding).
+template <bool RUNS>
+__device__ __forceinline__ int64_t units_of(const K2Params& p, int i, int G) {
+    if (p.status[i] & kSkip) return 0;
+    return RUNS ? (int64_t)p.run_h[i] * G : (int64_t)((p.n[i] + 31) >> 5) * G;
 }
 
-template <int D, int RU>
-__global__ void __launch_bounds__(kThreads, 2)
+// K2a (run mode only): per instance, the runs of consecutive iterations m whose (batch, KV)
+// features have the same ranks among the ensemble's thresholds -- M is constant on each run
+// because tp and f are fixed per (instance, level).  One CTA per instance: keys for all m in
+// shared memory (cut lists staged in shared memory when they fit), then a block-wide ballot
+// compaction of the run heads.
+constexpr int kRunsThreads = 256;
+constexpr int kRunsCutCap = 2048;     // cuts per feature staged in shared memory (else global)
+
+__device__ __forceinline__ uint32_t rank_smem(const float* c, int cnt, float x) {
+    int lo = 0, hi = cnt;
+    while (lo < hi) {
+        const int mid = (lo + hi) >> 1;
+        if (c[mid] <= x) lo = mid + 1;
+        else hi = mid;
+    }
+    return (uint32_t)lo;
+}
+
+__global__ void __launch_bounds__(kRunsThreads)
+k2_runs(const __grid_constant__ K2Params p) {
+    extern __shared__ uint32_t skey[];               // [H + 1]: key of iteration m at skey[m]
+    __shared__ float scB[kRunsCutCap], scKV[kRunsCutCap];
+    __shared__ int swarp[kRunsThreads / 32];
+    const int i = blockIdx.x, tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int n = (p.status[i] & kSkip) ? 0 : p.n[i];
+    if (n == 0) {
+        if (tid == 0) p.run_h[i] = 0;
+        return;
+    }
+    const int nB = p.cut_off[2] - p.cut_off[1], nKV = p.cut_off[3] - p.cut_off[2];
+    const bool smB = nB <= kRunsCutCap, smKV = nKV <= kRunsCutCap;
+    if (smB)
+        for (int j = tid; j < nB; j += kRunsThreads) scB[j] = p.cuts[p.cut_off[1] + j];
+    if (smKV)
+        for (int j = tid; j < nKV; j += kRunsThreads) scKV[j] = p.cuts[p.cut_off[2] + j];
+    __syncthreads();
+    const size_t row = (size_t)i * p.H;
+    for (int m = 1 + tid; m <= n; m += kRunsThreads) {
+        const float b = (float)p.B[row + m - 1], kv = (float)p.KV[row + m - 1];
+        const uint32_t rb = smB ? rank_smem(scB, nB, b) : rank_of(p.cuts + p.cut_off[1], nB, b);
+        const uint32_t rk = smKV ? rank_smem(scKV, nKV, kv) : rank_of(p.cuts + p.cut_off[2], nKV, kv);
+        skey[m] = rb | (rk << 16);
+    }
+    __syncthreads();
+    int base = 0;
+    for (int m0 = 1; m0 <= n; m0 += kRunsThreads) {
+        const int m = m0 + tid;
+        const bool head = m <= n && (m == 1 || skey[m] != skey[m - 1]);
+        const unsigned mask = __ballot_sync(0xffffffffu, head);
+        if (lane == 0) swarp[warp] = __popc(mask);
+        __syncthreads();
+        int before = base;
+        for (int w = 0; w < warp; ++w) before += swarp[w];
+        if (head) {
+            const int pos = before + __popc(mask & ((1u << lane) - 1u));
+            p.run_m[row + pos] = m;
+            p.run_key[row + pos] = skey[m];
+        }
+        for (int w = 0; w < kRunsThreads / 32; ++w) base += swarp[w];
+        __syncthreads();
+    }
+    if (tid == 0) p.run_h[i] = base;
+}
+
+template <int D, int RU, bool RUNS>
+__global__ void __launch_bounds__(kMaxThreads, 2)
 k2_gbdt(const __grid_constant__ K2Params p, int TC, int nchunks) {
     extern __shared__ __align__(128) uint32_t sw[];
     __shared__ __align__(8) uint64_t full[2];
-    __shared__ int64_t red[kWarps];
+    __shared__ int64_t red[kMaxWarps];
     __shared__ int64_t s_start_pc;
     __shared__ int s_start_i;
     __shared__ uint32_t s_rf[kMaxF];
 
     constexpr int TW = (2 << D) < 4 ? 4 : (2 << D);    // words per tree (>= 16 B for TMA)
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int nthreads = blockDim.x, nwarps = nthreads >> 5;
     const int G = (p.F + RU - 1) / RU;
     const int I = p.n_inst;
+    constexpr int UPT = RUNS ? 32 : 1;            // units per warp tile
     const bool resident = nchunks == 1;
     const int stages = resident ? 1 : 2;
     const int chunk_words = TC * TW;
@@ -107,24 +197,26 @@ k2_gbdt(const __grid_constant__ K2Params p, int TC, int nchunks) {
     if (tid < p.F)
         s_rf[tid] = rank_of(p.cuts + p.cut_off[3], p.cut_off[4] - p.cut_off[3], p.freq[tid]);
 
-    // ---- split the tile space [0, Ttot) evenly over CTAs ----
-    int64_t tot = 0;
-    for (int i = tid; i < I; i += kThreads) tot += tiles_of(p.n, p.status, i, G);
-    for (int o = 16; o; o >>= 1) tot += __shfl_xor_sync(0xffffffffu, tot, o);
-    if (lane == 0) red[warp] = tot;
+    // ---- split the tile space [0, ceil(U / UPT)) evenly over CTAs ----
+    int64_t U = 0;
+    for (int i = tid; i < I; i += nthreads) U += units_of<RUNS>(p, i, G);
+    for (int o = 16; o; o >>= 1) U += __shfl_xor_sync(0xffffffffu, U, o);
+    if (lane == 0) red[warp] = U;
     __syncthreads();
-    tot = 0;
-    for (int k = 0; k < kWarps; ++k) tot += red[k];
-    const int64_t t0 = tot * blockIdx.x / gridDim.x, t1 = tot * (blockIdx.x + 1) / gridDim.x;
+    U = 0;
+    for (int k = 0; k < nwarps; ++k) U += red[k];
+    const int64_t ntiles = (U + UPT - 1) / UPT;
+    const int64_t t0 = ntiles * blockIdx.x / gridDim.x, t1 = ntiles * (blockIdx.x + 1) / gridDim.x;
     if (t0 >= t1) return;   // uniform: no work for this CTA
+    const int64_t u_first = t0 * UPT;
 
-    // locate the instance holding tile t0 (block-wide scan over instances, chunk by chunk)
+    // locate the instance holding unit u_first (block-wide scan over instances, chunk by chunk)
     if (tid == 0) s_start_i = -1;
     __syncthreads();
     int64_t base_pc = 0;
-    for (int c0 = 0; c0 < I; c0 += kThreads) {
+    for (int c0 = 0; c0 < I; c0 += nthreads) {
         const int i = c0 + tid;
-        const int64_t v = i < I ? tiles_of(p.n, p.status, i, G) : 0;
+        const int64_t v = i < I ? units_of<RUNS>(p, i, G) : 0;
         int64_t x = v;
         for (int o = 1; o < 32; o <<= 1) {
             const int64_t y = __shfl_up_sync(0xffffffffu, x, o);
@@ -136,11 +228,11 @@ k2_gbdt(const __grid_constant__ K2Params p, int TC, int nchunks) {
         int64_t pre = base_pc;
         for (int k = 0; k < warp; ++k) pre += red[k];
         const int64_t incl = pre + x, excl = incl - v;
-        if (i < I && v > 0 && excl <= t0 && t0 < incl) {
+        if (i < I && v > 0 && excl <= u_first && u_first < incl) {
             s_start_i = i;
             s_start_pc = excl;
         }
-        for (int k = 0; k < kWarps; ++k) base_pc += red[k];
+        for (int k = 0; k < nwarps; ++k) base_pc += red[k];
         __syncthreads();
         if (s_start_i >= 0) break;
     }
@@ -151,7 +243,7 @@ k2_gbdt(const __grid_constant__ K2Params p, int TC, int nchunks) {
     }
     __syncthreads();
 
-    const int nrounds = (int)((t1 - t0 + kWarps - 1) / kWarps);
+    const int nrounds = (int)((t1 - t0 + nwarps - 1) / nwarps);
     const int64_t total_loads = nchunks == 0 ? 0 : (resident ? 1 : (int64_t)nrounds * nchunks);
     auto issue = [&](int64_t g) {
         const int c = (int)(g % nchunks), s = (int)(g % stages);
@@ -172,31 +264,60 @@ k2_gbdt(const __grid_constant__ K2Params p, int TC, int nchunks) {
     const int nB = p.cut_off[2] - p.cut_off[1], nKV = p.cut_off[3] - p.cut_off[2], nTP = p.cut_off[1] - p.cut_off[0];
 
     for (int round = 0; round < nrounds; ++round) {
-        const int64_t t = t0 + (int64_t)round * kWarps + warp;
+        const int64_t t = t0 + (int64_t)round * nwarps + warp;
         const bool active = t < t1;
-        int i = 0, m = 0, u0 = 0, ni = 0;
+        int i = 0, m = 0, u0 = 0, ni = 0, m_end = 0;
         uint32_t xlo = 0, xhi[RU];
         float acc[RU];
         if (active) {
+            const int64_t ub = t * UPT;   // first unit of the tile
             int64_t ti;
-            while (t >= pc + (ti = tiles_of(p.n, p.status, ci, G)) && ci < I - 1) {
+            while (ub >= pc + (ti = units_of<RUNS>(p, ci, G)) && ci < I - 1) {
                 pc += ti;
                 ++ci;
             }
-            i = ci;
-            const int64_t tau = t - pc;
-            const int mt = (int)(tau / G), ug = (int)(tau % G);
-            ni = p.n[i];
-            m = mt * 32 + lane + 1;
-            u0 = ug * RU;
-            const int tpv = p.inst[i].tp;
-            int bv = 0, kvv = 0;
-            if (m <= ni) {
-                bv = p.B[(size_t)i * p.H + m - 1];
-                kvv = p.KV[(size_t)i * p.H + m - 1];
+            uint32_t rkv;
+            if constexpr (RUNS) {
+                // lane task = unit ub + lane -> (instance li, run k, level group ug); the tile's
+                // lanes may span several instances (each lane walks on from the warp's cursor)
+                const int64_t uu = ub + lane;
+                int li = ci;
+                int64_t lpc = pc, lt;
+                while (uu >= lpc + (lt = units_of<RUNS>(p, li, G)) && li < I - 1) {
+                    lpc += lt;
+                    ++li;
+                }
+                i = li;
+                uint32_t key = 0;
+                m = 0x7fffffff;
+                if (uu < U) {
+                    const int h = p.run_h[i];
+                    const int tau = (int)(uu - lpc);
+                    const int ug = tau / h, k = tau - ug * h;
+                    u0 = ug * RU;
+                    key = p.run_key[(size_t)i * p.H + k];
+                    m = p.run_m[(size_t)i * p.H + k];
+                    ni = p.n[i];
+                    m_end = (k + 1 < h) ? p.run_m[(size_t)i * p.H + k + 1] : ni + 1;
+                }
+                xlo = rank_of(cutsTP, nTP, (float)p.inst[i].tp) | ((key & 0xFFFFu) << 16);
+                rkv = key >> 16;
+            } else {
+                i = ci;
+                const int64_t tau = ub - pc;
+                const int mt = (int)(tau / G), ug = (int)(tau % G);
+                ni = p.n[i];
+                u0 = ug * RU;
+                const int tpv = p.inst[i].tp;
+                m = mt * 32 + lane + 1;
+                int bv = 0, kvv = 0;
+                if (m <= ni) {
+                    bv = p.B[(size_t)i * p.H + m - 1];
+                    kvv = p.KV[(size_t)i * p.H + m - 1];
+                }
+                xlo = rank_of(cutsTP, nTP, (float)tpv) | (rank_of(cutsB, nB, (float)bv) << 16);
+                rkv = rank_of(cutsKV, nKV, (float)kvv);
             }
-            xlo = rank_of(cutsTP, nTP, (float)tpv) | (rank_of(cutsB, nB, (float)bv) << 16);
-            const uint32_t rkv = rank_of(cutsKV, nKV, (float)kvv);
 #pragma unroll
             for (int r = 0; r < RU; ++r) xhi[r] = rkv | (s_rf[min(u0 + r, p.F - 1)] << 16);
         }
@@ -212,10 +333,23 @@ k2_gbdt(const __grid_constant__ K2Params p, int TC, int nchunks) {
                 for (int tt = 0; tt < nt; ++tt) {
                     const uint32_t* tw = cw + tt * TW;
                     uint32_t idx[RU];
+                    if constexpr (D >= 2) {
+                        // levels 0-1: the root and both of its children are shared by all RU rows
+                        // of the lane, so one LDS + one LDS.64 replace 2 * RU loads; the level-0
+                        // carry selects the level-1 word directly.
+                        const uint32_t w1 = tw[1];
+                        const uint2 w23 = *reinterpret_cast<const uint2*>(tw + 2);
 #pragma unroll
-                    for (int r = 0; r < RU; ++r) idx[r] = 1u;
+                        for (int r = 0; r < RU; ++r) {
+                            const bool c0 = prmt(xlo, xhi[r], w1) > ~w1;    // carry-out of prmt + w1
+                            idx[r] = step_from(c0 ? 6u : 4u, c0 ? w23.y : w23.x, xlo, xhi[r]);
+                        }
+                    } else {
 #pragma unroll
-                    for (int d = 0; d < D; ++d) {
+                        for (int r = 0; r < RU; ++r) idx[r] = 1u;
+                    }
+#pragma unroll
+                    for (int d = (D >= 2 ? 2 : 0); d < D; ++d) {
 #pragma unroll
                         for (int r = 0; r < RU; ++r) idx[r] = descend(idx[r], tw[idx[r]], xlo, xhi[r]);
                     }
@@ -234,72 +368,125 @@ k2_gbdt(const __grid_constant__ K2Params p, int TC, int nchunks) {
 
         if (active) {
             bool clamped = false;
-            if (m <= ni) {
 #pragma unroll
-                for (int r = 0; r < RU; ++r) {
-                    const int u = u0 + r;
-                    if (u < p.F) {
-                        const float v = acc[r];
-                        float c = v;
-                        if (isnan(v)) c = 0x1p-4f;
-                        else c = fminf(fmaxf(v, 0x1p-4f), 0x1p17f);
-                        clamped |= isnan(v) || c != v;
-                        p.ips[((size_t)i * p.F + u) * p.H + (m - 1)] = c;
-                    }
+            for (int r = 0; r < RU; ++r) {
+                const float v = acc[r];
+                const float c = isnan(v) ? 0x1p-4f : fminf(fmaxf(v, 0x1p-4f), 0x1p17f);
+                clamped |= m <= ni && u0 + r < p.F && (isnan(v) || c != v);
+                acc[r] = c;
+            }
+            if constexpr (!RUNS) {
+                if (m <= ni) {
+#pragma unroll
+                    for (int r = 0; r < RU; ++r)
+                        if (u0 + r < p.F) p.ips[((size_t)i * p.F + u0 + r) * p.H + (m - 1)] = acc[r];
+                }
+            } else {
+                // expand: the lane writes its run [m, m_end) for its RU levels
+                for (int mm = m; mm < m_end; ++mm) {
+#pragma unroll
+                    for (int r = 0; r < RU; ++r)
+                        if (u0 + r < p.F) p.ips[((size_t)i * p.F + u0 + r) * p.H + (mm - 1)] = acc[r];
                 }
             }
-            if (__any_sync(0xffffffffu, clamped) && lane == 0) atomicOr(p.status + i, (uint32_t)TP_ST_IPS_CLAMPED);
+            if constexpr (RUNS) {
+                if (clamped) atomicOr(p.status + i, (uint32_t)TP_ST_IPS_CLAMPED);   // lanes may differ in i
+            } else {
+                if (__any_sync(0xffffffffu, clamped) && lane == 0) atomicOr(p.status + i, (uint32_t)TP_ST_IPS_CLAMPED);
+            }
         }
     }
 }
 
-template <int D, int RU>
+// Tuning knobs (read once): TP_K2_THREADS (CTA size, multiple of 32), TP_K2_CHUNK_KB (tree chunk).
+int env_int(const char* name, int dflt, int lo, int hi, int mult) {
+    const char* v = std::getenv(name);
+    if (!v) return dflt;
+    const int x = std::atoi(v);
+    return (x >= lo && x <= hi && x % mult == 0) ? x : dflt;
+}
+
+template <int D, int RU, bool RUNS>
 int launch_d(const K2Params& p, cudaStream_t s) {
     const int TW = (2 << D) < 4 ? 4 : (2 << D);
     const int tree_bytes = TW * 4;
-    int TC = std::max(1, std::min(std::max(p.n_trees, 1), kChunkBytes / tree_bytes));
+    static const int threads = env_int("TP_K2_THREADS", kDefaultThreads, 64, kMaxThreads, 32);
+    static const int chunk_bytes = env_int("TP_K2_CHUNK_KB", kDefaultChunkBytes / 1024, 4, 100, 1) * 1024;
+    int TC = std::max(1, std::min(std::max(p.n_trees, 1), chunk_bytes / tree_bytes));
     const int nchunks = p.n_trees == 0 ? 0 : (p.n_trees + TC - 1) / TC;
     const int stages = nchunks == 1 ? 1 : 2;
     const size_t smem = (size_t)stages * TC * tree_bytes;
-    auto kern = k2_gbdt<D, RU>;
+    auto kern = k2_gbdt<D, RU, RUNS>;
     int dev = 0, sms = 0, per_sm = 0;
     if (cudaGetDevice(&dev) != cudaSuccess) return TP_ECUDA;
+    if (RUNS) {
+        static bool runs_attr[64] = {};
+        if (dev < 64 && !runs_attr[dev]) {
+            if (cudaFuncSetAttribute(k2_runs, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     (kMaxH + 1) * 4) != cudaSuccess)
+                return TP_ECUDA;
+            runs_attr[dev] = true;
+        }
+        k2_runs<<<p.n_inst, kRunsThreads, (size_t)(p.H + 1) * 4, s>>>(p);
+        if (cudaPeekAtLastError() != cudaSuccess) return TP_ECUDA;
+    }
     if (cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess) return TP_ECUDA;
     if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess)
         return TP_ECUDA;
-    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kThreads, smem) != cudaSuccess) return TP_ECUDA;
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, threads, smem) != cudaSuccess) return TP_ECUDA;
     const int grid = std::max(1, sms * std::max(1, per_sm));
-    kern<<<grid, kThreads, smem, s>>>(p, TC, nchunks);
+    kern<<<grid, threads, smem, s>>>(p, TC, nchunks);
     return cudaPeekAtLastError() == cudaSuccess ? TP_OK : TP_ECUDA;
 }
 
-template <int RU>
+template <int RU, bool RUNS>
 int launch_ru(const K2Params& p, cudaStream_t s) {
     switch (p.depth) {
-        case 0: return launch_d<0, RU>(p, s);
-        case 1: return launch_d<1, RU>(p, s);
-        case 2: return launch_d<2, RU>(p, s);
-        case 3: return launch_d<3, RU>(p, s);
-        case 4: return launch_d<4, RU>(p, s);
-        case 5: return launch_d<5, RU>(p, s);
-        case 6: return launch_d<6, RU>(p, s);
-        case 7: return launch_d<7, RU>(p, s);
-        case 8: return launch_d<8, RU>(p, s);
-        case 9: return launch_d<9, RU>(p, s);
-        case 10: return launch_d<10, RU>(p, s);
-        case 11: return launch_d<11, RU>(p, s);
-        case 12: return launch_d<12, RU>(p, s);
+        case 0: return launch_d<0, RU, RUNS>(p, s);
+        case 1: return launch_d<1, RU, RUNS>(p, s);
+        case 2: return launch_d<2, RU, RUNS>(p, s);
+        case 3: return launch_d<3, RU, RUNS>(p, s);
+        case 4: return launch_d<4, RU, RUNS>(p, s);
+        case 5: return launch_d<5, RU, RUNS>(p, s);
+        case 6: return launch_d<6, RU, RUNS>(p, s);
+        case 7: return launch_d<7, RU, RUNS>(p, s);
+        case 8: return launch_d<8, RU, RUNS>(p, s);
+        case 9: return launch_d<9, RU, RUNS>(p, s);
+        case 10: return launch_d<10, RU, RUNS>(p, s);
+        case 11: return launch_d<11, RU, RUNS>(p, s);
+        case 12: return launch_d<12, RU, RUNS>(p, s);
         default: return TP_EFORMAT;
     }
 }
 
 }  // namespace
 
-int launch_gbdt(const K2Params& p, cudaStream_t s) {
+int launch_gbdt(const K2Params& p, bool runs, cudaStream_t s) {
     if (p.n_inst == 0) return TP_OK;
-    if (p.F <= 2) return launch_ru<2>(p, s);
-    if (p.F <= 4) return launch_ru<4>(p, s);
-    return launch_ru<8>(p, s);
+    if (runs) {
+        if (p.F <= 2) return launch_ru<2, true>(p, s);
+        if (p.F <= 4) return launch_ru<4, true>(p, s);
+        return launch_ru<8, true>(p, s);
+    }
+    if (p.F <= 2) return launch_ru<2, false>(p, s);
+    if (p.F <= 4) return launch_ru<4, false>(p, s);
+    return launch_ru<8, false>(p, s);
+}
+
+size_t runs_workspace_bytes(int32_t n_inst, int32_t H) {
+    const size_t I = (size_t)(n_inst > 0 ? n_inst : 1);
+    return 256 + I * 4 + 2 * I * (size_t)H * 4 + 512;
+}
+
+void runs_workspace_carve(void* ws, int32_t n_inst, int32_t H, K2Params& p) {
+    const size_t I = (size_t)(n_inst > 0 ? n_inst : 1);
+    auto up = [](uintptr_t x) { return (x + 255) & ~(uintptr_t)255; };
+    uintptr_t a = up((uintptr_t)ws);
+    p.run_h = reinterpret_cast<int32_t*>(a);
+    a = up(a + I * 4);
+    p.run_m = reinterpret_cast<int32_t*>(a);
+    a = up(a + I * (size_t)H * 4);
+    p.run_key = reinterpret_cast<uint32_t*>(a);
 }
 
 }  // namespace tp

@@ -61,25 +61,35 @@ k3_select(const tp_inst* __restrict__ inst, const int4* __restrict__ req, const 
         long long* trow = tr ? tr + ((size_t)i * F + u) * H : nullptr;
         long long carry = 0;
         bool ok = true;
-        for (int m0 = 1; m0 <= n; m0 += 32) {
-            const int m = m0 + lane;
-            long long x = 0;
-            if (m <= n) {
-                const float t = __frcp_rn(__ldg(row + m - 1));    // fl32(1 / IPS), reading A-9
-                x = (long long)(t * 0x1p40f);                      // exact: t in [2^-17, 16]
-            }
+        // 4 x 32 iterations per step: the 4 coalesced loads are issued back to back, then scanned
+        for (int m0 = 1; m0 <= n; m0 += 128) {
+            float v[4];
 #pragma unroll
-            for (int o = 1; o < 32; o <<= 1) {
-                const long long y = __shfl_up_sync(0xffffffffu, x, o);
-                if (lane >= o) x += y;
+            for (int j = 0; j < 4; ++j) {
+                const int m = m0 + 32 * j + lane;
+                v[j] = m <= n ? __ldg(row + m - 1) : 1.0f;
             }
-            const long long TR = carry + x;
-            carry = __shfl_sync(0xffffffffu, TR, 31);
             bool bad = false;
-            if (m <= n) {
-                bad = !(TR < dmin[m]);
-                if (m == n) bad |= TR > tbt_bound;
-                if (trow) trow[m - 1] = TR;
+#pragma unroll
+            for (int j = 0; j < 4; ++j) {
+                const int m = m0 + 32 * j + lane;
+                long long x = 0;
+                if (m <= n) {
+                    const float t = __frcp_rn(v[j]);                   // fl32(1 / IPS), reading A-9
+                    x = (long long)(t * 0x1p40f);                      // exact: t in [2^-17, 16]
+                }
+#pragma unroll
+                for (int o = 1; o < 32; o <<= 1) {
+                    const long long y = __shfl_up_sync(0xffffffffu, x, o);
+                    if (lane >= o) x += y;
+                }
+                const long long TR = carry + x;
+                carry = __shfl_sync(0xffffffffu, TR, 31);
+                if (m <= n) {
+                    bad |= !(TR < dmin[m]);
+                    if (m == n) bad |= TR > tbt_bound;
+                    if (trow) trow[m - 1] = TR;
+                }
             }
             if (__any_sync(0xffffffffu, bad)) {
                 ok = false;

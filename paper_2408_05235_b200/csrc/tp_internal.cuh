@@ -53,11 +53,19 @@ struct K2Params {
     float* ips;
     int32_t n_inst, H, F;
     float freq[kMaxF];
+    // run-compressed mode (tp_predict_ips_runs): consecutive iterations with identical
+    // (batch, KV) threshold ranks form a run; the ensemble is evaluated once per run.
+    int32_t* run_h;          // [n_inst] runs per instance (0 for skipped instances)
+    int32_t* run_m;          // [n_inst][H] first iteration m of each run
+    uint32_t* run_key;       // [n_inst][H] rank_B | rank_KV << 16 of each run
 };
+
+size_t runs_workspace_bytes(int32_t n_inst, int32_t H);
+void runs_workspace_carve(void* ws, int32_t n_inst, int32_t H, K2Params& p);
 
 int launch_project(const tp_inst* inst, int32_t n_inst, const tp_req* req, int32_t n_req, int32_t H,
                    int32_t* B, int32_t* KV, int32_t* n, int32_t* n_adm, uint32_t* status, cudaStream_t s);
-int launch_gbdt(const K2Params& p, cudaStream_t s);
+int launch_gbdt(const K2Params& p, bool runs, cudaStream_t s);
 int launch_select(const tp_inst* inst, int32_t n_inst, const tp_req* req, int32_t n_req, const double* t_dead,
                   const int32_t* n, const int32_t* n_adm, const float* ips, int32_t H, int32_t F,
                   int64_t tbt_ticks, int32_t* level, uint32_t* status, int64_t* tr, cudaStream_t s);

@@ -21,7 +21,7 @@ def to_device_bytes(a: np.ndarray, device) -> torch.Tensor:
 class Round:
     """One decision round's device buffers (inputs + K1/K2/K3 outputs)."""
 
-    def __init__(self, inputs: dict, device="cuda:0", want_tr=False):
+    def __init__(self, inputs: dict, device="cuda:0", want_tr=False, k2_mode="runs"):
         dev = torch.device(device)
         self.device = dev
         inst, req, t_dead = inputs["inst"], inputs["req"], inputs["t_dead"]
@@ -43,14 +43,22 @@ class Round:
         self.level = torch.empty(I, dtype=torch.int32, device=dev)
         self.ips = torch.zeros((I, F, H), dtype=torch.float32, device=dev)
         self.tr = torch.zeros((I, F, H), dtype=torch.int64, device=dev) if want_tr else None
+        assert k2_mode in ("runs", "direct")
+        self.k2_mode = k2_mode
+        self.work = torch.empty(tp.tp_predict_ips_workspace_size(I, H), dtype=torch.uint8, device=dev) \
+            if k2_mode == "runs" else None
 
     def project(self, stream=None):
         tp.tp_project(self.inst, self.I, self.req, self.R, self.H, self.B, self.KV, self.n, self.n_adm, self.status,
                       stream)
 
     def predict(self, model, stream=None):
-        tp.tp_predict_ips(model, self.inst, self.I, self.B, self.KV, self.n, self.H, self.freq, self.ips, self.status,
-                          stream)
+        if self.k2_mode == "runs":
+            tp.tp_predict_ips_runs(model, self.inst, self.I, self.B, self.KV, self.n, self.H, self.freq, self.ips,
+                                   self.status, self.work, stream)
+        else:
+            tp.tp_predict_ips(model, self.inst, self.I, self.B, self.KV, self.n, self.H, self.freq, self.ips,
+                              self.status, stream)
 
     def select(self, stream=None):
         tp.tp_select_freq(self.inst, self.I, self.req, self.R, self.t_dead, self.n, self.n_adm, self.ips, self.H,

@@ -20,9 +20,10 @@ ST_EMPTY, ST_BYPASS_LOST, ST_INFEASIBLE, ST_KV_OVER = 1, 2, 4, 8
 ST_QUEUE_BLOCKED, ST_IPS_CLAMPED, ST_BAD_INPUT = 16, 32, 64
 
 # every symbol include/tp.h declares
-EXPORTS = ["tp_gbdt_load", "tp_gbdt_free", "tp_gbdt_get_info", "tp_project", "tp_predict_ips", "tp_select_freq",
-           "tp_ctx_create", "tp_ctx_free", "tp_decide", "tp_decide_host", "tp_ctx_buffers", "tp_strerror",
-           "tp_abi_version"]
+EXPORTS = ["tp_gbdt_load", "tp_gbdt_free", "tp_gbdt_get_info", "tp_project", "tp_predict_ips",
+           "tp_predict_ips_workspace_size", "tp_predict_ips_runs", "tp_runs_total", "tp_select_freq", "tp_ctx_create", "tp_ctx_free",
+           "tp_decide", "tp_decide_host", "tp_ctx_set_k2_mode", "tp_ctx_buffers", "tp_strerror", "tp_abi_version"]
+K2_DIRECT, K2_RUNS = 0, 1
 
 if not os.path.exists(LIB_PATH):
     raise ImportError(f"libtp.so not built ({LIB_PATH}); run __graft_entry__.build()")
@@ -42,6 +43,10 @@ _L.tp_gbdt_free.argtypes = [_vp]
 _L.tp_gbdt_get_info.argtypes = [_vp, ctypes.POINTER(GbdtInfo)]
 _L.tp_project.argtypes = [_vp, _i32, _vp, _i32, _i32, _vp, _vp, _vp, _vp, _vp, _vp]
 _L.tp_predict_ips.argtypes = [_vp, _vp, _i32, _vp, _vp, _vp, _i32, _vp, _i32, _vp, _vp, _vp]
+_L.tp_predict_ips_workspace_size.argtypes = [_i32, _i32]
+_L.tp_predict_ips_runs.argtypes = [_vp, _vp, _i32, _vp, _vp, _vp, _i32, _vp, _i32, _vp, _vp, _vp, ctypes.c_size_t, _vp]
+_L.tp_ctx_set_k2_mode.argtypes = [_vp, ctypes.c_int]
+_L.tp_runs_total.argtypes = [_vp, _i32, _i32, ctypes.POINTER(_i64)]
 _L.tp_select_freq.argtypes = [_vp, _i32, _vp, _i32, _vp, _vp, _vp, _vp, _i32, _i32, _f32, _vp, _vp, _vp, _vp]
 _L.tp_ctx_create.argtypes = [ctypes.c_int, _i32, _i32, _i32, _i32, ctypes.POINTER(_vp)]
 _L.tp_ctx_free.argtypes = [_vp]
@@ -53,6 +58,7 @@ _L.tp_strerror.restype = ctypes.c_char_p
 for _f in EXPORTS:
     if _f != "tp_strerror":
         getattr(_L, _f).restype = ctypes.c_int
+_L.tp_predict_ips_workspace_size.restype = ctypes.c_size_t
 
 
 class TpError(RuntimeError):
@@ -147,6 +153,25 @@ def tp_predict_ips(model: Gbdt, inst, n_inst, B, KV, n, H, freq, ips, status, st
                              F, _dp(ips), _dp(status), _stream(stream)), "tp_predict_ips")
 
 
+def tp_predict_ips_workspace_size(n_inst, H) -> int:
+    return int(_L.tp_predict_ips_workspace_size(int(n_inst), int(H)))
+
+
+def tp_predict_ips_runs(model: Gbdt, inst, n_inst, B, KV, n, H, freq, ips, status, workspace, stream=None):
+    """workspace: a uint8 CUDA tensor of at least tp_predict_ips_workspace_size(n_inst, H) bytes."""
+    f, F = _freq(freq)
+    _check(_L.tp_predict_ips_runs(model.handle, _dp(inst), int(n_inst), _dp(B), _dp(KV), _dp(n), int(H),
+                                  f.ctypes.data, F, _dp(ips), _dp(status), _dp(workspace), workspace.numel(),
+                                  _stream(stream)), "tp_predict_ips_runs")
+
+
+def runs_total(workspace, n_inst, H) -> int:
+    """Runs evaluated by the last tp_predict_ips_runs on ``workspace`` (synchronous diagnostic)."""
+    t = _i64()
+    _check(_L.tp_runs_total(_dp(workspace), int(n_inst), int(H), ctypes.byref(t)), "tp_runs_total")
+    return int(t.value)
+
+
 def tp_select_freq(inst, n_inst, req, n_req, t_dead, n, n_adm, ips, H, F, tbt_slo, level, status, tr_ticks=None,
                    stream=None):
     _check(_L.tp_select_freq(_dp(inst), int(n_inst), _dp(req), int(n_req), _dp(t_dead), _dp(n), _dp(n_adm),
@@ -175,6 +200,9 @@ class Ctx:
         _check(_L.tp_decide_host(self.handle, model.handle, _hp(inst), int(n_inst), _hp(req), int(n_req),
                                  _hp(t_dead), f.ctypes.data, F, float(np.float32(tbt_slo)), _hp(level), _hp(status),
                                  _stream(stream)), "tp_decide_host")
+
+    def set_k2_mode(self, mode):
+        _check(_L.tp_ctx_set_k2_mode(self.handle, int(mode)), "tp_ctx_set_k2_mode")
 
     def buffers(self):
         ptrs = [_vp() for _ in range(5)]

@@ -30,10 +30,16 @@ def gpu():
     return tp, runner
 
 
-def run_gpu(gpu, blob, inputs, want_tr=True, idx=None):
+@pytest.fixture(params=["direct", "runs"])
+def mode(request):
+    """Both K2 variants: tp_predict_ips (direct) and tp_predict_ips_runs (run-compressed)."""
+    return request.param
+
+
+def run_gpu(gpu, blob, inputs, want_tr=True, idx=None, mode="runs"):
     tp, runner = gpu
     model = tp.Gbdt(blob, 0)
-    r = runner.Round(inputs, "cuda:0", want_tr=want_tr)
+    r = runner.Round(inputs, "cuda:0", want_tr=want_tr, k2_mode=mode)
     r.run(model)
     out = r.results(idx)
     del r
@@ -70,54 +76,54 @@ def assert_parity(got, ref, idx=None, grid=True, tr=True, compact=False):
 # ------------------------------------------------------------------ hand-worked W1
 
 @pytest.mark.parametrize("case", [d["case"] for d in cases.load_w1()["decisions"]])
-def test_w1(gpu, oracle_mod, case):
+def test_w1(gpu, oracle_mod, mode, case):
     d = [x for x in cases.load_w1()["decisions"] if x["case"] == case][0]
     ens, inst, req, td, H, freq, tbt = cases.w1_inputs(d)
     inputs = dict(inst=inst, req=req, t_dead=td, H=H, freq=freq, tbt_slo=tbt)
     blob = W.write_blob(ens)
-    got = run_gpu(gpu, blob, inputs)
+    got = run_gpu(gpu, blob, inputs, mode=mode)
     assert int(got["level"][0]) == d["level"] and int(got["status"][0]) == d["status"]
     assert_parity(got, run_oracle(oracle_mod, blob, inputs))
 
 
 # ------------------------------------------------------------------ brute-force scale random cases
 
-def test_tiny_random(gpu, oracle_mod):
+def test_tiny_random(gpu, oracle_mod, mode):
     rng = np.random.default_rng(11)
     for trial in range(150):
         ens, inst, req, td, H, freq, tbt = cases.random_tiny_case(rng)
         inputs = dict(inst=inst, req=req, t_dead=td, H=H, freq=freq, tbt_slo=tbt)
         blob = W.write_blob(ens)
-        assert_parity(run_gpu(gpu, blob, inputs), run_oracle(oracle_mod, blob, inputs, threads=1))
+        assert_parity(run_gpu(gpu, blob, inputs, mode=mode), run_oracle(oracle_mod, blob, inputs, threads=1))
 
 
 # ------------------------------------------------------------------ parity configs (several tiles + ragged tails)
 
 @pytest.mark.parametrize("name", ["P1", "P2"])
-def test_parity_configs(gpu, oracle_mod, name):
+def test_parity_configs(gpu, oracle_mod, mode, name):
     cfg = W.CONFIGS[name]
     blob = W.write_blob(W.config_ensemble(cfg))
     inputs = W.config_inputs(cfg)
-    assert_parity(run_gpu(gpu, blob, inputs), run_oracle(oracle_mod, blob, inputs))
+    assert_parity(run_gpu(gpu, blob, inputs, mode=mode), run_oracle(oracle_mod, blob, inputs))
 
 
-def test_c1_sweep_10k(gpu, oracle_mod):
+def test_c1_sweep_10k(gpu, oracle_mod, mode):
     """BASELINE configs[0] shape, 10^4 instances (one seeded block per 1024)."""
     cfg = dataclasses.replace(W.CONFIGS["C1"], n_inst=10000)
     blob = W.write_blob(W.config_ensemble(cfg))
     inputs = W.config_inputs(cfg)
-    got = run_gpu(gpu, blob, inputs)
+    got = run_gpu(gpu, blob, inputs, mode=mode)
     ref = run_oracle(oracle_mod, blob, inputs)
     assert_parity(got, ref)
     assert len(np.unique(ref["level"])) >= 4          # decisions spread over levels
 
 
-def test_c2_full(gpu, oracle_mod):
+def test_c2_full(gpu, oracle_mod, mode):
     """BASELINE configs[1] at full size: every decision; full grids on a stratified eighth."""
     cfg = W.CONFIGS["C2"]
     blob = W.write_blob(W.config_ensemble(cfg))
     inputs = W.config_inputs(cfg)
-    got = run_gpu(gpu, blob, inputs, want_tr=False)
+    got = run_gpu(gpu, blob, inputs, want_tr=False, mode=mode)
     ref = run_oracle(oracle_mod, blob, inputs, want_grid=False, want_tr=False)
     assert_parity(got, ref, grid=False)
     sub = np.arange(0, cfg.n_inst, 8)
@@ -138,31 +144,31 @@ def _subset(inputs, idx):
 
 
 @pytest.mark.parametrize("name,stride", [("C3", 1024), ("C4", 256)])
-def test_full_size_sampled(gpu, oracle_mod, name, stride):
+def test_full_size_sampled(gpu, oracle_mod, mode, name, stride):
     """BASELINE configs[2]/[3] at full size on the GPU; the oracle recomputes a stratified sample."""
     cfg = W.CONFIGS[name]
     blob = W.write_blob(W.config_ensemble(cfg))
     inputs = W.config_inputs(cfg)
     sub = np.arange(3, cfg.n_inst, stride)
-    got = run_gpu(gpu, blob, inputs, want_tr=False, idx=sub)
+    got = run_gpu(gpu, blob, inputs, want_tr=False, idx=sub, mode=mode)
     assert_parity(got, run_oracle(oracle_mod, blob, _subset(inputs, sub), want_tr=False), idx=sub, tr=False,
                   compact=True)
 
 
 # ------------------------------------------------------------------ edge cases
 
-def test_empty_batch(gpu, oracle_mod):
+def test_empty_batch(gpu, oracle_mod, mode):
     cfg = W.CONFIGS["P1"]
     blob = W.write_blob(W.config_ensemble(cfg))
     inputs = dict(W.config_inputs(cfg), inst=np.zeros(0, W.INST_DTYPE), req=np.zeros(0, W.REQ_DTYPE),
                   t_dead=np.zeros(0))
-    got = run_gpu(gpu, blob, inputs)
+    got = run_gpu(gpu, blob, inputs, mode=mode)
     assert got["level"].shape == (0,)
 
 
 @pytest.mark.parametrize("F,H,N,depth,n_trees", [(1, 1, 1, 0, 3), (32, 37, 1, 3, 9), (3, 300, 2, 12, 4),
                                                  (17, 65, 128, 1, 0), (32, 1024, 64, 8, 33), (2, 33, 3, 5, 120)])
-def test_shapes(gpu, oracle_mod, F, H, N, depth, n_trees):
+def test_shapes(gpu, oracle_mod, mode, F, H, N, depth, n_trees):
     """Degenerate and maximal shapes: F = 1 / 32, H = 1 (one iteration), N = 1 (a block per
     token), depth 0 (stumps-free constant trees) and 12 (deepest), zero trees, ragged tails."""
     cfg = dataclasses.replace(W.CONFIGS["P1"], n_inst=70, H=H, F=F, N=N, n_trees=n_trees, depth=depth,
@@ -170,10 +176,10 @@ def test_shapes(gpu, oracle_mod, F, H, N, depth, n_trees):
     ens = W.gen_ensemble(n_trees, depth, 7 + depth, W.freq_levels(F), b_max=40, kv_max=4000, ragged=True)
     blob = W.write_blob(ens)
     inputs = W.config_inputs(cfg)
-    assert_parity(run_gpu(gpu, blob, inputs), run_oracle(oracle_mod, blob, inputs))
+    assert_parity(run_gpu(gpu, blob, inputs, mode=mode), run_oracle(oracle_mod, blob, inputs))
 
 
-def test_many_thresholds(gpu, oracle_mod):
+def test_many_thresholds(gpu, oracle_mod, mode):
     """> 255 distinct thresholds per feature (16-bit ranks) and thresholds equal to feature values."""
     rng = np.random.default_rng(5)
     freq = W.freq_levels(12)
@@ -203,10 +209,10 @@ def test_many_thresholds(gpu, oracle_mod):
     assert info.n_cuts[2] > 255
     cfg = dataclasses.replace(W.CONFIGS["P2"], n_inst=50, F=12, seed=91)
     inputs = W.config_inputs(cfg)
-    assert_parity(run_gpu(gpu, blob, inputs), run_oracle(oracle_mod, blob, inputs))
+    assert_parity(run_gpu(gpu, blob, inputs, mode=mode), run_oracle(oracle_mod, blob, inputs))
 
 
-def test_clamp_and_bad_input(gpu, oracle_mod):
+def test_clamp_and_bad_input(gpu, oracle_mod, mode):
     ens = cases.ensemble_from_nodes([{"feature": 1, "threshold": 2.0, "left": 1, "right": 2},
                                      {"feature": -1, "leaf": -5.0}, {"feature": -1, "leaf": 1e9}])
     inst, req, td = cases.make_instances([dict(N=16, running=[(0, 5, 3, 0, 1e9), (0, 5, 1, 0, 1e9)]),
@@ -218,13 +224,14 @@ def test_clamp_and_bad_input(gpu, oracle_mod):
     req[4]["a"] = 2          # queued entry with a != 0 -> BAD_INPUT
     inputs = dict(inst=inst, req=req, t_dead=td, H=4, freq=np.array([1000.0, 1200.0], np.float32), tbt_slo=16.0)
     blob = W.write_blob(ens)
-    got = run_gpu(gpu, blob, inputs)
+    got = run_gpu(gpu, blob, inputs, mode=mode)
     assert_parity(got, run_oracle(oracle_mod, blob, inputs))
     assert got["status"][0] & 32 and got["status"].tolist()[1:] == [64, 64, 64, 1]
 
 
-def test_decide_entry_points_agree(gpu, oracle_mod):
-    """tp_decide (device) and tp_decide_host (host buffers, e2e path) == the three calls."""
+@pytest.mark.parametrize("k2", [0, 1])
+def test_decide_entry_points_agree(gpu, oracle_mod, k2):
+    """tp_decide (device) and tp_decide_host (host buffers, e2e path) == the oracle, both K2 modes."""
     tp, runner = gpu
     cfg = W.CONFIGS["P2"]
     blob = W.write_blob(W.config_ensemble(cfg))
@@ -233,6 +240,7 @@ def test_decide_entry_points_agree(gpu, oracle_mod):
     model = tp.Gbdt(blob, 0)
     I, R = len(inputs["inst"]), len(inputs["req"])
     ctx = tp.Ctx(0, I, R, inputs["H"], len(inputs["freq"]))
+    ctx.set_k2_mode(k2)
     r = runner.Round(inputs, "cuda:0")
     ctx.decide(model, r.inst, I, r.req, R, r.t_dead, inputs["freq"], inputs["tbt_slo"], r.level, r.status)
     torch.cuda.synchronize()
@@ -245,6 +253,19 @@ def test_decide_entry_points_agree(gpu, oracle_mod):
     torch.cuda.synchronize()
     assert np.array_equal(h_level.numpy(), ref["level"])
     assert np.array_equal(h_status.numpy().view(np.uint32), ref["status"])
+
+
+def test_runs_are_fewer_than_grid_rows(gpu, oracle_mod):
+    """The run compression is real on the C2 workload (and exact, by the parity tests)."""
+    tp, runner = gpu
+    cfg = W.CONFIGS["C2"]
+    model = tp.Gbdt(W.write_blob(W.config_ensemble(cfg)), 0)
+    r = runner.Round(W.config_inputs(cfg), "cuda:0", k2_mode="runs")
+    r.run(model)
+    torch.cuda.synchronize()
+    runs = tp.runs_total(r.work, r.I, r.H)
+    rows = int(r.n.cpu().numpy().astype(np.int64)[(r.status.cpu().numpy() & SKIP) == 0].sum())
+    assert 0 < runs < rows / 3
 
 
 def test_concurrent_streams_share_model(gpu, oracle_mod):

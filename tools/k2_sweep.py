@@ -1,17 +1,16 @@
-"""Time K2 (tp_predict_ips) alone on a workload; env knobs TP_K2_THREADS / TP_K2_CHUNK_KB are
-read by libtp at first launch, so each setting runs in its own process.
-Usage (GPU box): python tools/k2_sweep.py C2 [reps]"""
+"""Time the K2 variants alone on a workload; env knobs TP_K2_THREADS / TP_K2_CHUNK_KB are read by
+libtp at first launch, so each setting runs in its own process.
+Usage (GPU box): python tools/k2_sweep.py C2 [reps] [mode]"""
 import json, os, subprocess, sys
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path.insert(0, ROOT)
 
-def one(wl, reps):
+def one(wl, reps, mode):
     import torch
-    import numpy as np
     from paper_2408_05235_b200 import runner, tp, workload as W
     cfg = W.CONFIGS[wl]
     model = tp.Gbdt(W.write_blob(W.config_ensemble(cfg)), 0)
-    r = runner.Round(W.config_inputs(cfg), "cuda:0")
+    r = runner.Round(W.config_inputs(cfg), "cuda:0", k2_mode=mode)
     r.project(); r.predict(model); torch.cuda.synchronize()
     ev = [torch.cuda.Event(enable_timing=True) for _ in range(2 * reps)]
     for k in range(reps):
@@ -22,13 +21,14 @@ def one(wl, reps):
 
 if __name__ == "__main__":
     if os.environ.get("K2_SWEEP_CHILD"):
-        print(json.dumps({"ms": one(sys.argv[1], int(sys.argv[2]))}))
+        print(json.dumps({"ms": one(sys.argv[1], int(sys.argv[2]), sys.argv[3])}))
         sys.exit(0)
     wl = sys.argv[1] if len(sys.argv) > 1 else "C2"
     reps = int(sys.argv[2]) if len(sys.argv) > 2 else 20
-    for th in [256, 384]:
-        for ck in [24, 32, 48]:
+    mode = sys.argv[3] if len(sys.argv) > 3 else "runs"
+    for th in [128, 256, 384]:
+        for ck in [16, 32, 48]:
             env = dict(os.environ, K2_SWEEP_CHILD="1", TP_K2_THREADS=str(th), TP_K2_CHUNK_KB=str(ck))
-            out = subprocess.run([sys.executable, __file__, wl, str(reps)], env=env, capture_output=True, text=True)
+            out = subprocess.run([sys.executable, __file__, wl, str(reps), mode], env=env, capture_output=True, text=True)
             line = [l for l in out.stdout.splitlines() if l.startswith("{")]
-            print(wl, "threads", th, "chunk_kb", ck, line[-1] if line else out.stderr[-300:], flush=True)
+            print(wl, mode, "threads", th, "chunk_kb", ck, line[-1] if line else out.stderr[-300:], flush=True)
