@@ -174,8 +174,8 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--e2e-steps", type=int, default=None)
-    ap.add_argument("--k2", default="runs", choices=["runs", "direct"],
-                    help="K2 variant: run-compressed (default) or one evaluation per grid point")
+    ap.add_argument("--k2", default="cells", choices=["cells", "runs", "direct"],
+                    help="K2 variant: cell-memoised (default), run-compressed, or one evaluation per grid point")
     args = ap.parse_args()
     cfg = W.CONFIGS[args.workload]
     if args.impl == "reference":
@@ -219,7 +219,7 @@ def main():
     I, R = len(inputs["inst"]), len(inputs["req"])
     model = tp.Gbdt(blob, local)
     info = model.info()
-    rnd = runner.Round(inputs, dev, k2_mode=args.k2)
+    rnd = runner.Round(inputs, dev, k2_mode=args.k2, model=model)
     dec = torch.empty((2, max(I, 1)), dtype=torch.int32, device=dev)   # level, status rows
     rnd.level, rnd.status = dec[0], dec[1]
     # equal shards (C2 weak, C5 = 262144 / {1,2,4,8}): one preallocated all-gather of [2, I] rows
@@ -258,7 +258,9 @@ def main():
     st_h = rnd.status[:I].cpu().numpy().view(np.uint32)
     grid = int((n_h * ((st_h & SKIP) == 0)).sum()) * rnd.F
     padded = int((((n_h + 31) // 32) * 32 * ((st_h & SKIP) == 0)).sum()) * rnd.F
-    evaluated = tp.runs_total(rnd.work, I, rnd.H) * rnd.F if args.k2 == "runs" else grid
+    evaluated = {"runs": lambda: tp.runs_total(rnd.work, I, rnd.H) * rnd.F,
+                 "cells": lambda: tp.cells_total(rnd.work, model, I, rnd.H, rnd.F) * rnd.F,
+                 "direct": lambda: grid}[args.k2]()
 
     evs = [[torch.cuda.Event(enable_timing=True) for _ in range(5)] for _ in range(args.steps)]
     clocks = Clocks(local)
@@ -279,7 +281,7 @@ def main():
     k_ms = per.mean(axis=0)
     # the north_star's direct K2 (one descent per grid point), timed on the same inputs for reference
     d_ms = None
-    if args.k2 == "runs":
+    if args.k2 != "direct":
         rd = runner.Round(inputs, dev, k2_mode="direct")
         rd.project(stream)
         rd.predict(model, stream)
@@ -307,7 +309,8 @@ def main():
     # end to end through the C ABI with host buffers (pinned), copies inside the timed region
     e2e = None
     if True:
-        ctx = tp.Ctx(local, I, R, rnd.H, rnd.F)
+        ctx = tp.Ctx(local, I, R, rnd.H, rnd.F, model if args.k2 == "cells" else None)
+        ctx.set_k2_mode(tp.K2_DIRECT if args.k2 == "direct" else tp.K2_RUNS)
         h_inst = torch.from_numpy(inputs["inst"].view(np.uint8)).pin_memory()
         h_req = torch.from_numpy(inputs["req"].view(np.uint8)).pin_memory()
         h_td = torch.from_numpy(inputs["t_dead"]).pin_memory()
@@ -356,7 +359,8 @@ def main():
             traffic = tj.get("dram_bytes_per_launch")
     except (OSError, ValueError):
         pass
-    roof = {"bound": "smem", "kernel": "k2_gbdt" + ("<runs> (+ k2_runs pre-pass)" if args.k2 == "runs" else ""),
+    roof = {"bound": "smem", "kernel": {"direct": "k2_gbdt", "runs": "k2_gbdt<runs> (+ k2_runs pre-pass)",
+                                        "cells": "k2_gbdt<cells> (+ k2_runs pre-pass, k2_expand)"}[args.k2],
             "achieved": achieved, "peak": peak, "unit": "GB/s",
             "frac": achieved / peak, "traffic": traffic,
             "peak_basis": f"{sms} SMs x 128 B/clk (LDS) x sm_max_mhz {smax:.0f} (MEASURED_PEAKS.json clock)",

@@ -165,13 +165,16 @@ int tp_predict_ips(const tp_gbdt* m, const tp_inst* inst, int32_t n_inst, const 
  * m only through the features (B[m], KV[m]) and, for a given ensemble, only through their ranks
  * among the ensemble's thresholds; consecutive iterations with equal ranks ("runs", typically
  * 5-10 iterations long: KV grows by about B/N blocks per iteration) therefore share one IPS value
- * exactly.  A first kernel builds each instance's runs, the ensemble is evaluated once per
- * (run, level), and the value is written to every iteration of the run.
- *   workspace [dev] scratch of at least tp_predict_ips_workspace_size(n_inst, H) bytes, owned by
- *             the caller, not used concurrently by another call.
+ * exactly.  A first kernel builds each instance's runs; the ensemble is then evaluated once per
+ * (run, level) -- or, in cell mode, once per distinct (rank_tp, rank_B, rank_KV) cell and level
+ * across the whole batch into a lookup table that a last kernel expands onto every iteration.
+ *   workspace [dev] scratch owned by the caller, not used concurrently by another call:
+ *             >= tp_predict_ips_workspace_size(m, n_inst, H, F) bytes enables cell mode (used when
+ *             the model's dense cell space (n_cuts[0]+1)(n_cuts[1]+1)(n_cuts[2]+1) <= 2^22);
+ *             >= tp_predict_ips_workspace_size(NULL, n_inst, H, F) bytes gives run mode.
  * Other arguments, outputs and errors: as tp_predict_ips.
  */
-size_t tp_predict_ips_workspace_size(int32_t n_inst, int32_t H);
+size_t tp_predict_ips_workspace_size(const tp_gbdt* m, int32_t n_inst, int32_t H, int32_t F);
 int tp_predict_ips_runs(const tp_gbdt* m, const tp_inst* inst, int32_t n_inst, const int32_t* B,
                         const int32_t* KV, const int32_t* n, int32_t H, const float* freq_mhz,
                         int32_t F, float* ips, uint32_t* status, void* workspace,
@@ -180,6 +183,10 @@ int tp_predict_ips_runs(const tp_gbdt* m, const tp_inst* inst, int32_t n_inst, c
 /* Diagnostics (synchronous, not for the hot path): total number of runs the last
  * tp_predict_ips_runs call on `workspace` evaluated (per level). */
 int tp_runs_total(const void* workspace, int32_t n_inst, int32_t H, int64_t* total);
+/* ... and the number of distinct cells evaluated in cell mode (0 in run mode); `workspace` sized
+ * by tp_predict_ips_workspace_size(m, n_inst, H, F). */
+int tp_cells_total(const tp_gbdt* m, const void* workspace, int32_t n_inst, int32_t H, int32_t F,
+                   int64_t* total);
 
 /*
  * K3 -- SLO scan and frequency choice (Eq. 3-4; throttle P:550-557).
@@ -205,11 +212,12 @@ int tp_select_freq(const tp_inst* inst, int32_t n_inst, const tp_req* req, int32
 /*
  * Convenience: one decision round with library-owned scratch.
  * tp_ctx_create allocates, on `device`, B/KV/n/n_adm (n_inst_max x H), the ips grid
- * (n_inst_max x F_max x H), the run workspace and staging for up to n_req_max requests.
+ * (n_inst_max x F_max x H), the K2 workspace (sized for `model`'s cell mode; NULL = run mode)
+ * and staging for up to n_req_max requests.
  */
 typedef struct tp_ctx tp_ctx;
-int tp_ctx_create(int device, int32_t n_inst_max, int32_t n_req_max, int32_t H, int32_t F_max,
-                  tp_ctx** out);
+int tp_ctx_create(int device, const tp_gbdt* model, int32_t n_inst_max, int32_t n_req_max, int32_t H,
+                  int32_t F_max, tp_ctx** out);
 int tp_ctx_free(tp_ctx* c);
 
 /* K1 -> K2 -> K3 on device-resident inputs; level/status [dev] out. */

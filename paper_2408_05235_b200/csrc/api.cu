@@ -87,9 +87,9 @@ int tp_predict_ips(const tp_gbdt* m, const tp_inst* inst, int32_t n_inst, const 
     return tp::launch_gbdt(p, false, S(stream));
 }
 
-size_t tp_predict_ips_workspace_size(int32_t n_inst, int32_t H) {
-    if (n_inst < 0 || !H_ok(H)) return 0;
-    return tp::runs_workspace_bytes(n_inst, H);
+size_t tp_predict_ips_workspace_size(const tp_gbdt* m, int32_t n_inst, int32_t H, int32_t F) {
+    if (n_inst < 0 || !H_ok(H) || F < 1 || F > tp::kMaxF) return 0;
+    return tp::runs_workspace_bytes(m ? tp::model_cells(m->m) : 0, n_inst, H, F);
 }
 
 int tp_predict_ips_runs(const tp_gbdt* m, const tp_inst* inst, int32_t n_inst, const int32_t* B, const int32_t* KV,
@@ -97,7 +97,9 @@ int tp_predict_ips_runs(const tp_gbdt* m, const tp_inst* inst, int32_t n_inst, c
                         void* workspace, size_t workspace_bytes, void* stream) {
     if (!m || n_inst < 0 || !H_ok(H) || !freq_ok(freq_mhz, F)) return TP_EINVAL;
     if (n_inst > 0 && (!inst || !B || !KV || !n || !ips || !status || !workspace)) return TP_EINVAL;
-    if (n_inst > 0 && workspace_bytes < tp::runs_workspace_bytes(n_inst, H)) return TP_EINVAL;
+    const int64_t cells = tp::model_cells(m->m);
+    const bool use_cells = workspace_bytes >= tp::runs_workspace_bytes(cells, n_inst, H, F);
+    if (n_inst > 0 && workspace_bytes < tp::runs_workspace_bytes(0, n_inst, H, F)) return TP_EINVAL;
     tp::K2Params p;
     std::memset(&p, 0, sizeof(p));
     p.words = m->m.d_words;
@@ -116,7 +118,7 @@ int tp_predict_ips_runs(const tp_gbdt* m, const tp_inst* inst, int32_t n_inst, c
     p.H = H;
     p.F = F;
     for (int u = 0; u < F; ++u) p.freq[u] = freq_mhz[u];
-    if (n_inst > 0) tp::runs_workspace_carve(workspace, n_inst, H, p);
+    if (n_inst > 0) tp::runs_workspace_carve(workspace, use_cells ? cells : 0, n_inst, H, F, p);
     return tp::launch_gbdt(p, true, S(stream));
 }
 
@@ -126,13 +128,26 @@ int tp_runs_total(const void* workspace, int32_t n_inst, int32_t H, int64_t* tot
     if (n_inst == 0) return TP_OK;
     tp::K2Params p;
     std::memset(&p, 0, sizeof(p));
-    tp::runs_workspace_carve(const_cast<void*>(workspace), n_inst, H, p);
+    tp::runs_workspace_carve(const_cast<void*>(workspace), 0, n_inst, H, 1, p);
     int32_t* h = new (std::nothrow) int32_t[n_inst];
     if (!h) return TP_ENOMEM;
     const bool ok = cudaMemcpy(h, p.run_h, (size_t)n_inst * 4, cudaMemcpyDeviceToHost) == cudaSuccess;
     for (int32_t i = 0; ok && i < n_inst; ++i) *total += h[i];
     delete[] h;
     return ok ? TP_OK : TP_ECUDA;
+}
+
+int tp_cells_total(const tp_gbdt* m, const void* workspace, int32_t n_inst, int32_t H, int32_t F, int64_t* total) {
+    if (!m || !workspace || !total || n_inst < 0 || !H_ok(H) || F < 1 || F > tp::kMaxF) return TP_EINVAL;
+    *total = 0;
+    tp::K2Params p;
+    std::memset(&p, 0, sizeof(p));
+    tp::runs_workspace_carve(const_cast<void*>(workspace), tp::model_cells(m->m), n_inst, H, F, p);
+    if (!p.cell_count || n_inst == 0) return TP_OK;
+    int32_t c = 0;
+    if (cudaMemcpy(&c, p.cell_count, 4, cudaMemcpyDeviceToHost) != cudaSuccess) return TP_ECUDA;
+    *total = c;
+    return TP_OK;
 }
 
 int tp_select_freq(const tp_inst* inst, int32_t n_inst, const tp_req* req, int32_t n_req, const double* t_dead,
@@ -146,7 +161,8 @@ int tp_select_freq(const tp_inst* inst, int32_t n_inst, const tp_req* req, int32
                              tr_ticks, S(stream));
 }
 
-int tp_ctx_create(int device, int32_t n_inst_max, int32_t n_req_max, int32_t H, int32_t F_max, tp_ctx** out) {
+int tp_ctx_create(int device, const tp_gbdt* model, int32_t n_inst_max, int32_t n_req_max, int32_t H, int32_t F_max,
+                  tp_ctx** out) {
     if (!out || n_inst_max < 0 || n_req_max < 0 || !H_ok(H) || F_max < 1 || F_max > tp::kMaxF) return TP_EINVAL;
     *out = nullptr;
     tp_ctx* c = new (std::nothrow) tp_ctx();
@@ -169,7 +185,8 @@ int tp_ctx_create(int device, int32_t n_inst_max, int32_t n_req_max, int32_t H, 
               cudaMalloc(&c->n, I * 4) == cudaSuccess && cudaMalloc(&c->n_adm, I * 4) == cudaSuccess &&
               cudaMalloc(&c->level, I * 4) == cudaSuccess && cudaMalloc(&c->status, I * 4) == cudaSuccess &&
               cudaMalloc(&c->ips, I * F_max * H * 4) == cudaSuccess &&
-              cudaMalloc(&c->work, c->work_bytes = tp::runs_workspace_bytes((int32_t)I, H)) == cudaSuccess &&
+              cudaMalloc(&c->work, c->work_bytes = tp::runs_workspace_bytes(model ? tp::model_cells(model->m) : 0,
+                                                                            (int32_t)I, H, F_max)) == cudaSuccess &&
               cudaMalloc(&c->inst, I * sizeof(tp_inst)) == cudaSuccess &&
               cudaMalloc(&c->req, R * sizeof(tp_req)) == cudaSuccess &&
               cudaMalloc(&c->t_dead, R * sizeof(double)) == cudaSuccess;

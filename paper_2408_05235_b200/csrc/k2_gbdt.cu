@@ -26,8 +26,8 @@ namespace {
 
 constexpr int kMaxThreads = 384;        // CTA size is a launch parameter (256 or 384 threads)
 constexpr int kMaxWarps = kMaxThreads / 32;
-constexpr int kDefaultThreads = 384;
-constexpr int kDefaultChunkBytes = 48 * 1024;
+constexpr int kDefaultThreads = 384, kDefaultThreadsRuns = 128;              // measured best (C2, C3)
+constexpr int kDefaultChunkBytes = 48 * 1024, kDefaultChunkBytesRuns = 16 * 1024;
 constexpr uint32_t kSkip = TP_ST_BAD_INPUT | TP_ST_EMPTY | TP_ST_BYPASS_LOST;
 
 __device__ __forceinline__ uint32_t smem_addr(const void* p) {
@@ -101,20 +101,26 @@ __device__ __forceinline__ uint32_t rank_of(const float* __restrict__ c, int cnt
     return (uint32_t)lo;
 }
 
-// Work units of instance i.  Direct mode: one unit = one warp tile = 32 consecutive iterations x
-// RU levels, ceil(n/32) * G units.  Run mode: one unit = one lane task = one run x RU levels,
-// h * G units, packed 32 per warp tile across instance boundaries (no padding).
-template <bool RUNS>
+
+enum Mode : int { kDirect = 0, kRuns = 1, kCells = 2 };
+
+// Work units.  Direct: one unit = one warp tile = 32 consecutive iterations x RU levels of one
+// instance (ceil(n/32) * G units per instance).  Runs: one unit = one lane task = one run x RU
+// levels (h * G per instance), packed 32 per warp tile across instance boundaries.  Cells: one unit
+// = one distinct cell x RU levels (n_cells * G in total), no instance structure.
+template <int MODE>
 __device__ __forceinline__ int64_t units_of(const K2Params& p, int i, int G) {
     if (p.status[i] & kSkip) return 0;
-    return RUNS ? (int64_t)p.run_h[i] * G : (int64_t)((p.n[i] + 31) >> 5) * G;
+    return MODE == kRuns ? (int64_t)p.run_h[i] * G : (int64_t)((p.n[i] + 31) >> 5) * G;
 }
 
-// K2a (run mode only): per instance, the runs of consecutive iterations m whose (batch, KV)
+// ---------------------------------------------------------------------------------------------
+// K2a (runs / cells): per instance, the runs of consecutive iterations m whose (batch, KV)
 // features have the same ranks among the ensemble's thresholds -- M is constant on each run
 // because tp and f are fixed per (instance, level).  One CTA per instance: keys for all m in
 // shared memory (cut lists staged in shared memory when they fit), then a block-wide ballot
-// compaction of the run heads.
+// compaction of the run heads.  Cell mode also claims each run's cell (rank_tp, rank_B,
+// rank_KV) in a dense table and appends first-seen cells to the cell list.
 constexpr int kRunsThreads = 256;
 constexpr int kRunsCutCap = 2048;     // cuts per feature staged in shared memory (else global)
 
@@ -146,12 +152,18 @@ k2_runs(const __grid_constant__ K2Params p) {
     if (smKV)
         for (int j = tid; j < nKV; j += kRunsThreads) scKV[j] = p.cuts[p.cut_off[2] + j];
     __syncthreads();
+    const bool cells = p.cell_tab != nullptr;
+    uint32_t cell_base = 0;
+    if (cells) {
+        const uint32_t rtp = rank_of(p.cuts + p.cut_off[0], p.cut_off[1] - p.cut_off[0], (float)p.inst[i].tp);
+        cell_base = rtp * (uint32_t)(nB + 1) * (uint32_t)(nKV + 1);
+    }
     const size_t row = (size_t)i * p.H;
     for (int m = 1 + tid; m <= n; m += kRunsThreads) {
         const float b = (float)p.B[row + m - 1], kv = (float)p.KV[row + m - 1];
         const uint32_t rb = smB ? rank_smem(scB, nB, b) : rank_of(p.cuts + p.cut_off[1], nB, b);
         const uint32_t rk = smKV ? rank_smem(scKV, nKV, kv) : rank_of(p.cuts + p.cut_off[2], nKV, kv);
-        skey[m] = rb | (rk << 16);
+        skey[m] = cells ? cell_base + rb * (uint32_t)(nKV + 1) + rk : (rb | (rk << 16));
     }
     __syncthreads();
     int base = 0;
@@ -165,8 +177,16 @@ k2_runs(const __grid_constant__ K2Params p) {
         for (int w = 0; w < warp; ++w) before += swarp[w];
         if (head) {
             const int pos = before + __popc(mask & ((1u << lane) - 1u));
+            const uint32_t key = skey[m];
             p.run_m[row + pos] = m;
-            p.run_key[row + pos] = skey[m];
+            p.run_key[row + pos] = key;
+            // first claimant of a cell appends it to the list; the LUT row index is published in
+            // cell_tab after the claim and read only by later kernels
+            if (cells && __ldcg(p.cell_tab + key) == -1 && atomicCAS(p.cell_tab + key, -1, -2) == -1) {
+                const int idx = atomicAdd(p.cell_count, 1);
+                p.cell_list[idx] = key;
+                p.cell_tab[key] = idx;
+            }
         }
         for (int w = 0; w < kRunsThreads / 32; ++w) base += swarp[w];
         __syncthreads();
@@ -174,7 +194,46 @@ k2_runs(const __grid_constant__ K2Params p) {
     if (tid == 0) p.run_h[i] = base;
 }
 
-template <int D, int RU, bool RUNS>
+// ---------------------------------------------------------------------------------------------
+// K2c (cells): every iteration of every run gets its cell's LUT row; IPS_CLAMPED from the
+// per-cell clamp masks.  One CTA per instance; run starts in shared memory; the stores of one
+// level are coalesced over consecutive iterations.
+constexpr int kExpandThreads = 256;
+
+__global__ void __launch_bounds__(kExpandThreads)
+k2_expand(const __grid_constant__ K2Params p) {
+    extern __shared__ int sx[];     // [h] run starts, [h] LUT rows
+    const int i = blockIdx.x, tid = threadIdx.x;
+    const int h = p.run_h[i];
+    if (h == 0) return;
+    const int n = p.n[i];
+    const size_t row = (size_t)i * p.H;
+    int* sm = sx;
+    int* sidx = sx + h;
+    bool clamped = false;
+    for (int k = tid; k < h; k += kExpandThreads) {
+        sm[k] = p.run_m[row + k];
+        const int idx = p.cell_tab[p.run_key[row + k]];
+        sidx[k] = idx;
+        clamped |= p.cell_clamp[idx] != 0;
+    }
+    if (__syncthreads_or(clamped) && tid == 0) atomicOr(p.status + i, (uint32_t)TP_ST_IPS_CLAMPED);
+    const int F = p.F;
+    for (int m = 1 + tid; m <= n; m += kExpandThreads) {
+        int lo = 0, hi = h;     // last run with start <= m
+        while (hi - lo > 1) {
+            const int mid = (lo + hi) >> 1;
+            if (sm[mid] <= m) lo = mid;
+            else hi = mid;
+        }
+        const float* lrow = p.lut + (size_t)sidx[lo] * F;
+        for (int u = 0; u < F; ++u) p.ips[(row * F) + (size_t)u * p.H + (m - 1)] = __ldg(lrow + u);
+    }
+}
+
+// ---------------------------------------------------------------------------------------------
+// K2b: tree-ensemble evaluation (all modes)
+template <int D, int RU, int MODE>
 __global__ void __launch_bounds__(kMaxThreads, 2)
 k2_gbdt(const __grid_constant__ K2Params p, int TC, int nchunks) {
     extern __shared__ __align__(128) uint32_t sw[];
@@ -185,56 +244,71 @@ k2_gbdt(const __grid_constant__ K2Params p, int TC, int nchunks) {
     __shared__ uint32_t s_rf[kMaxF];
 
     constexpr int TW = (2 << D) < 4 ? 4 : (2 << D);    // words per tree (>= 16 B for TMA)
+    constexpr int UPT = MODE == kDirect ? 1 : 32;      // units per warp tile
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int nthreads = blockDim.x, nwarps = nthreads >> 5;
     const int G = (p.F + RU - 1) / RU;
     const int I = p.n_inst;
-    constexpr int UPT = RUNS ? 32 : 1;            // units per warp tile
     const bool resident = nchunks == 1;
     const int stages = resident ? 1 : 2;
     const int chunk_words = TC * TW;
+    const float* cutsB = p.cuts + p.cut_off[1];
+    const float* cutsKV = p.cuts + p.cut_off[2];
+    const float* cutsTP = p.cuts + p.cut_off[0];
+    const int nB = p.cut_off[2] - p.cut_off[1], nKV = p.cut_off[3] - p.cut_off[2], nTP = p.cut_off[1] - p.cut_off[0];
 
     if (tid < p.F)
         s_rf[tid] = rank_of(p.cuts + p.cut_off[3], p.cut_off[4] - p.cut_off[3], p.freq[tid]);
 
     // ---- split the tile space [0, ceil(U / UPT)) evenly over CTAs ----
     int64_t U = 0;
-    for (int i = tid; i < I; i += nthreads) U += units_of<RUNS>(p, i, G);
-    for (int o = 16; o; o >>= 1) U += __shfl_xor_sync(0xffffffffu, U, o);
-    if (lane == 0) red[warp] = U;
-    __syncthreads();
-    U = 0;
-    for (int k = 0; k < nwarps; ++k) U += red[k];
+    int ncell = 0;
+    if constexpr (MODE == kCells) {
+        ncell = *p.cell_count;
+        U = (int64_t)ncell * G;
+    } else {
+        for (int i = tid; i < I; i += nthreads) U += units_of<MODE>(p, i, G);
+        for (int o = 16; o; o >>= 1) U += __shfl_xor_sync(0xffffffffu, U, o);
+        if (lane == 0) red[warp] = U;
+        __syncthreads();
+        U = 0;
+        for (int k = 0; k < nwarps; ++k) U += red[k];
+    }
     const int64_t ntiles = (U + UPT - 1) / UPT;
     const int64_t t0 = ntiles * blockIdx.x / gridDim.x, t1 = ntiles * (blockIdx.x + 1) / gridDim.x;
     if (t0 >= t1) return;   // uniform: no work for this CTA
     const int64_t u_first = t0 * UPT;
 
     // locate the instance holding unit u_first (block-wide scan over instances, chunk by chunk)
-    if (tid == 0) s_start_i = -1;
+    if (tid == 0) {
+        s_start_i = MODE == kCells ? 0 : -1;
+        s_start_pc = 0;
+    }
     __syncthreads();
-    int64_t base_pc = 0;
-    for (int c0 = 0; c0 < I; c0 += nthreads) {
-        const int i = c0 + tid;
-        const int64_t v = i < I ? units_of<RUNS>(p, i, G) : 0;
-        int64_t x = v;
-        for (int o = 1; o < 32; o <<= 1) {
-            const int64_t y = __shfl_up_sync(0xffffffffu, x, o);
-            if (lane >= o) x += y;
+    if constexpr (MODE != kCells) {
+        int64_t base_pc = 0;
+        for (int c0 = 0; c0 < I; c0 += nthreads) {
+            const int i = c0 + tid;
+            const int64_t v = i < I ? units_of<MODE>(p, i, G) : 0;
+            int64_t x = v;
+            for (int o = 1; o < 32; o <<= 1) {
+                const int64_t y = __shfl_up_sync(0xffffffffu, x, o);
+                if (lane >= o) x += y;
+            }
+            __syncthreads();
+            if (lane == 31) red[warp] = x;
+            __syncthreads();
+            int64_t pre = base_pc;
+            for (int k = 0; k < warp; ++k) pre += red[k];
+            const int64_t incl = pre + x, excl = incl - v;
+            if (i < I && v > 0 && excl <= u_first && u_first < incl) {
+                s_start_i = i;
+                s_start_pc = excl;
+            }
+            for (int k = 0; k < nwarps; ++k) base_pc += red[k];
+            __syncthreads();
+            if (s_start_i >= 0) break;
         }
-        __syncthreads();
-        if (lane == 31) red[warp] = x;
-        __syncthreads();
-        int64_t pre = base_pc;
-        for (int k = 0; k < warp; ++k) pre += red[k];
-        const int64_t incl = pre + x, excl = incl - v;
-        if (i < I && v > 0 && excl <= u_first && u_first < incl) {
-            s_start_i = i;
-            s_start_pc = excl;
-        }
-        for (int k = 0; k < nwarps; ++k) base_pc += red[k];
-        __syncthreads();
-        if (s_start_i >= 0) break;
     }
 
     if (tid == 0) {
@@ -256,67 +330,77 @@ k2_gbdt(const __grid_constant__ K2Params p, int TC, int nchunks) {
         for (int64_t g = 0; g < (total_loads < stages ? total_loads : (int64_t)stages); ++g) issue(g);
 
     int ci = s_start_i;        // per-warp cursor over instances (warp-uniform)
-    int64_t pc = s_start_pc;   // tiles before instance ci
+    int64_t pc = s_start_pc;   // units before instance ci
     int64_t g = 0;             // loads consumed so far
-    const float* cutsB = p.cuts + p.cut_off[1];
-    const float* cutsKV = p.cuts + p.cut_off[2];
-    const float* cutsTP = p.cuts + p.cut_off[0];
-    const int nB = p.cut_off[2] - p.cut_off[1], nKV = p.cut_off[3] - p.cut_off[2], nTP = p.cut_off[1] - p.cut_off[0];
 
     for (int round = 0; round < nrounds; ++round) {
         const int64_t t = t0 + (int64_t)round * nwarps + warp;
         const bool active = t < t1;
-        int i = 0, m = 0, u0 = 0, ni = 0, m_end = 0;
+        int i = 0, m = 0, u0 = 0, ni = 0, m_end = 0, cidx = -1;
         uint32_t xlo = 0, xhi[RU];
         float acc[RU];
         if (active) {
             const int64_t ub = t * UPT;   // first unit of the tile
-            int64_t ti;
-            while (ub >= pc + (ti = units_of<RUNS>(p, ci, G)) && ci < I - 1) {
-                pc += ti;
-                ++ci;
-            }
-            uint32_t rkv;
-            if constexpr (RUNS) {
-                // lane task = unit ub + lane -> (instance li, run k, level group ug); the tile's
-                // lanes may span several instances (each lane walks on from the warp's cursor)
+            uint32_t rkv = 0;
+            if constexpr (MODE == kCells) {
+                // lane task = unit ub + lane -> (cell row idx, level group ug)
                 const int64_t uu = ub + lane;
-                int li = ci;
-                int64_t lpc = pc, lt;
-                while (uu >= lpc + (lt = units_of<RUNS>(p, li, G)) && li < I - 1) {
-                    lpc += lt;
-                    ++li;
-                }
-                i = li;
-                uint32_t key = 0;
-                m = 0x7fffffff;
                 if (uu < U) {
-                    const int h = p.run_h[i];
-                    const int tau = (int)(uu - lpc);
-                    const int ug = tau / h, k = tau - ug * h;
+                    const int ug = (int)(uu / ncell);
+                    cidx = (int)(uu - (int64_t)ug * ncell);
                     u0 = ug * RU;
-                    key = p.run_key[(size_t)i * p.H + k];
-                    m = p.run_m[(size_t)i * p.H + k];
-                    ni = p.n[i];
-                    m_end = (k + 1 < h) ? p.run_m[(size_t)i * p.H + k + 1] : ni + 1;
+                    const uint32_t c = p.cell_list[cidx];
+                    const uint32_t nk1 = (uint32_t)nKV + 1, nb1 = (uint32_t)nB + 1;
+                    rkv = c % nk1;
+                    const uint32_t rb = (c / nk1) % nb1, rtp = c / (nk1 * nb1);
+                    xlo = rtp | (rb << 16);
                 }
-                xlo = rank_of(cutsTP, nTP, (float)p.inst[i].tp) | ((key & 0xFFFFu) << 16);
-                rkv = key >> 16;
             } else {
-                i = ci;
-                const int64_t tau = ub - pc;
-                const int mt = (int)(tau / G), ug = (int)(tau % G);
-                ni = p.n[i];
-                u0 = ug * RU;
-                const int tpv = p.inst[i].tp;
-                m = mt * 32 + lane + 1;
-                int bv = 0, kvv = 0;
-                if (m <= ni) {
-                    bv = p.B[(size_t)i * p.H + m - 1];
-                    kvv = p.KV[(size_t)i * p.H + m - 1];
+                int64_t ti;
+                while (ub >= pc + (ti = units_of<MODE>(p, ci, G)) && ci < I - 1) {
+                    pc += ti;
+                    ++ci;
                 }
-                xlo = rank_of(cutsTP, nTP, (float)tpv) | (rank_of(cutsB, nB, (float)bv) << 16);
-                rkv = rank_of(cutsKV, nKV, (float)kvv);
+                if constexpr (MODE == kRuns) {
+                    // lane task = unit ub + lane -> (instance li, run k, level group ug); the tile's
+                    // lanes may span several instances (each lane walks on from the warp's cursor)
+                    const int64_t uu = ub + lane;
+                    int li = ci;
+                    int64_t lpc = pc, lt;
+                    while (uu >= lpc + (lt = units_of<MODE>(p, li, G)) && li < I - 1) {
+                        lpc += lt;
+                        ++li;
+                    }
+                    i = li;
+                    uint32_t key = 0;
+                    m = 0x7fffffff;
+                    if (uu < U) {
+                        const int h = p.run_h[i];
+                        const int tau = (int)(uu - lpc);
+                        const int ug = tau / h, k = tau - ug * h;
+                        u0 = ug * RU;
+                        key = p.run_key[(size_t)i * p.H + k];
+                        m = p.run_m[(size_t)i * p.H + k];
+                        ni = p.n[i];
+                        m_end = (k + 1 < h) ? p.run_m[(size_t)i * p.H + k + 1] : ni + 1;
+                    }
+                    xlo = rank_of(cutsTP, nTP, (float)p.inst[i].tp) | ((key & 0xFFFFu) << 16);
+                    rkv = key >> 16;
+                } else {
+                    i = ci;
+                    const int64_t tau = ub - pc;
+                    const int mt = (int)(tau / G), ug = (int)(tau % G);
+                    ni = p.n[i];
+                    u0 = ug * RU;
+                    m = mt * 32 + lane + 1;
+                    int bv = 0, kvv = 0;
+                    if (m <= ni) {
+                        bv = p.B[(size_t)i * p.H + m - 1];
+                        kvv = p.KV[(size_t)i * p.H + m - 1];
+                    }
+                    xlo = rank_of(cutsTP, nTP, (float)p.inst[i].tp) | (rank_of(cutsB, nB, (float)bv) << 16);
+                    rkv = rank_of(cutsKV, nKV, (float)kvv);
+                }
             }
 #pragma unroll
             for (int r = 0; r < RU; ++r) xhi[r] = rkv | (s_rf[min(u0 + r, p.F - 1)] << 16);
@@ -335,8 +419,8 @@ k2_gbdt(const __grid_constant__ K2Params p, int TC, int nchunks) {
                     uint32_t idx[RU];
                     if constexpr (D >= 2) {
                         // levels 0-1: the root and both of its children are shared by all RU rows
-                        // of the lane, so one LDS + one LDS.64 replace 2 * RU loads; the level-0
-                        // carry selects the level-1 word directly.
+                        // of the lane (one LDS.128 of words 0..3); the level-0 carry selects the
+                        // level-1 word directly.
                         const uint32_t w1 = tw[1];
                         const uint2 w23 = *reinterpret_cast<const uint2*>(tw + 2);
 #pragma unroll
@@ -367,32 +451,37 @@ k2_gbdt(const __grid_constant__ K2Params p, int TC, int nchunks) {
         }
 
         if (active) {
-            bool clamped = false;
+            uint32_t cmask = 0;
 #pragma unroll
             for (int r = 0; r < RU; ++r) {
                 const float v = acc[r];
                 const float c = isnan(v) ? 0x1p-4f : fminf(fmaxf(v, 0x1p-4f), 0x1p17f);
-                clamped |= m <= ni && u0 + r < p.F && (isnan(v) || c != v);
+                if (u0 + r < p.F && (isnan(v) || c != v)) cmask |= 1u << (u0 + r);
                 acc[r] = c;
             }
-            if constexpr (!RUNS) {
-                if (m <= ni) {
+            if constexpr (MODE == kCells) {
+                if (cidx >= 0) {
 #pragma unroll
                     for (int r = 0; r < RU; ++r)
-                        if (u0 + r < p.F) p.ips[((size_t)i * p.F + u0 + r) * p.H + (m - 1)] = acc[r];
+                        if (u0 + r < p.F) p.lut[(size_t)cidx * p.F + u0 + r] = acc[r];
+                    if (cmask) atomicOr(p.cell_clamp + cidx, cmask);
                 }
-            } else {
-                // expand: the lane writes its run [m, m_end) for its RU levels
+            } else if constexpr (MODE == kRuns) {
+                // the lane writes its run [m, m_end) for its RU levels
                 for (int mm = m; mm < m_end; ++mm) {
 #pragma unroll
                     for (int r = 0; r < RU; ++r)
                         if (u0 + r < p.F) p.ips[((size_t)i * p.F + u0 + r) * p.H + (mm - 1)] = acc[r];
                 }
-            }
-            if constexpr (RUNS) {
-                if (clamped) atomicOr(p.status + i, (uint32_t)TP_ST_IPS_CLAMPED);   // lanes may differ in i
+                if (cmask && m <= ni) atomicOr(p.status + i, (uint32_t)TP_ST_IPS_CLAMPED);
             } else {
-                if (__any_sync(0xffffffffu, clamped) && lane == 0) atomicOr(p.status + i, (uint32_t)TP_ST_IPS_CLAMPED);
+                if (m <= ni) {
+#pragma unroll
+                    for (int r = 0; r < RU; ++r)
+                        if (u0 + r < p.F) p.ips[((size_t)i * p.F + u0 + r) * p.H + (m - 1)] = acc[r];
+                }
+                if (__any_sync(0xffffffffu, cmask != 0 && m <= ni) && lane == 0)
+                    atomicOr(p.status + i, (uint32_t)TP_ST_IPS_CLAMPED);
             }
         }
     }
@@ -406,26 +495,37 @@ int env_int(const char* name, int dflt, int lo, int hi, int mult) {
     return (x >= lo && x <= hi && x % mult == 0) ? x : dflt;
 }
 
-template <int D, int RU, bool RUNS>
+bool set_smem_attr(const void* fn, int bytes, bool* done, int dev) {
+    if (dev < 64 && done[dev]) return true;
+    if (cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes) != cudaSuccess) return false;
+    if (dev < 64) done[dev] = true;
+    return true;
+}
+
+template <int D, int RU, int MODE>
 int launch_d(const K2Params& p, cudaStream_t s) {
     const int TW = (2 << D) < 4 ? 4 : (2 << D);
     const int tree_bytes = TW * 4;
-    static const int threads = env_int("TP_K2_THREADS", kDefaultThreads, 64, kMaxThreads, 32);
-    static const int chunk_bytes = env_int("TP_K2_CHUNK_KB", kDefaultChunkBytes / 1024, 4, 100, 1) * 1024;
+    static const int threads =
+        env_int("TP_K2_THREADS", MODE == kDirect ? kDefaultThreads : kDefaultThreadsRuns, 64, kMaxThreads, 32);
+    static const int chunk_bytes =
+        env_int("TP_K2_CHUNK_KB", (MODE == kDirect ? kDefaultChunkBytes : kDefaultChunkBytesRuns) / 1024, 4, 100, 1) *
+        1024;
     int TC = std::max(1, std::min(std::max(p.n_trees, 1), chunk_bytes / tree_bytes));
     const int nchunks = p.n_trees == 0 ? 0 : (p.n_trees + TC - 1) / TC;
     const int stages = nchunks == 1 ? 1 : 2;
     const size_t smem = (size_t)stages * TC * tree_bytes;
-    auto kern = k2_gbdt<D, RU, RUNS>;
+    auto kern = k2_gbdt<D, RU, MODE>;
     int dev = 0, sms = 0, per_sm = 0;
     if (cudaGetDevice(&dev) != cudaSuccess) return TP_ECUDA;
-    if (RUNS) {
+    if (MODE != kDirect) {
         static bool runs_attr[64] = {};
-        if (dev < 64 && !runs_attr[dev]) {
-            if (cudaFuncSetAttribute(k2_runs, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                     (kMaxH + 1) * 4) != cudaSuccess)
+        if (!set_smem_attr((const void*)k2_runs, (kMaxH + 1) * 4, runs_attr, dev)) return TP_ECUDA;
+        if (MODE == kCells) {
+            if (cudaMemsetAsync(p.cell_tab, 0xFF, (size_t)p.n_cells * 4, s) != cudaSuccess ||
+                cudaMemsetAsync(p.cell_count, 0, 4, s) != cudaSuccess ||
+                cudaMemsetAsync(p.cell_clamp, 0, (size_t)p.cell_cap * 4, s) != cudaSuccess)
                 return TP_ECUDA;
-            runs_attr[dev] = true;
         }
         k2_runs<<<p.n_inst, kRunsThreads, (size_t)(p.H + 1) * 4, s>>>(p);
         if (cudaPeekAtLastError() != cudaSuccess) return TP_ECUDA;
@@ -436,57 +536,94 @@ int launch_d(const K2Params& p, cudaStream_t s) {
     if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, threads, smem) != cudaSuccess) return TP_ECUDA;
     const int grid = std::max(1, sms * std::max(1, per_sm));
     kern<<<grid, threads, smem, s>>>(p, TC, nchunks);
-    return cudaPeekAtLastError() == cudaSuccess ? TP_OK : TP_ECUDA;
+    if (cudaPeekAtLastError() != cudaSuccess) return TP_ECUDA;
+    if (MODE == kCells) {
+        static bool exp_attr[64] = {};
+        if (!set_smem_attr((const void*)k2_expand, 2 * kMaxH * 4, exp_attr, dev)) return TP_ECUDA;
+        k2_expand<<<p.n_inst, kExpandThreads, (size_t)2 * p.H * 4, s>>>(p);
+        if (cudaPeekAtLastError() != cudaSuccess) return TP_ECUDA;
+    }
+    return TP_OK;
 }
 
-template <int RU, bool RUNS>
+template <int RU, int MODE>
 int launch_ru(const K2Params& p, cudaStream_t s) {
     switch (p.depth) {
-        case 0: return launch_d<0, RU, RUNS>(p, s);
-        case 1: return launch_d<1, RU, RUNS>(p, s);
-        case 2: return launch_d<2, RU, RUNS>(p, s);
-        case 3: return launch_d<3, RU, RUNS>(p, s);
-        case 4: return launch_d<4, RU, RUNS>(p, s);
-        case 5: return launch_d<5, RU, RUNS>(p, s);
-        case 6: return launch_d<6, RU, RUNS>(p, s);
-        case 7: return launch_d<7, RU, RUNS>(p, s);
-        case 8: return launch_d<8, RU, RUNS>(p, s);
-        case 9: return launch_d<9, RU, RUNS>(p, s);
-        case 10: return launch_d<10, RU, RUNS>(p, s);
-        case 11: return launch_d<11, RU, RUNS>(p, s);
-        case 12: return launch_d<12, RU, RUNS>(p, s);
+        case 0: return launch_d<0, RU, MODE>(p, s);
+        case 1: return launch_d<1, RU, MODE>(p, s);
+        case 2: return launch_d<2, RU, MODE>(p, s);
+        case 3: return launch_d<3, RU, MODE>(p, s);
+        case 4: return launch_d<4, RU, MODE>(p, s);
+        case 5: return launch_d<5, RU, MODE>(p, s);
+        case 6: return launch_d<6, RU, MODE>(p, s);
+        case 7: return launch_d<7, RU, MODE>(p, s);
+        case 8: return launch_d<8, RU, MODE>(p, s);
+        case 9: return launch_d<9, RU, MODE>(p, s);
+        case 10: return launch_d<10, RU, MODE>(p, s);
+        case 11: return launch_d<11, RU, MODE>(p, s);
+        case 12: return launch_d<12, RU, MODE>(p, s);
         default: return TP_EFORMAT;
     }
 }
+
+template <int MODE>
+int launch_mode(const K2Params& p, cudaStream_t s) {
+    if (p.F <= 2) return launch_ru<2, MODE>(p, s);
+    if (p.F <= 4) return launch_ru<4, MODE>(p, s);
+    return launch_ru<8, MODE>(p, s);
+}
+
+uintptr_t align256(uintptr_t x) { return (x + 255) & ~(uintptr_t)255; }
 
 }  // namespace
 
 int launch_gbdt(const K2Params& p, bool runs, cudaStream_t s) {
     if (p.n_inst == 0) return TP_OK;
-    if (runs) {
-        if (p.F <= 2) return launch_ru<2, true>(p, s);
-        if (p.F <= 4) return launch_ru<4, true>(p, s);
-        return launch_ru<8, true>(p, s);
-    }
-    if (p.F <= 2) return launch_ru<2, false>(p, s);
-    if (p.F <= 4) return launch_ru<4, false>(p, s);
-    return launch_ru<8, false>(p, s);
+    if (!runs) return launch_mode<kDirect>(p, s);
+    return p.cell_tab ? launch_mode<kCells>(p, s) : launch_mode<kRuns>(p, s);
 }
 
-size_t runs_workspace_bytes(int32_t n_inst, int32_t H) {
-    const size_t I = (size_t)(n_inst > 0 ? n_inst : 1);
-    return 256 + I * 4 + 2 * I * (size_t)H * 4 + 512;
+int64_t model_cells(const Model& m) {
+    return (int64_t)(m.n_cuts[0] + 1) * (m.n_cuts[1] + 1) * (m.n_cuts[2] + 1);
 }
 
-void runs_workspace_carve(void* ws, int32_t n_inst, int32_t H, K2Params& p) {
+// Workspace: run_h [I], run_m [I][H], run_key [I][H]; cell mode adds cell_tab [n_cells],
+// cell_list [cap], cell_count, cell_clamp [cap], lut [cap][F] with cap = min(n_cells, I * H).
+size_t runs_workspace_bytes(int64_t n_cells, int32_t n_inst, int32_t H, int32_t F) {
+    K2Params p{};
+    runs_workspace_carve(nullptr, n_cells, n_inst, H, F, p);
+    return (size_t)reinterpret_cast<uintptr_t>(p.lut ? (void*)(p.lut + (size_t)p.cell_cap * F) : (void*)(p.run_key + (size_t)(n_inst > 0 ? n_inst : 1) * H)) + 256;
+}
+
+void runs_workspace_carve(void* ws, int64_t n_cells, int32_t n_inst, int32_t H, int32_t F, K2Params& p) {
     const size_t I = (size_t)(n_inst > 0 ? n_inst : 1);
-    auto up = [](uintptr_t x) { return (x + 255) & ~(uintptr_t)255; };
-    uintptr_t a = up((uintptr_t)ws);
+    uintptr_t a = align256((uintptr_t)ws);
     p.run_h = reinterpret_cast<int32_t*>(a);
-    a = up(a + I * 4);
+    a = align256(a + I * 4);
     p.run_m = reinterpret_cast<int32_t*>(a);
-    a = up(a + I * (size_t)H * 4);
+    a = align256(a + I * (size_t)H * 4);
     p.run_key = reinterpret_cast<uint32_t*>(a);
+    a = align256(a + I * (size_t)H * 4);
+    p.cell_tab = nullptr;
+    p.cell_list = nullptr;
+    p.cell_count = nullptr;
+    p.cell_clamp = nullptr;
+    p.lut = nullptr;
+    p.n_cells = 0;
+    p.cell_cap = 0;
+    if (n_cells <= 0 || n_cells > kMaxCells) return;
+    const int64_t cap = std::min<int64_t>(n_cells, (int64_t)I * H);
+    p.n_cells = (int32_t)n_cells;
+    p.cell_cap = (int32_t)cap;
+    p.cell_tab = reinterpret_cast<int32_t*>(a);
+    a = align256(a + (size_t)n_cells * 4);
+    p.cell_list = reinterpret_cast<uint32_t*>(a);
+    a = align256(a + (size_t)cap * 4);
+    p.cell_count = reinterpret_cast<int32_t*>(a);
+    a = align256(a + 4);
+    p.cell_clamp = reinterpret_cast<uint32_t*>(a);
+    a = align256(a + (size_t)cap * 4);
+    p.lut = reinterpret_cast<float*>(a);
 }
 
 }  // namespace tp

@@ -57,11 +57,23 @@ struct K2Params {
     // (batch, KV) threshold ranks form a run; the ensemble is evaluated once per run.
     int32_t* run_h;          // [n_inst] runs per instance (0 for skipped instances)
     int32_t* run_m;          // [n_inst][H] first iteration m of each run
-    uint32_t* run_key;       // [n_inst][H] rank_B | rank_KV << 16 of each run
+    uint32_t* run_key;       // [n_inst][H] rank_B | rank_KV << 16 of each run (cell id in cell mode)
+    // cell-memoised mode: M depends on a grid row only through its cell = (rank_tp, rank_B,
+    // rank_KV) (and the level); distinct cells are evaluated once into a LUT, then expanded.
+    int32_t* cell_tab;       // [n_cells] dense cell id -> LUT row (-1 = absent), or null
+    uint32_t* cell_list;     // [cap] LUT row -> cell id
+    int32_t* cell_count;     // [1] distinct cells
+    float* lut;              // [cap][F] clamped IPS
+    uint32_t* cell_clamp;    // [cap] bit u set if level u's value was clamped
+    int32_t n_cells, cell_cap;
 };
 
-size_t runs_workspace_bytes(int32_t n_inst, int32_t H);
-void runs_workspace_carve(void* ws, int32_t n_inst, int32_t H, K2Params& p);
+// workspace for tp_predict_ips_runs; cell mode is used when the model's dense cell space
+// (nTP+1)(nB+1)(nKV+1) is at most kMaxCells
+constexpr int64_t kMaxCells = 1LL << 22;
+size_t runs_workspace_bytes(int64_t n_cells, int32_t n_inst, int32_t H, int32_t F);
+void runs_workspace_carve(void* ws, int64_t n_cells, int32_t n_inst, int32_t H, int32_t F, K2Params& p);
+int64_t model_cells(const Model& m);
 
 int launch_project(const tp_inst* inst, int32_t n_inst, const tp_req* req, int32_t n_req, int32_t H,
                    int32_t* B, int32_t* KV, int32_t* n, int32_t* n_adm, uint32_t* status, cudaStream_t s);

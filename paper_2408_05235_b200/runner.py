@@ -21,7 +21,7 @@ def to_device_bytes(a: np.ndarray, device) -> torch.Tensor:
 class Round:
     """One decision round's device buffers (inputs + K1/K2/K3 outputs)."""
 
-    def __init__(self, inputs: dict, device="cuda:0", want_tr=False, k2_mode="runs"):
+    def __init__(self, inputs: dict, device="cuda:0", want_tr=False, k2_mode="cells", model=None):
         dev = torch.device(device)
         self.device = dev
         inst, req, t_dead = inputs["inst"], inputs["req"], inputs["t_dead"]
@@ -43,17 +43,18 @@ class Round:
         self.level = torch.empty(I, dtype=torch.int32, device=dev)
         self.ips = torch.zeros((I, F, H), dtype=torch.float32, device=dev)
         self.tr = torch.zeros((I, F, H), dtype=torch.int64, device=dev) if want_tr else None
-        assert k2_mode in ("runs", "direct")
+        assert k2_mode in ("cells", "runs", "direct")
+        assert k2_mode != "cells" or model is not None, "cell mode sizes its workspace from the model"
         self.k2_mode = k2_mode
-        self.work = torch.empty(tp.tp_predict_ips_workspace_size(I, H), dtype=torch.uint8, device=dev) \
-            if k2_mode == "runs" else None
+        self.work = torch.empty(tp.tp_predict_ips_workspace_size(model if k2_mode == "cells" else None, I, H, F),
+                                dtype=torch.uint8, device=dev) if k2_mode != "direct" else None
 
     def project(self, stream=None):
         tp.tp_project(self.inst, self.I, self.req, self.R, self.H, self.B, self.KV, self.n, self.n_adm, self.status,
                       stream)
 
     def predict(self, model, stream=None):
-        if self.k2_mode == "runs":
+        if self.k2_mode in ("runs", "cells"):
             tp.tp_predict_ips_runs(model, self.inst, self.I, self.B, self.KV, self.n, self.H, self.freq, self.ips,
                                    self.status, self.work, stream)
         else:

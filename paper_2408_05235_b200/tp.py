@@ -21,7 +21,7 @@ ST_QUEUE_BLOCKED, ST_IPS_CLAMPED, ST_BAD_INPUT = 16, 32, 64
 
 # every symbol include/tp.h declares
 EXPORTS = ["tp_gbdt_load", "tp_gbdt_free", "tp_gbdt_get_info", "tp_project", "tp_predict_ips",
-           "tp_predict_ips_workspace_size", "tp_predict_ips_runs", "tp_runs_total", "tp_select_freq", "tp_ctx_create", "tp_ctx_free",
+           "tp_predict_ips_workspace_size", "tp_predict_ips_runs", "tp_runs_total", "tp_cells_total", "tp_select_freq", "tp_ctx_create", "tp_ctx_free",
            "tp_decide", "tp_decide_host", "tp_ctx_set_k2_mode", "tp_ctx_buffers", "tp_strerror", "tp_abi_version"]
 K2_DIRECT, K2_RUNS = 0, 1
 
@@ -43,12 +43,13 @@ _L.tp_gbdt_free.argtypes = [_vp]
 _L.tp_gbdt_get_info.argtypes = [_vp, ctypes.POINTER(GbdtInfo)]
 _L.tp_project.argtypes = [_vp, _i32, _vp, _i32, _i32, _vp, _vp, _vp, _vp, _vp, _vp]
 _L.tp_predict_ips.argtypes = [_vp, _vp, _i32, _vp, _vp, _vp, _i32, _vp, _i32, _vp, _vp, _vp]
-_L.tp_predict_ips_workspace_size.argtypes = [_i32, _i32]
+_L.tp_predict_ips_workspace_size.argtypes = [_vp, _i32, _i32, _i32]
 _L.tp_predict_ips_runs.argtypes = [_vp, _vp, _i32, _vp, _vp, _vp, _i32, _vp, _i32, _vp, _vp, _vp, ctypes.c_size_t, _vp]
 _L.tp_ctx_set_k2_mode.argtypes = [_vp, ctypes.c_int]
 _L.tp_runs_total.argtypes = [_vp, _i32, _i32, ctypes.POINTER(_i64)]
+_L.tp_cells_total.argtypes = [_vp, _vp, _i32, _i32, _i32, ctypes.POINTER(_i64)]
 _L.tp_select_freq.argtypes = [_vp, _i32, _vp, _i32, _vp, _vp, _vp, _vp, _i32, _i32, _f32, _vp, _vp, _vp, _vp]
-_L.tp_ctx_create.argtypes = [ctypes.c_int, _i32, _i32, _i32, _i32, ctypes.POINTER(_vp)]
+_L.tp_ctx_create.argtypes = [ctypes.c_int, _vp, _i32, _i32, _i32, _i32, ctypes.POINTER(_vp)]
 _L.tp_ctx_free.argtypes = [_vp]
 _L.tp_decide.argtypes = [_vp, _vp, _vp, _i32, _vp, _i32, _vp, _vp, _i32, _f32, _vp, _vp, _vp]
 _L.tp_decide_host.argtypes = [_vp, _vp, _vp, _i32, _vp, _i32, _vp, _vp, _i32, _f32, _vp, _vp, _vp]
@@ -153,8 +154,10 @@ def tp_predict_ips(model: Gbdt, inst, n_inst, B, KV, n, H, freq, ips, status, st
                              F, _dp(ips), _dp(status), _stream(stream)), "tp_predict_ips")
 
 
-def tp_predict_ips_workspace_size(n_inst, H) -> int:
-    return int(_L.tp_predict_ips_workspace_size(int(n_inst), int(H)))
+def tp_predict_ips_workspace_size(model, n_inst, H, F) -> int:
+    """model=None sizes run mode; a Gbdt sizes its cell mode."""
+    return int(_L.tp_predict_ips_workspace_size(model.handle if model is not None else None, int(n_inst), int(H),
+                                                int(F)))
 
 
 def tp_predict_ips_runs(model: Gbdt, inst, n_inst, B, KV, n, H, freq, ips, status, workspace, stream=None):
@@ -172,6 +175,14 @@ def runs_total(workspace, n_inst, H) -> int:
     return int(t.value)
 
 
+def cells_total(workspace, model, n_inst, H, F) -> int:
+    """Distinct cells evaluated by the last cell-mode tp_predict_ips_runs (synchronous diagnostic)."""
+    t = _i64()
+    _check(_L.tp_cells_total(model.handle, _dp(workspace), int(n_inst), int(H), int(F), ctypes.byref(t)),
+           "tp_cells_total")
+    return int(t.value)
+
+
 def tp_select_freq(inst, n_inst, req, n_req, t_dead, n, n_adm, ips, H, F, tbt_slo, level, status, tr_ticks=None,
                    stream=None):
     _check(_L.tp_select_freq(_dp(inst), int(n_inst), _dp(req), int(n_req), _dp(t_dead), _dp(n), _dp(n_adm),
@@ -182,10 +193,10 @@ def tp_select_freq(inst, n_inst, req, n_req, t_dead, n, n_adm, ips, H, F, tbt_sl
 class Ctx:
     """tp_ctx_create / tp_decide / tp_decide_host."""
 
-    def __init__(self, device, n_inst_max, n_req_max, H, F_max):
+    def __init__(self, device, n_inst_max, n_req_max, H, F_max, model=None):
         h = _vp()
-        _check(_L.tp_ctx_create(int(device), int(n_inst_max), int(n_req_max), int(H), int(F_max), ctypes.byref(h)),
-               "tp_ctx_create")
+        _check(_L.tp_ctx_create(int(device), model.handle if model is not None else None, int(n_inst_max),
+                                int(n_req_max), int(H), int(F_max), ctypes.byref(h)), "tp_ctx_create")
         self.handle = h
         self.H = H
 
@@ -221,5 +232,5 @@ class Ctx:
             pass
 
 
-def tp_ctx_create(device, n_inst_max, n_req_max, H, F_max) -> Ctx:
-    return Ctx(device, n_inst_max, n_req_max, H, F_max)
+def tp_ctx_create(device, model, n_inst_max, n_req_max, H, F_max) -> Ctx:
+    return Ctx(device, n_inst_max, n_req_max, H, F_max, model)

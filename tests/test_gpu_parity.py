@@ -30,16 +30,16 @@ def gpu():
     return tp, runner
 
 
-@pytest.fixture(params=["direct", "runs"])
+@pytest.fixture(params=["direct", "runs", "cells"])
 def mode(request):
-    """Both K2 variants: tp_predict_ips (direct) and tp_predict_ips_runs (run-compressed)."""
+    """All K2 variants: tp_predict_ips (direct) and tp_predict_ips_runs in run and cell mode."""
     return request.param
 
 
 def run_gpu(gpu, blob, inputs, want_tr=True, idx=None, mode="runs"):
     tp, runner = gpu
     model = tp.Gbdt(blob, 0)
-    r = runner.Round(inputs, "cuda:0", want_tr=want_tr, k2_mode=mode)
+    r = runner.Round(inputs, "cuda:0", want_tr=want_tr, k2_mode=mode, model=model)
     r.run(model)
     out = r.results(idx)
     del r
@@ -229,8 +229,8 @@ def test_clamp_and_bad_input(gpu, oracle_mod, mode):
     assert got["status"][0] & 32 and got["status"].tolist()[1:] == [64, 64, 64, 1]
 
 
-@pytest.mark.parametrize("k2", [0, 1])
-def test_decide_entry_points_agree(gpu, oracle_mod, k2):
+@pytest.mark.parametrize("k2,cells", [(0, False), (1, False), (1, True)])
+def test_decide_entry_points_agree(gpu, oracle_mod, k2, cells):
     """tp_decide (device) and tp_decide_host (host buffers, e2e path) == the oracle, both K2 modes."""
     tp, runner = gpu
     cfg = W.CONFIGS["P2"]
@@ -239,9 +239,9 @@ def test_decide_entry_points_agree(gpu, oracle_mod, k2):
     ref = run_oracle(oracle_mod, blob, inputs, want_grid=False, want_tr=False)
     model = tp.Gbdt(blob, 0)
     I, R = len(inputs["inst"]), len(inputs["req"])
-    ctx = tp.Ctx(0, I, R, inputs["H"], len(inputs["freq"]))
+    ctx = tp.Ctx(0, I, R, inputs["H"], len(inputs["freq"]), model if cells else None)
     ctx.set_k2_mode(k2)
-    r = runner.Round(inputs, "cuda:0")
+    r = runner.Round(inputs, "cuda:0", k2_mode="direct")
     ctx.decide(model, r.inst, I, r.req, R, r.t_dead, inputs["freq"], inputs["tbt_slo"], r.level, r.status)
     torch.cuda.synchronize()
     assert np.array_equal(r.level.cpu().numpy(), ref["level"])
@@ -260,7 +260,7 @@ def test_runs_are_fewer_than_grid_rows(gpu, oracle_mod):
     tp, runner = gpu
     cfg = W.CONFIGS["C2"]
     model = tp.Gbdt(W.write_blob(W.config_ensemble(cfg)), 0)
-    r = runner.Round(W.config_inputs(cfg), "cuda:0", k2_mode="runs")
+    r = runner.Round(W.config_inputs(cfg), "cuda:0", k2_mode="runs", model=model)
     r.run(model)
     torch.cuda.synchronize()
     runs = tp.runs_total(r.work, r.I, r.H)
@@ -276,7 +276,7 @@ def test_concurrent_streams_share_model(gpu, oracle_mod):
     a_in = W.config_inputs(cfg)
     b_in = W.config_inputs(dataclasses.replace(cfg, seed=4242))
     model = tp.Gbdt(blob, 0)
-    ra, rb = runner.Round(a_in, "cuda:0"), runner.Round(b_in, "cuda:0")
+    ra, rb = runner.Round(a_in, "cuda:0", model=model), runner.Round(b_in, "cuda:0", model=model)
     sa, sb = torch.cuda.Stream(), torch.cuda.Stream()
     for _ in range(3):
         ra.run(model, sa)
