@@ -174,8 +174,9 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--e2e-steps", type=int, default=None)
-    ap.add_argument("--k2", default="cells", choices=["cells", "runs", "direct"],
-                    help="K2 variant: cell-memoised (default), run-compressed, or one evaluation per grid point")
+    ap.add_argument("--k2", default="fused", choices=["fused", "cells", "runs", "direct"],
+                    help="K2 variant: cell-memoised fused with K3 (default), cell-memoised with the ips grid, "
+                         "run-compressed, or one evaluation per grid point")
     args = ap.parse_args()
     cfg = W.CONFIGS[args.workload]
     if args.impl == "reference":
@@ -260,6 +261,7 @@ def main():
     padded = int((((n_h + 31) // 32) * 32 * ((st_h & SKIP) == 0)).sum()) * rnd.F
     evaluated = {"runs": lambda: tp.runs_total(rnd.work, I, rnd.H) * rnd.F,
                  "cells": lambda: tp.cells_total(rnd.work, model, I, rnd.H, rnd.F) * rnd.F,
+                 "fused": lambda: tp.cells_total(rnd.work, model, I, rnd.H, rnd.F) * rnd.F,
                  "direct": lambda: grid}[args.k2]()
 
     evs = [[torch.cuda.Event(enable_timing=True) for _ in range(5)] for _ in range(args.steps)]
@@ -309,7 +311,7 @@ def main():
     # end to end through the C ABI with host buffers (pinned), copies inside the timed region
     e2e = None
     if True:
-        ctx = tp.Ctx(local, I, R, rnd.H, rnd.F, model if args.k2 == "cells" else None)
+        ctx = tp.Ctx(local, I, R, rnd.H, rnd.F, model if args.k2 in ("cells", "fused") else None)
         ctx.set_k2_mode(tp.K2_DIRECT if args.k2 == "direct" else tp.K2_RUNS)
         h_inst = torch.from_numpy(inputs["inst"].view(np.uint8)).pin_memory()
         h_req = torch.from_numpy(inputs["req"].view(np.uint8)).pin_memory()
@@ -360,7 +362,8 @@ def main():
     except (OSError, ValueError):
         pass
     roof = {"bound": "smem", "kernel": {"direct": "k2_gbdt", "runs": "k2_gbdt<runs> (+ k2_runs pre-pass)",
-                                        "cells": "k2_gbdt<cells> (+ k2_runs pre-pass, k2_expand)"}[args.k2],
+                                        "cells": "k2_gbdt<cells> (+ k2_runs pre-pass, k2_expand)",
+                                        "fused": "k2_gbdt<cells> (+ k2_runs pre-pass)"}[args.k2],
             "achieved": achieved, "peak": peak, "unit": "GB/s",
             "frac": achieved / peak, "traffic": traffic,
             "peak_basis": f"{sms} SMs x 128 B/clk (LDS) x sm_max_mhz {smax:.0f} (MEASURED_PEAKS.json clock)",

@@ -172,6 +172,8 @@ int tp_predict_ips(const tp_gbdt* m, const tp_inst* inst, int32_t n_inst, const 
  *             >= tp_predict_ips_workspace_size(m, n_inst, H, F) bytes enables cell mode (used when
  *             the model's dense cell space (n_cuts[0]+1)(n_cuts[1]+1)(n_cuts[2]+1) <= 2^22);
  *             >= tp_predict_ips_workspace_size(NULL, n_inst, H, F) bytes gives run mode.
+ *   ips       [dev] as tp_predict_ips; may be NULL in cell mode (values stay in the workspace for
+ *             tp_select_freq_ws; IPS_CLAMPED is then set by tp_select_freq_ws).
  * Other arguments, outputs and errors: as tp_predict_ips.
  */
 size_t tp_predict_ips_workspace_size(const tp_gbdt* m, int32_t n_inst, int32_t H, int32_t F);
@@ -210,6 +212,18 @@ int tp_select_freq(const tp_inst* inst, int32_t n_inst, const tp_req* req, int32
                    int64_t* tr_ticks, void* stream);
 
 /*
+ * K3 fused with K2's cell mode: after tp_predict_ips_runs(m, ..., ips = NULL, workspace) in cell mode
+ * the IPS values live only in the workspace's per-cell table; this K3 reads them through each
+ * instance's runs (same outputs as tp_select_freq on the expanded grid, bit for bit), so the
+ * [n_inst][F][H] ips grid is never written or read.  TP_ST_IPS_CLAMPED is OR-ed here.
+ * TP_EINVAL if the workspace / model has no cell mode.  Other arguments: as tp_select_freq.
+ */
+int tp_select_freq_ws(const tp_gbdt* m, const void* workspace, const tp_inst* inst, int32_t n_inst,
+                      const tp_req* req, int32_t n_req, const double* t_dead, const int32_t* n,
+                      const int32_t* n_adm, int32_t H, int32_t F, float tbt_slo, int32_t* level,
+                      uint32_t* status, int64_t* tr_ticks, void* stream);
+
+/*
  * Convenience: one decision round with library-owned scratch.
  * tp_ctx_create allocates, on `device`, B/KV/n/n_adm (n_inst_max x H), the ips grid
  * (n_inst_max x F_max x H), the K2 workspace (sized for `model`'s cell mode; NULL = run mode)
@@ -220,7 +234,9 @@ int tp_ctx_create(int device, const tp_gbdt* model, int32_t n_inst_max, int32_t 
                   int32_t F_max, tp_ctx** out);
 int tp_ctx_free(tp_ctx* c);
 
-/* K1 -> K2 -> K3 on device-resident inputs; level/status [dev] out. */
+/* K1 -> K2 -> K3 on device-resident inputs; level/status [dev] out.  With TP_K2_RUNS (default) and a
+ * context created for `m`, K2 runs in cell mode without materialising the ips grid
+ * (tp_predict_ips_runs with ips = NULL, then tp_select_freq_ws). */
 int tp_decide(tp_ctx* c, const tp_gbdt* m, const tp_inst* inst, int32_t n_inst, const tp_req* req,
               int32_t n_req, const double* t_dead, const float* freq_mhz, int32_t F, float tbt_slo,
               int32_t* level, uint32_t* status, void* stream);

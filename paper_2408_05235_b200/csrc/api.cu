@@ -33,6 +33,7 @@ struct tp_ctx {
     void* work;
     size_t work_bytes;
     int k2_mode;
+    const tp_gbdt* cells_model;   // the model the workspace was sized for (cell mode), or null
     tp_inst* inst;
     tp_req* req;
     double* t_dead;
@@ -96,9 +97,10 @@ int tp_predict_ips_runs(const tp_gbdt* m, const tp_inst* inst, int32_t n_inst, c
                         const int32_t* n, int32_t H, const float* freq_mhz, int32_t F, float* ips, uint32_t* status,
                         void* workspace, size_t workspace_bytes, void* stream) {
     if (!m || n_inst < 0 || !H_ok(H) || !freq_ok(freq_mhz, F)) return TP_EINVAL;
-    if (n_inst > 0 && (!inst || !B || !KV || !n || !ips || !status || !workspace)) return TP_EINVAL;
+    if (n_inst > 0 && (!inst || !B || !KV || !n || !status || !workspace)) return TP_EINVAL;
     const int64_t cells = tp::model_cells(m->m);
-    const bool use_cells = workspace_bytes >= tp::runs_workspace_bytes(cells, n_inst, H, F);
+    const bool use_cells = cells <= tp::kMaxCells && workspace_bytes >= tp::runs_workspace_bytes(cells, n_inst, H, F);
+    if (n_inst > 0 && !ips && !use_cells) return TP_EINVAL;   // ips may be NULL only in cell mode
     if (n_inst > 0 && workspace_bytes < tp::runs_workspace_bytes(0, n_inst, H, F)) return TP_EINVAL;
     tp::K2Params p;
     std::memset(&p, 0, sizeof(p));
@@ -158,7 +160,22 @@ int tp_select_freq(const tp_inst* inst, int32_t n_inst, const tp_req* req, int32
         return TP_EINVAL;
     const int64_t tbt_ticks = (int64_t)((double)tbt_slo * 0x1p40);   // exact: tbt_slo >= 2^-17
     return tp::launch_select(inst, n_inst, req, n_req, t_dead, n, n_adm, ips, H, F, tbt_ticks, level, status,
-                             tr_ticks, S(stream));
+                             tr_ticks, nullptr, S(stream));
+}
+
+int tp_select_freq_ws(const tp_gbdt* m, const void* workspace, const tp_inst* inst, int32_t n_inst, const tp_req* req,
+                      int32_t n_req, const double* t_dead, const int32_t* n, const int32_t* n_adm, int32_t H, int32_t F,
+                      float tbt_slo, int32_t* level, uint32_t* status, int64_t* tr_ticks, void* stream) {
+    if (!m || n_inst < 0 || n_req < 0 || !H_ok(H) || F < 1 || F > tp::kMaxF || !tbt_ok(tbt_slo)) return TP_EINVAL;
+    if (n_inst > 0 && (!workspace || !inst || !n || !n_adm || !level || !status || (n_req > 0 && (!req || !t_dead))))
+        return TP_EINVAL;
+    tp::K2Params p;
+    std::memset(&p, 0, sizeof(p));
+    tp::runs_workspace_carve(const_cast<void*>(workspace), tp::model_cells(m->m), n_inst, H, F, p);
+    if (n_inst > 0 && !p.cell_tab) return TP_EINVAL;   // the model has no cell mode
+    const int64_t tbt_ticks = (int64_t)((double)tbt_slo * 0x1p40);
+    return tp::launch_select(inst, n_inst, req, n_req, t_dead, n, n_adm, nullptr, H, F, tbt_ticks, level, status,
+                             tr_ticks, &p, S(stream));
 }
 
 int tp_ctx_create(int device, const tp_gbdt* model, int32_t n_inst_max, int32_t n_req_max, int32_t H, int32_t F_max,
@@ -174,6 +191,7 @@ int tp_ctx_create(int device, const tp_gbdt* model, int32_t n_inst_max, int32_t 
     c->H = H;
     c->F_max = F_max;
     c->k2_mode = TP_K2_RUNS;
+    c->cells_model = (model && tp::model_cells(model->m) <= tp::kMaxCells) ? model : nullptr;
     int prev = 0;
     cudaGetDevice(&prev);
     if (cudaSetDevice(device) != cudaSuccess) {
@@ -236,11 +254,18 @@ int tp_decide(tp_ctx* c, const tp_gbdt* m, const tp_inst* inst, int32_t n_inst, 
         return TP_EINVAL;
     int rc = tp_project(inst, n_inst, req, n_req, c->H, c->B, c->KV, c->n, c->n_adm, status, stream);
     if (rc) return rc;
-    rc = c->k2_mode == TP_K2_RUNS
-             ? tp_predict_ips_runs(m, inst, n_inst, c->B, c->KV, c->n, c->H, freq_mhz, F, c->ips, status, c->work,
-                                   c->work_bytes, stream)
-             : tp_predict_ips(m, inst, n_inst, c->B, c->KV, c->n, c->H, freq_mhz, F, c->ips, status, stream);
+    // cell mode (ctx created with the model): K2 leaves the IPS values in the LUT and K3 reads them
+    // through the runs -- the ips grid is never materialised
+    const bool fused = c->k2_mode == TP_K2_RUNS && c->cells_model == m && m != nullptr;
+    if (c->k2_mode == TP_K2_RUNS)
+        rc = tp_predict_ips_runs(m, inst, n_inst, c->B, c->KV, c->n, c->H, freq_mhz, F, fused ? nullptr : c->ips,
+                                 status, c->work, c->work_bytes, stream);
+    else
+        rc = tp_predict_ips(m, inst, n_inst, c->B, c->KV, c->n, c->H, freq_mhz, F, c->ips, status, stream);
     if (rc) return rc;
+    if (fused)
+        return tp_select_freq_ws(m, c->work, inst, n_inst, req, n_req, t_dead, c->n, c->n_adm, c->H, F, tbt_slo,
+                                 level, status, nullptr, stream);
     return tp_select_freq(inst, n_inst, req, n_req, t_dead, c->n, c->n_adm, c->ips, c->H, F, tbt_slo, level, status,
                           nullptr, stream);
 }

@@ -537,7 +537,7 @@ int launch_d(const K2Params& p, cudaStream_t s) {
     const int grid = std::max(1, sms * std::max(1, per_sm));
     kern<<<grid, threads, smem, s>>>(p, TC, nchunks);
     if (cudaPeekAtLastError() != cudaSuccess) return TP_ECUDA;
-    if (MODE == kCells) {
+    if (MODE == kCells && p.ips) {   // ips == NULL: values stay in the LUT (tp_select_freq_ws)
         static bool exp_attr[64] = {};
         if (!set_smem_attr((const void*)k2_expand, 2 * kMaxH * 4, exp_attr, dev)) return TP_ECUDA;
         k2_expand<<<p.n_inst, kExpandThreads, (size_t)2 * p.H * 4, s>>>(p);

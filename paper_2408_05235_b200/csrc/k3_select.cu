@@ -29,12 +29,24 @@ __device__ __forceinline__ long long slack_ticks(double s) {
     return (long long)ceil(d);
 }
 
+// WS = false: IPS read from the ips grid.  WS = true (fused with K2's cell mode): IPS read from the
+// cell LUT through the instance's runs, so the ips grid is never materialised.
+struct WsView {
+    const int32_t* run_h;
+    const int32_t* run_m;
+    const uint32_t* run_key;
+    const int32_t* cell_tab;
+    const float* lut;
+    const uint32_t* cell_clamp;
+};
+
+template <bool WS>
 __global__ void __launch_bounds__(kThreads)
 k3_select(const tp_inst* __restrict__ inst, const int4* __restrict__ req, const double* __restrict__ t_dead,
           const int32_t* __restrict__ nv, const int32_t* __restrict__ nadm, const float* __restrict__ ips,
           int32_t H, int32_t F, long long tbt_ticks, int32_t* __restrict__ level, uint32_t* __restrict__ status,
-          long long* __restrict__ tr) {
-    extern __shared__ long long dmin[];   // index m in [1, n]
+          long long* __restrict__ tr, const __grid_constant__ WsView ws) {
+    extern __shared__ long long dmin[];   // index m in [1, n]; (WS) then int lrow[m], m in [1, n]
     __shared__ int s_pass[kMaxF];
     const int i = blockIdx.x, tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const uint32_t st = status[i];
@@ -45,6 +57,25 @@ k3_select(const tp_inst* __restrict__ inst, const int4* __restrict__ req, const 
     const int n = nv[i];
     const tp_inst in = inst[i];
     for (int m = tid; m <= n; m += kThreads) dmin[m] = 0x7fffffffffffffffLL;
+    int* lrow = reinterpret_cast<int*>(dmin + (n + 1));
+    uint32_t st_or = 0;
+    if constexpr (WS) {
+        // LUT row of every iteration: its run's cell (binary search over the run starts)
+        const size_t row = (size_t)i * H;
+        const int h = ws.run_h[i];
+        for (int m = 1 + tid; m <= n; m += kThreads) {
+            int lo = 0, hi = h;
+            while (hi - lo > 1) {
+                const int mid = (lo + hi) >> 1;
+                if (__ldg(ws.run_m + row + mid) <= m) lo = mid;
+                else hi = mid;
+            }
+            lrow[m] = __ldg(ws.cell_tab + __ldg(ws.run_key + row + lo));
+        }
+        bool cl = false;
+        for (int k = tid; k < h; k += kThreads) cl |= __ldg(ws.cell_clamp + __ldg(ws.cell_tab + __ldg(ws.run_key + row + k))) != 0;
+        if (__syncthreads_or(cl)) st_or = TP_ST_IPS_CLAMPED;
+    }
     __syncthreads();
     const int nsched = in.n_run + nadm[i];
     for (int e = tid; e < nsched; e += kThreads) {
@@ -67,7 +98,8 @@ k3_select(const tp_inst* __restrict__ inst, const int4* __restrict__ req, const 
 #pragma unroll
             for (int j = 0; j < 4; ++j) {
                 const int m = m0 + 32 * j + lane;
-                v[j] = m <= n ? __ldg(row + m - 1) : 1.0f;
+                if constexpr (WS) v[j] = m <= n ? __ldg(ws.lut + (size_t)lrow[m] * F + u) : 1.0f;
+                else v[j] = m <= n ? __ldg(row + m - 1) : 1.0f;
             }
             bool bad = false;
 #pragma unroll
@@ -104,9 +136,10 @@ k3_select(const tp_inst* __restrict__ inst, const int4* __restrict__ req, const 
         if (lane == 0) {
             if (pass) {
                 level[i] = __ffs(pass) - 1;
+                if (st_or) status[i] = st | st_or;
             } else {
                 level[i] = F - 1;
-                status[i] = st | TP_ST_INFEASIBLE;
+                status[i] = st | st_or | TP_ST_INFEASIBLE;
             }
         }
     }
@@ -116,21 +149,37 @@ k3_select(const tp_inst* __restrict__ inst, const int4* __restrict__ req, const 
 
 int launch_select(const tp_inst* inst, int32_t n_inst, const tp_req* req, int32_t n_req, const double* t_dead,
                   const int32_t* n, const int32_t* n_adm, const float* ips, int32_t H, int32_t F,
-                  int64_t tbt_ticks, int32_t* level, uint32_t* status, int64_t* tr, cudaStream_t s) {
+                  int64_t tbt_ticks, int32_t* level, uint32_t* status, int64_t* tr, const K2Params* ws,
+                  cudaStream_t s) {
     (void)n_req;
     if (n_inst == 0) return TP_OK;
-    const size_t smem = (size_t)(H + 1) * sizeof(long long);
     int dev = 0;
     if (cudaGetDevice(&dev) != cudaSuccess) return TP_ECUDA;
-    static bool attr_done[64] = {};
-    if (dev < 64 && !attr_done[dev]) {
-        if (cudaFuncSetAttribute(k3_select, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                 (kMaxH + 1) * (int)sizeof(long long)) != cudaSuccess)
-            return TP_ECUDA;
-        attr_done[dev] = true;
+    static bool attr_done[2][64] = {};
+    WsView v{};
+    if (ws) {
+        v.run_h = ws->run_h;
+        v.run_m = ws->run_m;
+        v.run_key = ws->run_key;
+        v.cell_tab = ws->cell_tab;
+        v.lut = ws->lut;
+        v.cell_clamp = ws->cell_clamp;
     }
-    k3_select<<<n_inst, kThreads, smem, s>>>(inst, reinterpret_cast<const int4*>(req), t_dead, n, n_adm, ips, H, F,
-                                             (long long)tbt_ticks, level, status, reinterpret_cast<long long*>(tr));
+    const size_t smem = (size_t)(H + 1) * (sizeof(long long) + (ws ? 4 : 0));
+    const void* fn = ws ? (const void*)k3_select<true> : (const void*)k3_select<false>;
+    if (dev < 64 && !attr_done[ws ? 1 : 0][dev]) {
+        if (cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (kMaxH + 1) * 12) != cudaSuccess)
+            return TP_ECUDA;
+        attr_done[ws ? 1 : 0][dev] = true;
+    }
+    if (ws)
+        k3_select<true><<<n_inst, kThreads, smem, s>>>(inst, reinterpret_cast<const int4*>(req), t_dead, n, n_adm,
+                                                       nullptr, H, F, (long long)tbt_ticks, level, status,
+                                                       reinterpret_cast<long long*>(tr), v);
+    else
+        k3_select<false><<<n_inst, kThreads, smem, s>>>(inst, reinterpret_cast<const int4*>(req), t_dead, n, n_adm,
+                                                        ips, H, F, (long long)tbt_ticks, level, status,
+                                                        reinterpret_cast<long long*>(tr), v);
     return cudaPeekAtLastError() == cudaSuccess ? TP_OK : TP_ECUDA;
 }
 

@@ -43,10 +43,12 @@ class Round:
         self.level = torch.empty(I, dtype=torch.int32, device=dev)
         self.ips = torch.zeros((I, F, H), dtype=torch.float32, device=dev)
         self.tr = torch.zeros((I, F, H), dtype=torch.int64, device=dev) if want_tr else None
-        assert k2_mode in ("cells", "runs", "direct")
-        assert k2_mode != "cells" or model is not None, "cell mode sizes its workspace from the model"
+        assert k2_mode in ("fused", "cells", "runs", "direct")
+        assert k2_mode not in ("cells", "fused") or model is not None, "cell mode sizes its workspace from the model"
         self.k2_mode = k2_mode
-        self.work = torch.empty(tp.tp_predict_ips_workspace_size(model if k2_mode == "cells" else None, I, H, F),
+        self.model = model
+        self.work = torch.empty(tp.tp_predict_ips_workspace_size(model if k2_mode in ("cells", "fused") else None,
+                                                                 I, H, F),
                                 dtype=torch.uint8, device=dev) if k2_mode != "direct" else None
 
     def project(self, stream=None):
@@ -54,14 +56,19 @@ class Round:
                       stream)
 
     def predict(self, model, stream=None):
-        if self.k2_mode in ("runs", "cells"):
-            tp.tp_predict_ips_runs(model, self.inst, self.I, self.B, self.KV, self.n, self.H, self.freq, self.ips,
-                                   self.status, self.work, stream)
+        if self.k2_mode in ("runs", "cells", "fused"):
+            # fused: cell mode without the ips grid (values stay in the workspace for K3)
+            tp.tp_predict_ips_runs(model, self.inst, self.I, self.B, self.KV, self.n, self.H, self.freq,
+                                   None if self.k2_mode == "fused" else self.ips, self.status, self.work, stream)
         else:
             tp.tp_predict_ips(model, self.inst, self.I, self.B, self.KV, self.n, self.H, self.freq, self.ips,
                               self.status, stream)
 
     def select(self, stream=None):
+        if self.k2_mode == "fused":
+            tp.tp_select_freq_ws(self.model, self.work, self.inst, self.I, self.req, self.R, self.t_dead, self.n,
+                                 self.n_adm, self.H, self.F, self.tbt, self.level, self.status, self.tr, stream)
+            return
         tp.tp_select_freq(self.inst, self.I, self.req, self.R, self.t_dead, self.n, self.n_adm, self.ips, self.H,
                           self.F, self.tbt, self.level, self.status, self.tr, stream)
 

@@ -30,9 +30,10 @@ def gpu():
     return tp, runner
 
 
-@pytest.fixture(params=["direct", "runs", "cells"])
+@pytest.fixture(params=["direct", "runs", "cells", "fused"])
 def mode(request):
-    """All K2 variants: tp_predict_ips (direct) and tp_predict_ips_runs in run and cell mode."""
+    """All K2 variants: tp_predict_ips (direct), tp_predict_ips_runs in run and cell mode, and cell
+    mode fused with K3 (tp_predict_ips_runs without the ips grid + tp_select_freq_ws)."""
     return request.param
 
 
@@ -42,6 +43,8 @@ def run_gpu(gpu, blob, inputs, want_tr=True, idx=None, mode="runs"):
     r = runner.Round(inputs, "cuda:0", want_tr=want_tr, k2_mode=mode, model=model)
     r.run(model)
     out = r.results(idx)
+    if mode == "fused":
+        del out["ips"]          # never materialised; T_R (tr) is still produced by K3
     del r
     model.free()
     return out
@@ -67,8 +70,9 @@ def assert_parity(got, ref, idx=None, grid=True, tr=True, compact=False):
             if ref["status"][j] & SKIP:
                 continue
             n = int(ref["n"][j])
-            g, r = got["ips"][i, :, :n], ref["ips"][j, :, :n]
-            assert np.array_equal(g.view(np.uint32), r.view(np.uint32)), f"ips instance {i}"
+            if "ips" in got:
+                g, r = got["ips"][i, :, :n], ref["ips"][j, :, :n]
+                assert np.array_equal(g.view(np.uint32), r.view(np.uint32)), f"ips instance {i}"
             if tr and "tr" in ref and "tr" in got:
                 assert np.array_equal(got["tr"][i, :, :n], ref["tr"][j, :, :n]), f"T_R instance {i}"
 
