@@ -216,7 +216,8 @@ int tp_select_freq(const tp_inst* inst, int32_t n_inst, const tp_req* req, int32
  * the IPS values live only in the workspace's per-cell table; this K3 reads them through each
  * instance's runs (same outputs as tp_select_freq on the expanded grid, bit for bit), so the
  * [n_inst][F][H] ips grid is never written or read.  TP_ST_IPS_CLAMPED is OR-ed here.
- * TP_EINVAL if the workspace / model has no cell mode.  Other arguments: as tp_select_freq.
+ * TP_EINVAL if the workspace / model has no cell mode or H > 8192.  Other arguments: as
+ * tp_select_freq.
  */
 int tp_select_freq_ws(const tp_gbdt* m, const void* workspace, const tp_inst* inst, int32_t n_inst,
                       const tp_req* req, int32_t n_req, const double* t_dead, const int32_t* n,

@@ -166,7 +166,9 @@ int tp_select_freq(const tp_inst* inst, int32_t n_inst, const tp_req* req, int32
 int tp_select_freq_ws(const tp_gbdt* m, const void* workspace, const tp_inst* inst, int32_t n_inst, const tp_req* req,
                       int32_t n_req, const double* t_dead, const int32_t* n, const int32_t* n_adm, int32_t H, int32_t F,
                       float tbt_slo, int32_t* level, uint32_t* status, int64_t* tr_ticks, void* stream) {
-    if (!m || n_inst < 0 || n_req < 0 || !H_ok(H) || F < 1 || F > tp::kMaxF || !tbt_ok(tbt_slo)) return TP_EINVAL;
+    if (!m || n_inst < 0 || n_req < 0 || !H_ok(H) || H > tp::kMaxHRunsSelect || F < 1 || F > tp::kMaxF ||
+        !tbt_ok(tbt_slo))
+        return TP_EINVAL;
     if (n_inst > 0 && (!workspace || !inst || !n || !n_adm || !level || !status || (n_req > 0 && (!req || !t_dead))))
         return TP_EINVAL;
     tp::K2Params p;
@@ -256,7 +258,7 @@ int tp_decide(tp_ctx* c, const tp_gbdt* m, const tp_inst* inst, int32_t n_inst, 
     if (rc) return rc;
     // cell mode (ctx created with the model): K2 leaves the IPS values in the LUT and K3 reads them
     // through the runs -- the ips grid is never materialised
-    const bool fused = c->k2_mode == TP_K2_RUNS && c->cells_model == m && m != nullptr;
+    const bool fused = c->k2_mode == TP_K2_RUNS && c->cells_model == m && m != nullptr && c->H <= tp::kMaxHRunsSelect;
     if (c->k2_mode == TP_K2_RUNS)
         rc = tp_predict_ips_runs(m, inst, n_inst, c->B, c->KV, c->n, c->H, freq_mhz, F, fused ? nullptr : c->ips,
                                  status, c->work, c->work_bytes, stream);

@@ -17,6 +17,7 @@ namespace {
 
 constexpr int kThreads = 256;
 constexpr int kWarps = kThreads / 32;
+constexpr int kGate = 8;        // queued candidates evaluated per block reduction
 
 __device__ __forceinline__ int64_t block_sum64(int64_t v, int64_t* red) {
     for (int o = 16; o; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
@@ -52,9 +53,10 @@ k1_project(const tp_inst* __restrict__ inst, const int4* __restrict__ req, int32
     __shared__ int64_t red64[kWarps];
     __shared__ int redi[kWarps];
     __shared__ int s_admit;
+    __shared__ int s_gate[kWarps][kGate];
 
     const int i = blockIdx.x;
-    const int tid = threadIdx.x;
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const tp_inst in = inst[i];
     const int64_t rb = in.req_begin;
     const int nr = in.n_run, nq = in.n_queue, N = in.N;
@@ -118,7 +120,7 @@ k1_project(const tp_inst* __restrict__ inst, const int4* __restrict__ req, int32
         }
         // exclusive block scan of the (sb, skv) pairs
         int xb = sb, xkv = skv;
-        const int lane = tid & 31, w = tid >> 5;
+        const int w = warp;
 #pragma unroll
         for (int o = 1; o < 32; o <<= 1) {
             const int yb = __shfl_up_sync(0xffffffffu, xb, o), ykv = __shfl_up_sync(0xffffffffu, xkv, o);
@@ -152,27 +154,71 @@ k1_project(const tp_inst* __restrict__ inst, const int4* __restrict__ req, int32
     uint32_t st = block_max(kvmax, redi) > in.kv_cap ? TP_ST_KV_OVER : 0u;
 
     // ---- FIFO gate: queued c admitted iff B[1]+1 <= max_batch and max_m KV + KV_c <= kv_cap ----
+    // Candidates are taken in batches of kGate: admitting c means admitting the whole prefix before
+    // it, so one pass computes, for every prefix p of the batch, max_m (KV[m] + sum_{j<=p} KV_j[m]);
+    // the first prefix over the cap (or over max_batch) stops the queue.  Same result as one
+    // candidate at a time, with one block reduction per batch instead of per candidate.
     int n_adm = 0;
-    for (int c = 0; c < nq; ++c) {
-        const int4 r = __ldg(&req[rb + nr + c]);
-        const int q = r.y, lc = r.z;
-        int mx = 0;
-        for (int m = lo; m < hi; ++m) mx = max(mx, sKV[m] + (m <= lc ? (m + q - 2) / N + 1 : 0));
-        mx = block_max(mx, redi);
-        if (tid == 0) s_admit = (sB[1] + 1 <= in.max_batch) && (mx <= in.kv_cap);
+    bool blocked = false;
+    for (int c0 = 0; c0 < nq && !blocked; c0 += kGate) {
+        const int cn = min(kGate, nq - c0);
+        int q[kGate], lc[kGate], mx[kGate];
+#pragma unroll
+        for (int j = 0; j < kGate; ++j) {
+            q[j] = 1;
+            lc[j] = 0;
+            mx[j] = 0;
+            if (j < cn) {
+                const int4 r = __ldg(&req[rb + nr + c0 + j]);
+                q[j] = r.y;
+                lc[j] = r.z;
+            }
+        }
+        for (int m = lo; m < hi; ++m) {
+            int run = sKV[m];
+#pragma unroll
+            for (int j = 0; j < kGate; ++j) {
+                run += (m <= lc[j]) ? (m + q[j] - 2) / N + 1 : 0;   // lc[j] = 0 past the batch
+                mx[j] = max(mx[j], run);
+            }
+        }
+#pragma unroll
+        for (int j = 0; j < kGate; ++j) mx[j] = __reduce_max_sync(0xffffffffu, mx[j]);
+        if (lane == 0)
+#pragma unroll
+            for (int j = 0; j < kGate; ++j) s_gate[warp][j] = mx[j];
         __syncthreads();
-        const int admit = s_admit;
-        if (!admit) {
+        if (tid == 0) {
+            int p = 0;
+            while (p < cn) {
+                int M = 0;
+                for (int w = 0; w < kWarps; ++w) M = max(M, s_gate[w][p]);
+                if (sB[1] + p + 1 > in.max_batch || M > in.kv_cap) break;
+                ++p;
+            }
+            s_admit = p;
+        }
+        __syncthreads();
+        const int p = s_admit;
+        for (int m = lo; m < hi; ++m) {
+            int add = 0, addb = 0;
+            for (int j = 0; j < p; ++j)
+                if (m <= lc[j]) {
+                    add += (m + q[j] - 2) / N + 1;
+                    ++addb;
+                }
+            sKV[m] += add;
+            sB[m] += addb;
+        }
+        for (int j = 0; j < p; ++j) {
+            nloc = max(nloc, lc[j]);
+            lost |= (__ldg(&req[rb + nr + c0 + j]).w & TP_REQ_LOST) != 0;
+        }
+        n_adm += p;
+        if (p < cn) {
+            blocked = true;
             st |= TP_ST_QUEUE_BLOCKED;
-            break;
         }
-        for (int m = lo; m < min(hi, lc + 1); ++m) {
-            sKV[m] += (m + q - 2) / N + 1;
-            sB[m] += 1;
-        }
-        nloc = max(nloc, lc);
-        lost |= (r.w & TP_REQ_LOST) != 0;
-        ++n_adm;
         __syncthreads();
     }
     const int n = block_max(nloc, redi);

@@ -3,14 +3,19 @@
 // the lost bypass.
 //
 // One CTA per instance, one warp per frequency level (levels strided over the 8 warps).
-//  * Per instance, the scheduled requests' deadlines become a table Dmin[l] = min over requests
-//    ending at l of ceil(fl64(t_dead - t_cur) * 2^40) (int64 ticks of 2^-40 s) in shared memory,
-//    so Eq. 4 for every request is "T_R[m] < Dmin[m] for all m <= n".
-//  * T'[m] = fl32(1/ips) lies in [2^-17, 16] s, i.e. an integer number of 2^-40 s ticks, so the
-//    warp computes the cumulative sum exactly with an int64 shuffle scan (reading A-10): any
-//    summation order gives the same bits, and the SLO comparisons are exact integer compares.
-//  * A warp stops scanning at the first violated deadline (unless T_R is requested).
-//  * The decision is the lowest passing level: a ballot over the per-level pass flags.
+//  * The scheduled requests' deadlines become a table Dmin[l] = min over requests ending at l of
+//    ceil(fl64(t_dead - t_cur) * 2^40) (int64 ticks of 2^-40 s) in shared memory, so Eq. 4 for
+//    every request is "T_R[l] < Dmin[l] at every end position l".
+//  * T'[m] = fl32(1/ips) lies in [2^-17, 16] s, i.e. an integer number of 2^-40 s ticks, so T_R is
+//    an exact int64 sum (reading A-10): any summation order gives the same bits, and the SLO
+//    comparisons are exact integer compares.
+//  * Only the lowest passing level matters: a warp skips a level above one that already passed,
+//    and stops scanning a level at its first violated deadline (unless T_R is requested).
+//
+// k3_select      reads the [I][F][H] ips grid, one iteration per lane (tp_select_freq).
+// k3_select_runs reads K2's cell LUT through the instance's runs (tp_select_freq_ws): on a run of
+//                len iterations with constant T' = t, T_R grows by len * t (exact), so T_R is
+//                formed per run and evaluated only at the requests' end positions.
 #include "tp_internal.cuh"
 
 namespace tp {
@@ -19,35 +24,61 @@ namespace {
 constexpr int kThreads = 256;
 constexpr int kWarps = kThreads / 32;
 constexpr uint32_t kSkip = TP_ST_BAD_INPUT | TP_ST_EMPTY | TP_ST_BYPASS_LOST;
+constexpr long long kNoDeadline = 0x7fffffffffffffffLL;
 
 // ceil(s * 2^40) for the E2E compare T_R < s (T_R integer ticks): <= 0 / NaN -> 0 (never passes),
 // >= 2^62 -> INT64_MAX (always passes; T_R < 2^58).
 __device__ __forceinline__ long long slack_ticks(double s) {
     const double d = s * 0x1p40;
     if (!(d > 0.0)) return 0;
-    if (d >= 0x1p62) return 0x7fffffffffffffffLL;
+    if (d >= 0x1p62) return kNoDeadline;
     return (long long)ceil(d);
 }
 
-// WS = false: IPS read from the ips grid.  WS = true (fused with K2's cell mode): IPS read from the
-// cell LUT through the instance's runs, so the ips grid is never materialised.
-struct WsView {
-    const int32_t* run_h;
-    const int32_t* run_m;
-    const uint32_t* run_key;
-    const int32_t* cell_tab;
-    const float* lut;
-    const uint32_t* cell_clamp;
-};
+// T' of one IPS value in ticks of 2^-40 s: fl32 reciprocal (reading A-9), exact scaling.
+__device__ __forceinline__ long long ticks_of(float ips) {
+    const float t = __frcp_rn(ips);
+    return (long long)(t * 0x1p40f);    // exact: t in [2^-17, 16]
+}
 
-template <bool WS>
+// Per instance: dense Dmin table over m in [1, n] (shared memory).
+__device__ __forceinline__ void build_dmin(long long* dmin, const tp_inst& in, int n_sched, int n,
+                                           const int4* __restrict__ req, const double* __restrict__ t_dead) {
+    for (int m = threadIdx.x; m <= n; m += kThreads) dmin[m] = kNoDeadline;
+    __syncthreads();
+    for (int e = threadIdx.x; e < n_sched; e += kThreads) {
+        const int64_t j = (int64_t)in.req_begin + e;
+        const int4 r = __ldg(&req[j]);
+        const double slack = __ldg(&t_dead[j]) - in.t_cur;   // fl64(t_dead - t_cur), reading A-12
+        atomicMin(&dmin[r.z - r.x], slack_ticks(slack));
+    }
+    __syncthreads();
+}
+
+__device__ __forceinline__ void finish(int i, int F, uint32_t st, uint32_t st_or, const int* s_pass,
+                                       int32_t* level, uint32_t* status) {
+    const int lane = threadIdx.x & 31;
+    if ((threadIdx.x >> 5) != 0) return;
+    const unsigned pass = __ballot_sync(0xffffffffu, lane < F && s_pass[lane]);
+    if (lane == 0) {
+        if (pass) {
+            level[i] = __ffs(pass) - 1;
+            if (st_or) status[i] = st | st_or;
+        } else {
+            level[i] = F - 1;
+            status[i] = st | st_or | TP_ST_INFEASIBLE;
+        }
+    }
+}
+
 __global__ void __launch_bounds__(kThreads)
 k3_select(const tp_inst* __restrict__ inst, const int4* __restrict__ req, const double* __restrict__ t_dead,
           const int32_t* __restrict__ nv, const int32_t* __restrict__ nadm, const float* __restrict__ ips,
           int32_t H, int32_t F, long long tbt_ticks, int32_t* __restrict__ level, uint32_t* __restrict__ status,
-          long long* __restrict__ tr, const __grid_constant__ WsView ws) {
-    extern __shared__ long long dmin[];   // index m in [1, n]; (WS) then int lrow[m], m in [1, n]
+          long long* __restrict__ tr) {
+    extern __shared__ long long dmin[];   // index m in [1, n]
     __shared__ int s_pass[kMaxF];
+    __shared__ int s_best;
     const int i = blockIdx.x, tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const uint32_t st = status[i];
     if (st & kSkip) {
@@ -56,38 +87,13 @@ k3_select(const tp_inst* __restrict__ inst, const int4* __restrict__ req, const 
     }
     const int n = nv[i];
     const tp_inst in = inst[i];
-    for (int m = tid; m <= n; m += kThreads) dmin[m] = 0x7fffffffffffffffLL;
-    int* lrow = reinterpret_cast<int*>(dmin + (n + 1));
-    uint32_t st_or = 0;
-    if constexpr (WS) {
-        // LUT row of every iteration: its run's cell (binary search over the run starts)
-        const size_t row = (size_t)i * H;
-        const int h = ws.run_h[i];
-        for (int m = 1 + tid; m <= n; m += kThreads) {
-            int lo = 0, hi = h;
-            while (hi - lo > 1) {
-                const int mid = (lo + hi) >> 1;
-                if (__ldg(ws.run_m + row + mid) <= m) lo = mid;
-                else hi = mid;
-            }
-            lrow[m] = __ldg(ws.cell_tab + __ldg(ws.run_key + row + lo));
-        }
-        bool cl = false;
-        for (int k = tid; k < h; k += kThreads) cl |= __ldg(ws.cell_clamp + __ldg(ws.cell_tab + __ldg(ws.run_key + row + k))) != 0;
-        if (__syncthreads_or(cl)) st_or = TP_ST_IPS_CLAMPED;
-    }
-    __syncthreads();
-    const int nsched = in.n_run + nadm[i];
-    for (int e = tid; e < nsched; e += kThreads) {
-        const int64_t j = (int64_t)in.req_begin + e;
-        const int4 r = __ldg(&req[j]);
-        const double slack = __ldg(&t_dead[j]) - in.t_cur;   // fl64(t_dead - t_cur), reading A-12
-        atomicMin(&dmin[r.z - r.x], slack_ticks(slack));
-    }
-    __syncthreads();
+    if (tid < kMaxF) s_pass[tid] = 0;
+    if (tid == 0) s_best = F;
+    build_dmin(dmin, in, in.n_run + nadm[i], n, req, t_dead);
 
     const long long tbt_bound = (long long)n * tbt_ticks;   // TBT: T_R[n] <= n * slo (<= 2^58)
     for (int u = warp; u < F; u += kWarps) {
+        if (!tr && u > *(volatile int*)&s_best) break;      // a lower level already passed
         const float* row = ips + ((size_t)i * F + u) * H;
         long long* trow = tr ? tr + ((size_t)i * F + u) * H : nullptr;
         long long carry = 0;
@@ -98,18 +104,13 @@ k3_select(const tp_inst* __restrict__ inst, const int4* __restrict__ req, const 
 #pragma unroll
             for (int j = 0; j < 4; ++j) {
                 const int m = m0 + 32 * j + lane;
-                if constexpr (WS) v[j] = m <= n ? __ldg(ws.lut + (size_t)lrow[m] * F + u) : 1.0f;
-                else v[j] = m <= n ? __ldg(row + m - 1) : 1.0f;
+                v[j] = m <= n ? __ldg(row + m - 1) : 1.0f;
             }
             bool bad = false;
 #pragma unroll
             for (int j = 0; j < 4; ++j) {
                 const int m = m0 + 32 * j + lane;
-                long long x = 0;
-                if (m <= n) {
-                    const float t = __frcp_rn(v[j]);                   // fl32(1 / IPS), reading A-9
-                    x = (long long)(t * 0x1p40f);                      // exact: t in [2^-17, 16]
-                }
+                long long x = m <= n ? ticks_of(v[j]) : 0;
 #pragma unroll
                 for (int o = 1; o < 32; o <<= 1) {
                     const long long y = __shfl_up_sync(0xffffffffu, x, o);
@@ -128,21 +129,147 @@ k3_select(const tp_inst* __restrict__ inst, const int4* __restrict__ req, const 
                 if (!trow) break;
             }
         }
-        if (lane == 0) s_pass[u] = ok;
-    }
-    __syncthreads();
-    if (warp == 0) {
-        const unsigned pass = __ballot_sync(0xffffffffu, lane < F && s_pass[lane]);
         if (lane == 0) {
-            if (pass) {
-                level[i] = __ffs(pass) - 1;
-                if (st_or) status[i] = st | st_or;
-            } else {
-                level[i] = F - 1;
-                status[i] = st | st_or | TP_ST_INFEASIBLE;
-            }
+            s_pass[u] = ok;
+            if (ok) atomicMin(&s_best, u);
         }
     }
+    __syncthreads();
+    finish(i, F, st, 0u, s_pass, level, status);
+}
+
+struct WsView {
+    const int32_t* run_h;
+    const int32_t* run_m;
+    const uint32_t* run_key;
+    const int32_t* cell_tab;
+    const float* lut;
+    const uint32_t* cell_clamp;
+};
+
+__global__ void __launch_bounds__(kThreads)
+k3_select_runs(const tp_inst* __restrict__ inst, const int4* __restrict__ req, const double* __restrict__ t_dead,
+               const int32_t* __restrict__ nv, const int32_t* __restrict__ nadm, int32_t H, int32_t F,
+               long long tbt_ticks, int32_t* __restrict__ level, uint32_t* __restrict__ status,
+               long long* __restrict__ tr, const __grid_constant__ WsView ws) {
+    // shared: dmin[n + 1] (int64) | e_d[n] (int64) | e_l[n] | r_start[h + 1] | r_row[h]
+    extern __shared__ long long sm[];
+    __shared__ int s_pass[kMaxF];
+    __shared__ int s_best;
+    __shared__ int swarp[kWarps];
+    const int i = blockIdx.x, tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const uint32_t st = status[i];
+    if (st & kSkip) {
+        if (tid == 0) level[i] = (st & TP_ST_BAD_INPUT) ? F - 1 : (st & TP_ST_EMPTY) ? 0 : F - 1;
+        return;
+    }
+    const int n = nv[i];
+    const size_t row = (size_t)i * H;
+    const int h = ws.run_h[i];
+    long long* dmin = sm;
+    long long* e_d = dmin + (n + 1);
+    int* e_l = reinterpret_cast<int*>(e_d + n);
+    int* r_start = e_l + n;
+    int* r_row = r_start + (h + 1);
+    const tp_inst in = inst[i];
+    if (tid < kMaxF) s_pass[tid] = 0;
+    if (tid == 0) s_best = F;
+    // runs: first iteration and LUT row; clamp flag from the cells' masks
+    bool cl = false;
+    for (int k = tid; k < h; k += kThreads) {
+        r_start[k] = __ldg(ws.run_m + row + k);
+        const int rr = __ldg(ws.cell_tab + __ldg(ws.run_key + row + k));
+        r_row[k] = rr;
+        cl |= __ldg(ws.cell_clamp + rr) != 0;
+    }
+    if (tid == 0) r_start[h] = n + 1;
+    const uint32_t st_or = __syncthreads_or(cl) ? (uint32_t)TP_ST_IPS_CLAMPED : 0u;
+    build_dmin(dmin, in, in.n_run + nadm[i], n, req, t_dead);
+    // compact the end positions that carry a deadline (ascending)
+    int ne = 0;
+    for (int m0 = 1; m0 <= n; m0 += kThreads) {
+        const int m = m0 + tid;
+        const bool has = m <= n && dmin[m] != kNoDeadline;
+        const unsigned mask = __ballot_sync(0xffffffffu, has);
+        if (lane == 0) swarp[warp] = __popc(mask);
+        __syncthreads();
+        int before = ne;
+        for (int w = 0; w < warp; ++w) before += swarp[w];
+        if (has) {
+            const int pos = before + __popc(mask & ((1u << lane) - 1u));
+            e_l[pos] = m;
+            e_d[pos] = dmin[m];
+        }
+        for (int w = 0; w < kWarps; ++w) ne += swarp[w];
+        __syncthreads();
+    }
+
+    const long long tbt_bound = (long long)n * tbt_ticks;
+    for (int u = warp; u < F; u += kWarps) {
+        if (!tr && u > *(volatile int*)&s_best) break;      // a lower level already passed
+        long long* trow = tr ? tr + ((size_t)i * F + u) * H : nullptr;
+        long long carry = 0;     // T_R at the last iteration before the current chunk of runs
+        int ep = 0;              // next end position to check
+        bool ok = true;
+        for (int kb = 0; kb < h; kb += 32) {
+            const int k = kb + lane;
+            int s = 0x7fffffff;
+            long long t = 0, own = 0;
+            if (k < h) {
+                s = r_start[k];
+                t = ticks_of(__ldg(ws.lut + (size_t)r_row[k] * F + u));
+                own = (long long)(r_start[k + 1] - s) * t;      // the run's share of T_R, exact
+            }
+            long long x = own;
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+                const long long y = __shfl_up_sync(0xffffffffu, x, o);
+                if (lane >= o) x += y;
+            }
+            const long long before = carry + x - own;           // T_R at iteration s - 1
+            const int chunk_end = r_start[min(kb + 32, h)] - 1;  // last iteration of this chunk
+            bool bad = false;
+            // end positions inside this chunk: lane j checks e_l[ep + j]
+            while (ep < ne && e_l[ep] <= chunk_end) {
+                const int j = ep + lane;
+                const int e = (j < ne) ? e_l[j] : 0x7fffffff;
+                const bool mine = e <= chunk_end;
+                int r = 0;   // last run of the chunk with start <= e
+#pragma unroll
+                for (int step = 16; step; step >>= 1) {
+                    const int cand = r + step;
+                    const int sc = __shfl_sync(0xffffffffu, s, cand);
+                    if (sc <= e) r = cand;
+                }
+                const long long b = __shfl_sync(0xffffffffu, before, r);
+                const long long tt = __shfl_sync(0xffffffffu, t, r);
+                const int sr = __shfl_sync(0xffffffffu, s, r);
+                if (mine) bad |= !(b + (long long)(e - sr + 1) * tt < e_d[j]);
+                ep += __popc(__ballot_sync(0xffffffffu, mine));
+            }
+            if (trow && k < h)
+                for (int m = s; m < r_start[k + 1]; ++m) trow[m - 1] = before + (long long)(m - s + 1) * t;
+            carry = __shfl_sync(0xffffffffu, carry + x, 31);
+            if (__any_sync(0xffffffffu, bad)) {
+                ok = false;
+                if (!trow) break;
+            }
+        }
+        ok = ok && carry <= tbt_bound;          // TBT at m = n: T_R[n] <= n * slo
+        if (lane == 0) {
+            s_pass[u] = ok;
+            if (ok) atomicMin(&s_best, u);
+        }
+    }
+    __syncthreads();
+    finish(i, F, st, st_or, s_pass, level, status);
+}
+
+bool set_attr(const void* fn, int bytes, bool* done, int dev) {
+    if (dev < 64 && done[dev]) return true;
+    if (cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes) != cudaSuccess) return false;
+    if (dev < 64) done[dev] = true;
+    return true;
 }
 
 }  // namespace
@@ -155,31 +282,23 @@ int launch_select(const tp_inst* inst, int32_t n_inst, const tp_req* req, int32_
     if (n_inst == 0) return TP_OK;
     int dev = 0;
     if (cudaGetDevice(&dev) != cudaSuccess) return TP_ECUDA;
-    static bool attr_done[2][64] = {};
-    WsView v{};
-    if (ws) {
-        v.run_h = ws->run_h;
-        v.run_m = ws->run_m;
-        v.run_key = ws->run_key;
-        v.cell_tab = ws->cell_tab;
-        v.lut = ws->lut;
-        v.cell_clamp = ws->cell_clamp;
+    if (!ws) {
+        static bool done[64] = {};
+        if (!set_attr((const void*)k3_select, (kMaxH + 1) * 8, done, dev)) return TP_ECUDA;
+        k3_select<<<n_inst, kThreads, (size_t)(H + 1) * 8, s>>>(inst, reinterpret_cast<const int4*>(req), t_dead, n,
+                                                                n_adm, ips, H, F, (long long)tbt_ticks, level, status,
+                                                                reinterpret_cast<long long*>(tr));
+    } else {
+        static bool done[64] = {};
+        // dmin (H+1) + e_d H (int64) + e_l H + r_start (H+1) + r_row H (int32)
+        auto bytes = [](size_t h) { return (h + 1) * 8 + h * 8 + h * 4 + (h + 1) * 4 + h * 4; };
+        if (H > kMaxHRunsSelect) return TP_EINVAL;
+        if (!set_attr((const void*)k3_select_runs, (int)bytes(kMaxHRunsSelect), done, dev)) return TP_ECUDA;
+        WsView v{ws->run_h, ws->run_m, ws->run_key, ws->cell_tab, ws->lut, ws->cell_clamp};
+        k3_select_runs<<<n_inst, kThreads, bytes((size_t)H), s>>>(inst, reinterpret_cast<const int4*>(req), t_dead, n,
+                                                                  n_adm, H, F, (long long)tbt_ticks, level, status,
+                                                                  reinterpret_cast<long long*>(tr), v);
     }
-    const size_t smem = (size_t)(H + 1) * (sizeof(long long) + (ws ? 4 : 0));
-    const void* fn = ws ? (const void*)k3_select<true> : (const void*)k3_select<false>;
-    if (dev < 64 && !attr_done[ws ? 1 : 0][dev]) {
-        if (cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (kMaxH + 1) * 12) != cudaSuccess)
-            return TP_ECUDA;
-        attr_done[ws ? 1 : 0][dev] = true;
-    }
-    if (ws)
-        k3_select<true><<<n_inst, kThreads, smem, s>>>(inst, reinterpret_cast<const int4*>(req), t_dead, n, n_adm,
-                                                       nullptr, H, F, (long long)tbt_ticks, level, status,
-                                                       reinterpret_cast<long long*>(tr), v);
-    else
-        k3_select<false><<<n_inst, kThreads, smem, s>>>(inst, reinterpret_cast<const int4*>(req), t_dead, n, n_adm,
-                                                        ips, H, F, (long long)tbt_ticks, level, status,
-                                                        reinterpret_cast<long long*>(tr), v);
     return cudaPeekAtLastError() == cudaSuccess ? TP_OK : TP_ECUDA;
 }
 

@@ -10,6 +10,7 @@ namespace tp {
 
 constexpr int kMaxF = 32;
 constexpr int kMaxH = 16384;
+constexpr int kMaxHRunsSelect = 8192;      // tp_select_freq_ws keeps ~28 B per iteration in smem
 constexpr int kMaxDepth = 12;
 constexpr int kMaxCuts = 32767;            // ranks must fit 15 bits (K2 word encoding)
 constexpr int64_t kFeatLimit = 1LL << 24;  // integer features exact in fp32
