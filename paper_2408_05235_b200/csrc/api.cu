@@ -72,6 +72,11 @@ int tp_predict_ips(const tp_gbdt* m, const tp_inst* inst, int32_t n_inst, const 
     p.words = m->m.d_words;
     p.cuts = m->m.d_cuts;
     for (int f = 0; f < 5; ++f) p.cut_off[f] = m->m.cut_off[f];
+    p.rtab = m->m.d_rtab;
+    for (int w = 0; w < 2; ++w) {
+        p.rtab_off[w] = m->m.rtab_off[w];
+        p.rtab_len[w] = m->m.rtab_len[w];
+    }
     p.n_trees = m->m.n_trees;
     p.depth = m->m.depth;
     p.base = m->m.base;
@@ -107,6 +112,11 @@ int tp_predict_ips_runs(const tp_gbdt* m, const tp_inst* inst, int32_t n_inst, c
     p.words = m->m.d_words;
     p.cuts = m->m.d_cuts;
     for (int f = 0; f < 5; ++f) p.cut_off[f] = m->m.cut_off[f];
+    p.rtab = m->m.d_rtab;
+    for (int w = 0; w < 2; ++w) {
+        p.rtab_off[w] = m->m.rtab_off[w];
+        p.rtab_len[w] = m->m.rtab_len[w];
+    }
     p.n_trees = m->m.n_trees;
     p.depth = m->m.depth;
     p.base = m->m.base;

@@ -174,11 +174,29 @@ k1_project(const tp_inst* __restrict__ inst, const int4* __restrict__ req, int32
                 lc[j] = r.z;
             }
         }
+        // candidate j's Eq. 1 blocks over this thread's segment, incrementally: kv = ceil(t / N) with
+        // t = m - 1 + q tokens and d = (t - 1) mod N; m -> m + 1 adds a block when d wraps to 0
+        int kvj[kGate], dj[kGate];
+#pragma unroll
+        for (int j = 0; j < kGate; ++j) {
+            kvj[j] = dj[j] = 0;
+            if (j < cn) {
+                const int t1 = lo + q[j] - 2;          // t - 1 at m = lo (>= 0)
+                kvj[j] = t1 / N + 1;
+                dj[j] = t1 - (kvj[j] - 1) * N;
+            }
+        }
         for (int m = lo; m < hi; ++m) {
             int run = sKV[m];
 #pragma unroll
             for (int j = 0; j < kGate; ++j) {
-                run += (m <= lc[j]) ? (m + q[j] - 2) / N + 1 : 0;   // lc[j] = 0 past the batch
+                if (j < cn) {
+                    run += (m <= lc[j]) ? kvj[j] : 0;
+                    if (++dj[j] == N) {
+                        dj[j] = 0;
+                        ++kvj[j];
+                    }
+                }
                 mx[j] = max(mx[j], run);
             }
         }
@@ -200,15 +218,31 @@ k1_project(const tp_inst* __restrict__ inst, const int4* __restrict__ req, int32
         }
         __syncthreads();
         const int p = s_admit;
-        for (int m = lo; m < hi; ++m) {
-            int add = 0, addb = 0;
-            for (int j = 0; j < p; ++j)
-                if (m <= lc[j]) {
-                    add += (m + q[j] - 2) / N + 1;
-                    ++addb;
+        if (p > 0) {
+#pragma unroll
+            for (int j = 0; j < kGate; ++j)
+                if (j < p) {
+                    const int t1 = lo + q[j] - 2;
+                    kvj[j] = t1 / N + 1;
+                    dj[j] = t1 - (kvj[j] - 1) * N;
                 }
-            sKV[m] += add;
-            sB[m] += addb;
+            for (int m = lo; m < hi; ++m) {
+                int add = 0, addb = 0;
+#pragma unroll
+                for (int j = 0; j < kGate; ++j)
+                    if (j < p) {
+                        if (m <= lc[j]) {
+                            add += kvj[j];
+                            ++addb;
+                        }
+                        if (++dj[j] == N) {
+                            dj[j] = 0;
+                            ++kvj[j];
+                        }
+                    }
+                sKV[m] += add;
+                sB[m] += addb;
+            }
         }
         for (int j = 0; j < p; ++j) {
             nloc = max(nloc, lc[j]);

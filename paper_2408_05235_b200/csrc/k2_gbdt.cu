@@ -122,22 +122,12 @@ __device__ __forceinline__ int64_t units_of(const K2Params& p, int i, int G) {
 // compaction of the run heads.  Cell mode also claims each run's cell (rank_tp, rank_B,
 // rank_KV) in a dense table and appends first-seen cells to the cell list.
 constexpr int kRunsThreads = 256;
-constexpr int kRunsCutCap = 2048;     // cuts per feature staged in shared memory (else global)
-
-__device__ __forceinline__ uint32_t rank_smem(const float* c, int cnt, float x) {
-    int lo = 0, hi = cnt;
-    while (lo < hi) {
-        const int mid = (lo + hi) >> 1;
-        if (c[mid] <= x) lo = mid + 1;
-        else hi = mid;
-    }
-    return (uint32_t)lo;
-}
+constexpr int kRunsTabCap = 8192;     // rank-table entries per feature staged in shared memory
 
 __global__ void __launch_bounds__(kRunsThreads)
 k2_runs(const __grid_constant__ K2Params p) {
     extern __shared__ uint32_t skey[];               // [H + 1]: key of iteration m at skey[m]
-    __shared__ float scB[kRunsCutCap], scKV[kRunsCutCap];
+    __shared__ uint16_t stB[kRunsTabCap], stKV[kRunsTabCap];
     __shared__ int swarp[kRunsThreads / 32];
     const int i = blockIdx.x, tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int n = (p.status[i] & kSkip) ? 0 : p.n[i];
@@ -146,11 +136,12 @@ k2_runs(const __grid_constant__ K2Params p) {
         return;
     }
     const int nB = p.cut_off[2] - p.cut_off[1], nKV = p.cut_off[3] - p.cut_off[2];
-    const bool smB = nB <= kRunsCutCap, smKV = nKV <= kRunsCutCap;
-    if (smB)
-        for (int j = tid; j < nB; j += kRunsThreads) scB[j] = p.cuts[p.cut_off[1] + j];
-    if (smKV)
-        for (int j = tid; j < nKV; j += kRunsThreads) scKV[j] = p.cuts[p.cut_off[2] + j];
+    // rank tables (exact for integer features): shared-memory copies of at most kRunsTabCap
+    // entries, the rest of each table from global memory, a binary search beyond it
+    const int lB = p.rtab_len[0], lKV = p.rtab_len[1];
+    const int sB = min(lB, kRunsTabCap), sKV = min(lKV, kRunsTabCap);
+    for (int j = tid; j < sB; j += kRunsThreads) stB[j] = p.rtab[p.rtab_off[0] + j];
+    for (int j = tid; j < sKV; j += kRunsThreads) stKV[j] = p.rtab[p.rtab_off[1] + j];
     __syncthreads();
     const bool cells = p.cell_tab != nullptr;
     uint32_t cell_base = 0;
@@ -160,9 +151,11 @@ k2_runs(const __grid_constant__ K2Params p) {
     }
     const size_t row = (size_t)i * p.H;
     for (int m = 1 + tid; m <= n; m += kRunsThreads) {
-        const float b = (float)p.B[row + m - 1], kv = (float)p.KV[row + m - 1];
-        const uint32_t rb = smB ? rank_smem(scB, nB, b) : rank_of(p.cuts + p.cut_off[1], nB, b);
-        const uint32_t rk = smKV ? rank_smem(scKV, nKV, kv) : rank_of(p.cuts + p.cut_off[2], nKV, kv);
+        const int b = p.B[row + m - 1], kv = p.KV[row + m - 1];
+        const uint32_t rb = b < sB ? stB[b] : b < lB ? p.rtab[p.rtab_off[0] + b]
+                                                     : rank_of(p.cuts + p.cut_off[1], nB, (float)b);
+        const uint32_t rk = kv < sKV ? stKV[kv] : kv < lKV ? p.rtab[p.rtab_off[1] + kv]
+                                                           : rank_of(p.cuts + p.cut_off[2], nKV, (float)kv);
         skey[m] = cells ? cell_base + rb * (uint32_t)(nKV + 1) + rk : (rb | (rk << 16));
     }
     __syncthreads();
@@ -398,8 +391,9 @@ k2_gbdt(const __grid_constant__ K2Params p, int TC, int nchunks) {
                         bv = p.B[(size_t)i * p.H + m - 1];
                         kvv = p.KV[(size_t)i * p.H + m - 1];
                     }
-                    xlo = rank_of(cutsTP, nTP, (float)p.inst[i].tp) | (rank_of(cutsB, nB, (float)bv) << 16);
-                    rkv = rank_of(cutsKV, nKV, (float)kvv);
+                    const uint32_t rb = bv < p.rtab_len[0] ? p.rtab[p.rtab_off[0] + bv] : rank_of(cutsB, nB, (float)bv);
+                    rkv = kvv < p.rtab_len[1] ? p.rtab[p.rtab_off[1] + kvv] : rank_of(cutsKV, nKV, (float)kvv);
+                    xlo = rank_of(cutsTP, nTP, (float)p.inst[i].tp) | (rb << 16);
                 }
             }
 #pragma unroll

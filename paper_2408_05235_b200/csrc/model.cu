@@ -135,6 +135,18 @@ extern "C" int tp_gbdt_load(const void* host_blob, size_t nbytes, int device, tp
     }
     m.cut_off[4] = (int32_t)allc.size();
     allc.push_back(0.f);   // never empty
+    // rank tables for integer batch / KV values: rank(x) = #cuts <= x for x in [0, len)
+    std::vector<uint16_t> rtab;
+    for (int w = 0; w < 2; ++w) {
+        const std::vector<float>& c = cuts[1 + w];
+        int64_t len = 0;
+        if (!c.empty() && c.back() >= 0.f) len = std::min<int64_t>((int64_t)std::floor(c.back()) + 1, tp::kRankTabMax);
+        m.rtab_off[w] = (int32_t)rtab.size();
+        m.rtab_len[w] = (int32_t)len;
+        for (int64_t x = 0; x < len; ++x)
+            rtab.push_back((uint16_t)(std::upper_bound(c.begin(), c.end(), (float)x) - c.begin()));
+    }
+    rtab.push_back(0);
 
     int prev = 0;
     if (cudaGetDevice(&prev) != cudaSuccess || cudaSetDevice(device) != cudaSuccess) {
@@ -142,14 +154,16 @@ extern "C" int tp_gbdt_load(const void* host_blob, size_t nbytes, int device, tp
         return TP_ECUDA;
     }
     int rc = TP_OK;
-    size_t wb = words.size() * 4, cb = allc.size() * 4;
-    if (cudaMalloc(&m.d_words, wb) != cudaSuccess || cudaMalloc(&m.d_cuts, cb) != cudaSuccess) {
+    size_t wb = words.size() * 4, cb = allc.size() * 4, rb = rtab.size() * 2;
+    if (cudaMalloc(&m.d_words, wb) != cudaSuccess || cudaMalloc(&m.d_cuts, cb) != cudaSuccess ||
+        cudaMalloc(&m.d_rtab, rb) != cudaSuccess) {
         rc = TP_ENOMEM;
     } else if (cudaMemcpy(m.d_words, words.data(), wb, cudaMemcpyHostToDevice) != cudaSuccess ||
-               cudaMemcpy(m.d_cuts, allc.data(), cb, cudaMemcpyHostToDevice) != cudaSuccess) {
+               cudaMemcpy(m.d_cuts, allc.data(), cb, cudaMemcpyHostToDevice) != cudaSuccess ||
+               cudaMemcpy(m.d_rtab, rtab.data(), rb, cudaMemcpyHostToDevice) != cudaSuccess) {
         rc = TP_ECUDA;
     }
-    m.device_bytes = (int64_t)(wb + cb);
+    m.device_bytes = (int64_t)(wb + cb + rb);
     cudaSetDevice(prev);
     if (rc != TP_OK) {
         tp_gbdt_free(h);
@@ -166,6 +180,7 @@ extern "C" int tp_gbdt_free(tp_gbdt* h) {
     cudaSetDevice(h->m.device);
     if (h->m.d_words) cudaFree(h->m.d_words);
     if (h->m.d_cuts) cudaFree(h->m.d_cuts);
+    if (h->m.d_rtab) cudaFree(h->m.d_rtab);
     cudaSetDevice(prev);
     delete h;
     return TP_OK;

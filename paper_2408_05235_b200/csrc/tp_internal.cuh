@@ -14,6 +14,7 @@ constexpr int kMaxHRunsSelect = 8192;      // tp_select_freq_ws keeps ~28 B per 
 constexpr int kMaxDepth = 12;
 constexpr int kMaxCuts = 32767;            // ranks must fit 15 bits (K2 word encoding)
 constexpr int64_t kFeatLimit = 1LL << 24;  // integer features exact in fp32
+constexpr int kRankTabMax = 1 << 16;       // rank table entries per integer feature
 
 // Device-resident, normalised ensemble (built by tp_gbdt_load, model.cu).
 //
@@ -37,6 +38,10 @@ struct Model {
     uint32_t* d_words = nullptr;   // n_trees * (2 << depth)
     float* d_cuts = nullptr;       // concatenated sorted cuts, feature order
     int32_t cut_off[5] = {0, 0, 0, 0, 0};
+    // rank tables for the integer features batch (0) and KV (1): rank(x) = rtab[off + x] for
+    // 0 <= x < len (len <= 65536; beyond it, a binary search over the cuts)
+    uint16_t* d_rtab = nullptr;
+    int32_t rtab_off[2] = {0, 0}, rtab_len[2] = {0, 0};
     int64_t device_bytes = 0;
 };
 
@@ -54,6 +59,8 @@ struct K2Params {
     float* ips;
     int32_t n_inst, H, F;
     float freq[kMaxF];
+    const uint16_t* rtab;
+    int32_t rtab_off[2], rtab_len[2];
     // run-compressed mode (tp_predict_ips_runs): consecutive iterations with identical
     // (batch, KV) threshold ranks form a run; the ensemble is evaluated once per run.
     int32_t* run_h;          // [n_inst] runs per instance (0 for skipped instances)
