@@ -60,6 +60,7 @@ k1_project(const tp_inst* __restrict__ inst, const int4* __restrict__ req, int32
     const tp_inst in = inst[i];
     const int64_t rb = in.req_begin;
     const int nr = in.n_run, nq = in.n_queue, N = in.N;
+    const FastDiv fdN((uint32_t)(N > 0 ? N : 1));
 
     for (int m = tid; m < H + 2; m += kThreads) sB[m] = sKV[m] = 0;
 
@@ -74,7 +75,7 @@ k1_project(const tp_inst* __restrict__ inst, const int4* __restrict__ req, int32
             const bool eb = r.x < 0 || r.y < 1 || r.z < 1 || r.x >= kFeatLimit || r.y >= kFeatLimit || l < 1 ||
                             l > H || (e >= nr && r.x != 0);
             bad |= eb;
-            if (!eb) foot += ((int64_t)r.x + l - 1 + r.y + N - 1) / N;
+            if (!eb) foot += (int64_t)fdN.div((uint32_t)(r.x + l - 2 + r.y)) + 1;   // ceil((a+l-1+q)/N)
         }
     }
     bad = __syncthreads_or(bad);
@@ -103,9 +104,11 @@ k1_project(const tp_inst* __restrict__ inst, const int4* __restrict__ req, int32
         const int aq = a + q;
         atomicAdd(&sB[1], 1);
         atomicAdd(&sB[l + 1], -1);
-        atomicAdd(&sKV[1], (aq - 1) / N + 1);                           // ceil(aq / N), aq >= 1
-        for (int64_t m = 2 + (int64_t)((N - aq % N) % N); m <= l; m += N) atomicAdd(&sKV[m], 1);
-        atomicAdd(&sKV[l + 1], -((aq + l - 2) / N + 1));                // -ceil((aq + l - 1) / N)
+        const int c1 = (int)fdN.div((uint32_t)(aq - 1));                 // ceil(aq / N) - 1, aq >= 1
+        atomicAdd(&sKV[1], c1 + 1);
+        // first m >= 2 with (aq + m - 2) % N == 0, then every N iterations
+        for (int64_t m = 2 + (int64_t)(c1 + 1) * N - aq; m <= l; m += N) atomicAdd(&sKV[m], 1);
+        atomicAdd(&sKV[l + 1], -((int)fdN.div((uint32_t)(aq + l - 2)) + 1));   // -ceil((aq + l - 1) / N)
     }
     lost = __syncthreads_or(lost);
 
@@ -182,11 +185,15 @@ k1_project(const tp_inst* __restrict__ inst, const int4* __restrict__ req, int32
             kvj[j] = dj[j] = 0;
             if (j < cn) {
                 const int t1 = lo + q[j] - 2;          // t - 1 at m = lo (>= 0)
-                kvj[j] = t1 / N + 1;
+                kvj[j] = (int)fdN.div((uint32_t)t1) + 1;
                 dj[j] = t1 - (kvj[j] - 1) * N;
             }
         }
-        for (int m = lo; m < hi; ++m) {
+        int maxlc = 0;
+#pragma unroll
+        for (int j = 0; j < kGate; ++j) maxlc = max(maxlc, lc[j]);
+        const int mlim = min(hi, maxlc + 1);     // past every candidate's window only KV[m] counts
+        for (int m = lo; m < mlim; ++m) {
             int run = sKV[m];
 #pragma unroll
             for (int j = 0; j < kGate; ++j) {
@@ -200,6 +207,10 @@ k1_project(const tp_inst* __restrict__ inst, const int4* __restrict__ req, int32
                 mx[j] = max(mx[j], run);
             }
         }
+        int tail = 0;
+        for (int m = max(lo, mlim); m < hi; ++m) tail = max(tail, sKV[m]);
+#pragma unroll
+        for (int j = 0; j < kGate; ++j) mx[j] = max(mx[j], tail);
 #pragma unroll
         for (int j = 0; j < kGate; ++j) mx[j] = __reduce_max_sync(0xffffffffu, mx[j]);
         if (lane == 0)
@@ -223,10 +234,10 @@ k1_project(const tp_inst* __restrict__ inst, const int4* __restrict__ req, int32
             for (int j = 0; j < kGate; ++j)
                 if (j < p) {
                     const int t1 = lo + q[j] - 2;
-                    kvj[j] = t1 / N + 1;
+                    kvj[j] = (int)fdN.div((uint32_t)t1) + 1;
                     dj[j] = t1 - (kvj[j] - 1) * N;
                 }
-            for (int m = lo; m < hi; ++m) {
+            for (int m = lo; m < mlim; ++m) {
                 int add = 0, addb = 0;
 #pragma unroll
                 for (int j = 0; j < kGate; ++j)
@@ -244,10 +255,12 @@ k1_project(const tp_inst* __restrict__ inst, const int4* __restrict__ req, int32
                 sB[m] += addb;
             }
         }
-        for (int j = 0; j < p; ++j) {
-            nloc = max(nloc, lc[j]);
-            lost |= (__ldg(&req[rb + nr + c0 + j]).w & TP_REQ_LOST) != 0;
-        }
+#pragma unroll
+        for (int j = 0; j < kGate; ++j)
+            if (j < p) {
+                nloc = max(nloc, lc[j]);
+                lost |= (__ldg(&req[rb + nr + c0 + j]).w & TP_REQ_LOST) != 0;
+            }
         n_adm += p;
         if (p < cn) {
             blocked = true;
@@ -257,9 +270,19 @@ k1_project(const tp_inst* __restrict__ inst, const int4* __restrict__ req, int32
     }
     const int n = block_max(nloc, redi);
 
-    for (int m = tid; m < H; m += kThreads) {
-        Bout[(int64_t)i * H + m] = sB[m + 1];
-        KVout[(int64_t)i * H + m] = sKV[m + 1];
+    if ((H & 3) == 0) {   // rows 16-byte aligned: 128-bit stores
+        int4* b4 = reinterpret_cast<int4*>(Bout + (int64_t)i * H);
+        int4* k4 = reinterpret_cast<int4*>(KVout + (int64_t)i * H);
+        for (int v = tid; v < (H >> 2); v += kThreads) {
+            const int m = 4 * v + 1;
+            b4[v] = make_int4(sB[m], sB[m + 1], sB[m + 2], sB[m + 3]);
+            k4[v] = make_int4(sKV[m], sKV[m + 1], sKV[m + 2], sKV[m + 3]);
+        }
+    } else {
+        for (int m = tid; m < H; m += kThreads) {
+            Bout[(int64_t)i * H + m] = sB[m + 1];
+            KVout[(int64_t)i * H + m] = sKV[m + 1];
+        }
     }
     if (tid == 0) {
         if (n == 0) st |= TP_ST_EMPTY;

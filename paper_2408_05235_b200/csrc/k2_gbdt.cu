@@ -26,8 +26,9 @@ namespace {
 
 constexpr int kMaxThreads = 384;        // CTA size is a launch parameter (256 or 384 threads)
 constexpr int kMaxWarps = kMaxThreads / 32;
-constexpr int kDefaultThreads = 384, kDefaultThreadsRuns = 128;              // measured best (C2, C3)
-constexpr int kDefaultChunkBytes = 48 * 1024, kDefaultChunkBytesRuns = 16 * 1024;
+// measured best (tools/k2_sweep.py, tools/k2_cells_sweep.py on C2 / C3)
+constexpr int kDefaultThreads = 384, kDefaultThreadsRuns = 128, kDefaultThreadsCells = 256;
+constexpr int kDefaultChunkBytes = 48 * 1024, kDefaultChunkBytesRuns = 16 * 1024, kDefaultChunkBytesCells = 32 * 1024;
 constexpr uint32_t kSkip = TP_ST_BAD_INPUT | TP_ST_EMPTY | TP_ST_BYPASS_LOST;
 
 __device__ __forceinline__ uint32_t smem_addr(const void* p) {
@@ -501,9 +502,14 @@ int launch_d(const K2Params& p, cudaStream_t s) {
     const int TW = (2 << D) < 4 ? 4 : (2 << D);
     const int tree_bytes = TW * 4;
     static const int threads =
-        env_int("TP_K2_THREADS", MODE == kDirect ? kDefaultThreads : kDefaultThreadsRuns, 64, kMaxThreads, 32);
+        env_int("TP_K2_THREADS",
+                MODE == kDirect ? kDefaultThreads : MODE == kRuns ? kDefaultThreadsRuns : kDefaultThreadsCells, 64,
+                kMaxThreads, 32);
     static const int chunk_bytes =
-        env_int("TP_K2_CHUNK_KB", (MODE == kDirect ? kDefaultChunkBytes : kDefaultChunkBytesRuns) / 1024, 4, 100, 1) *
+        env_int("TP_K2_CHUNK_KB",
+                (MODE == kDirect ? kDefaultChunkBytes : MODE == kRuns ? kDefaultChunkBytesRuns : kDefaultChunkBytesCells) /
+                    1024,
+                4, 100, 1) *
         1024;
     int TC = std::max(1, std::min(std::max(p.n_trees, 1), chunk_bytes / tree_bytes));
     const int nchunks = p.n_trees == 0 ? 0 : (p.n_trees + TC - 1) / TC;
@@ -560,10 +566,14 @@ int launch_ru(const K2Params& p, cudaStream_t s) {
     }
 }
 
+// Rows per lane: RU = 8 levels (fewer when F is small).  TP_K2_RU (2/4/8) overrides it per mode:
+// fewer rows per lane = more warps for the same work (latency-bound small problems).
 template <int MODE>
 int launch_mode(const K2Params& p, cudaStream_t s) {
-    if (p.F <= 2) return launch_ru<2, MODE>(p, s);
-    if (p.F <= 4) return launch_ru<4, MODE>(p, s);
+    static const int ru_env = env_int(MODE == kCells ? "TP_K2_RU_CELLS" : "TP_K2_RU", MODE == kCells ? 2 : 8, 2, 8, 2);
+    const int ru = std::min(ru_env, p.F <= 2 ? 2 : p.F <= 4 ? 4 : 8);
+    if (ru <= 2) return launch_ru<2, MODE>(p, s);
+    if (ru <= 4) return launch_ru<4, MODE>(p, s);
     return launch_ru<8, MODE>(p, s);
 }
 

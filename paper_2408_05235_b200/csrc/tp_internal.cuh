@@ -16,6 +16,27 @@ constexpr int kMaxCuts = 32767;            // ranks must fit 15 bits (K2 word en
 constexpr int64_t kFeatLimit = 1LL << 24;  // integer features exact in fp32
 constexpr int kRankTabMax = 1 << 16;       // rank table entries per integer feature
 
+// Unsigned division by a run-time invariant d >= 1, exact for every 32-bit dividend (Granlund &
+// Montgomery, "Division by invariant integers using multiplication", 1994, Fig. 4.1):
+// l = ceil(log2 d), m = floor(2^32 (2^l - d) / d) + 1, q = (t + ((n - t) >> min(l,1))) >> max(l-1,0),
+// t = mulhi(m, n).  Used by K1 for the per-instance block size N.
+struct FastDiv {
+    uint32_t m, s1, s2;
+    __host__ __device__ explicit FastDiv(uint32_t d) {
+        uint32_t l = 0;
+        while (l < 32 && (1ull << l) < d) ++l;
+        m = (uint32_t)((((1ull << l) - d) << 32) / d + 1);
+        s1 = l < 1 ? l : 1;
+        s2 = l > 1 ? l - 1 : 0;
+    }
+#ifdef __CUDACC__
+    __device__ __forceinline__ uint32_t div(uint32_t n) const {
+        const uint32_t t = __umulhi(m, n);
+        return (t + ((n - t) >> s1)) >> s2;
+    }
+#endif
+};
+
 // Device-resident, normalised ensemble (built by tp_gbdt_load, model.cu).
 //
 // Node words: tree t occupies words[t * TW .. (t + 1) * TW), TW = max(4, 2 << D), a complete binary heap

@@ -288,3 +288,30 @@ def test_concurrent_streams_share_model(gpu, oracle_mod):
     torch.cuda.synchronize()
     assert_parity(ra.results(), run_oracle(oracle_mod, blob, a_in), tr=False)
     assert_parity(rb.results(), run_oracle(oracle_mod, blob, b_in), tr=False)
+
+
+@pytest.mark.parametrize("N", [7, 1000, 1 << 20])
+def test_block_sizes(gpu, oracle_mod, mode, N):
+    """K1's block arithmetic (division by N, block boundaries) for unusual N."""
+    cfg = dataclasses.replace(W.CONFIGS["P1"], n_inst=40, N=N, seed=6000 + N % 97)
+    blob = W.write_blob(W.config_ensemble(W.CONFIGS["P1"]))
+    inputs = W.config_inputs(cfg)
+    assert_parity(run_gpu(gpu, blob, inputs, mode=mode), run_oracle(oracle_mod, blob, inputs))
+
+
+def test_imported_sklearn_model(gpu, oracle_mod, mode):
+    """A trained scikit-learn ensemble imported through model_io (N4) runs the whole path bit-exact."""
+    from sklearn.ensemble import HistGradientBoostingRegressor
+    from paper_2408_05235_b200 import model_io
+    rng = np.random.default_rng(1)
+    n = 4000
+    tp_ = rng.choice([1, 2, 4, 8], n)
+    B = rng.integers(1, 41, n)
+    KV = (B * rng.uniform(5, 60, n)).astype(int)
+    f = rng.choice(W.freq_levels(5), n)
+    X = np.stack([tp_, B, KV, f], 1).astype(np.float32)
+    y = W.surrogate_ips(tp_, B, KV, f) * (1 + 0.03 * rng.standard_normal(n))
+    est = HistGradientBoostingRegressor(max_iter=60, max_depth=6, random_state=0).fit(X, y)
+    blob = model_io.to_blob(model_io.from_sklearn(est))
+    inputs = W.config_inputs(dataclasses.replace(W.CONFIGS["P1"], n_inst=48, seed=777))
+    assert_parity(run_gpu(gpu, blob, inputs, mode=mode), run_oracle(oracle_mod, blob, inputs))
