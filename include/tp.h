@@ -257,6 +257,32 @@ int tp_ctx_set_k2_mode(tp_ctx* c, int mode);
 /* Device pointers of the context's scratch (for inspection / tests); any out may be NULL. */
 int tp_ctx_buffers(tp_ctx* c, int32_t** B, int32_t** KV, int32_t** n, int32_t** n_adm, float** ips);
 
+/*
+ * Trace replay (BASELINE configs[3]): advance every instance by one engine
+ * iteration after a decision round, on the GPU.  The request table uses fixed slots: instance i owns
+ * req[i * slot_cap .. (i + 1) * slot_cap) (inst[i].req_begin must be i * slot_cap), running entries
+ * first, then the FIFO queue.  For each instance with n > 0 the iteration lasts
+ * T' = fl32(1 / clamp(M(tp, B[1], KV[1], freq_mhz[level]))) seconds (the Scheduler's own time
+ * model): t_cur += T', k += 1; every scheduled request (running + the n_adm admitted
+ * queued ones) emits one token (a += 1) and completes when a == r (struck; oracle
+ * length predictor); the rest of the queue stays.  An idle instance (n = 0) jumps its
+ * clock to its next arrival.  Arrivals (per instance, sorted by time: arr_t[arr_off[i] ..
+ * arr_off[i+1]), records arr_req with deadlines arr_dead) with arr_t <= the new clock join the
+ * queue tail, up to slot_cap (the rest are dropped).  BAD_INPUT instances are left as they are.
+ *   inst [dev] in/out (n_run, n_queue, k, t_cur);  req, t_dead [dev] in;  req_out, t_dead_out
+ *   [dev] out (same slot layout; the caller swaps the buffers);  B, KV, n, n_adm, status, level
+ *   [dev] the round's K1 / K3 outputs;  freq_mhz [host] the round's levels;  arr_next [dev] in/out
+ *   next arrival per instance;  stats [dev] uint64[5] accumulators: completed, completed before
+ *   their deadline (Eq. 4), dropped arrivals, engine iterations, admissions.
+ */
+int tp_replay_advance(const tp_gbdt* m, tp_inst* inst, int32_t n_inst, const tp_req* req,
+                      const double* t_dead, tp_req* req_out, double* t_dead_out, int32_t slot_cap,
+                      int32_t H, const int32_t* B, const int32_t* KV, const int32_t* n,
+                      const int32_t* n_adm, const uint32_t* status, const int32_t* level,
+                      const float* freq_mhz, int32_t F, const double* arr_t, const tp_req* arr_req,
+                      const double* arr_dead, const int64_t* arr_off, int64_t* arr_next,
+                      uint64_t* stats, void* stream);
+
 const char* tp_strerror(int code);
 int tp_abi_version(void);
 

@@ -60,7 +60,9 @@ k1_project(const tp_inst* __restrict__ inst, const int4* __restrict__ req, int32
     const tp_inst in = inst[i];
     const int64_t rb = in.req_begin;
     const int nr = in.n_run, nq = in.n_queue, N = in.N;
-    const FastDiv fdN((uint32_t)(N > 0 ? N : 1));
+    // the divider for N is a per-instance constant: one thread builds it (64-bit division)
+    __shared__ FastDiv s_fd;
+    if (tid == 0) s_fd = FastDiv((uint32_t)(N > 0 ? N : 1));
 
     for (int m = tid; m < H + 2; m += kThreads) sB[m] = sKV[m] = 0;
 
@@ -68,6 +70,8 @@ k1_project(const tp_inst* __restrict__ inst, const int4* __restrict__ req, int32
     bool bad = N < 1 || in.tp < 1 || (int64_t)in.tp >= kFeatLimit || nr < 0 || nq < 0 || in.kv_cap < 0 ||
                in.max_batch < 0 || rb < 0 || rb + (int64_t)nr + nq > (int64_t)n_req;
     int64_t foot = 0;
+    __syncthreads();
+    const FastDiv fdN = s_fd;
     if (!bad) {
         for (int e = tid; e < nr + nq; e += kThreads) {
             const int4 r = __ldg(&req[rb + e]);
@@ -78,7 +82,7 @@ k1_project(const tp_inst* __restrict__ inst, const int4* __restrict__ req, int32
             if (!eb) foot += (int64_t)fdN.div((uint32_t)(r.x + l - 2 + r.y)) + 1;   // ceil((a+l-1+q)/N)
         }
     }
-    bad = __syncthreads_or(bad);
+    bad = __syncthreads_or(bad);   // (also publishes s_fd)
     if (!bad) bad = block_sum64(foot, red64) >= kFeatLimit;
     if (bad) {
         for (int m = tid; m < H; m += kThreads) {
@@ -114,6 +118,7 @@ k1_project(const tp_inst* __restrict__ inst, const int4* __restrict__ req, int32
 
     // ---- inclusive scans: thread t owns the contiguous segment [lo, hi) of m ----
     const int S = (H + kThreads - 1) / kThreads;
+    int kvmax = 0;
     const int lo = 1 + tid * S, hi = min(lo + S, H + 1);
     {
         int sb = 0, skv = 0;
@@ -148,12 +153,11 @@ k1_project(const tp_inst* __restrict__ inst, const int4* __restrict__ req, int32
             pkv += sKV[m];
             sB[m] = pb;
             sKV[m] = pkv;
+            kvmax = max(kvmax, pkv);
         }
     }
     __syncthreads();
 
-    int kvmax = 0;
-    for (int m = lo; m < hi; ++m) kvmax = max(kvmax, sKV[m]);
     uint32_t st = block_max(kvmax, redi) > in.kv_cap ? TP_ST_KV_OVER : 0u;
 
     // ---- FIFO gate: queued c admitted iff B[1]+1 <= max_batch and max_m KV + KV_c <= kv_cap ----
@@ -166,6 +170,7 @@ k1_project(const tp_inst* __restrict__ inst, const int4* __restrict__ req, int32
     for (int c0 = 0; c0 < nq && !blocked; c0 += kGate) {
         const int cn = min(kGate, nq - c0);
         int q[kGate], lc[kGate], mx[kGate];
+        uint32_t lostmask = 0;
 #pragma unroll
         for (int j = 0; j < kGate; ++j) {
             q[j] = 1;
@@ -175,6 +180,7 @@ k1_project(const tp_inst* __restrict__ inst, const int4* __restrict__ req, int32
                 const int4 r = __ldg(&req[rb + nr + c0 + j]);
                 q[j] = r.y;
                 lc[j] = r.z;
+                if (r.w & TP_REQ_LOST) lostmask |= 1u << j;
             }
         }
         // candidate j's Eq. 1 blocks over this thread's segment, incrementally: kv = ceil(t / N) with
@@ -259,7 +265,7 @@ k1_project(const tp_inst* __restrict__ inst, const int4* __restrict__ req, int32
         for (int j = 0; j < kGate; ++j)
             if (j < p) {
                 nloc = max(nloc, lc[j]);
-                lost |= (__ldg(&req[rb + nr + c0 + j]).w & TP_REQ_LOST) != 0;
+                lost |= (lostmask >> j) & 1u;
             }
         n_adm += p;
         if (p < cn) {

@@ -123,13 +123,11 @@ __device__ __forceinline__ int64_t units_of(const K2Params& p, int i, int G) {
 // compaction of the run heads.  Cell mode also claims each run's cell (rank_tp, rank_B,
 // rank_KV) in a dense table and appends first-seen cells to the cell list.
 constexpr int kRunsThreads = 256;
-constexpr int kRunsTabCap = 8192;     // rank-table entries per feature staged in shared memory
 
 __global__ void __launch_bounds__(kRunsThreads)
 k2_runs(const __grid_constant__ K2Params p) {
     extern __shared__ uint32_t skey[];               // [H + 1]: key of iteration m at skey[m]
-    __shared__ uint16_t stB[kRunsTabCap], stKV[kRunsTabCap];
-    __shared__ int swarp[kRunsThreads / 32];
+    __shared__ int swarp[kRunsThreads / 32], swarp_ex[kRunsThreads / 32 + 1];
     const int i = blockIdx.x, tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int n = (p.status[i] & kSkip) ? 0 : p.n[i];
     if (n == 0) {
@@ -137,13 +135,10 @@ k2_runs(const __grid_constant__ K2Params p) {
         return;
     }
     const int nB = p.cut_off[2] - p.cut_off[1], nKV = p.cut_off[3] - p.cut_off[2];
-    // rank tables (exact for integer features): shared-memory copies of at most kRunsTabCap
-    // entries, the rest of each table from global memory, a binary search beyond it
+    // rank tables (exact for integer features, L1-resident), a binary search beyond them
     const int lB = p.rtab_len[0], lKV = p.rtab_len[1];
-    const int sB = min(lB, kRunsTabCap), sKV = min(lKV, kRunsTabCap);
-    for (int j = tid; j < sB; j += kRunsThreads) stB[j] = p.rtab[p.rtab_off[0] + j];
-    for (int j = tid; j < sKV; j += kRunsThreads) stKV[j] = p.rtab[p.rtab_off[1] + j];
-    __syncthreads();
+    const uint16_t* tB = p.rtab + p.rtab_off[0];
+    const uint16_t* tKV = p.rtab + p.rtab_off[1];
     const bool cells = p.cell_tab != nullptr;
     uint32_t cell_base = 0;
     if (cells) {
@@ -153,10 +148,8 @@ k2_runs(const __grid_constant__ K2Params p) {
     const size_t row = (size_t)i * p.H;
     for (int m = 1 + tid; m <= n; m += kRunsThreads) {
         const int b = p.B[row + m - 1], kv = p.KV[row + m - 1];
-        const uint32_t rb = b < sB ? stB[b] : b < lB ? p.rtab[p.rtab_off[0] + b]
-                                                     : rank_of(p.cuts + p.cut_off[1], nB, (float)b);
-        const uint32_t rk = kv < sKV ? stKV[kv] : kv < lKV ? p.rtab[p.rtab_off[1] + kv]
-                                                           : rank_of(p.cuts + p.cut_off[2], nKV, (float)kv);
+        const uint32_t rb = b < lB ? __ldg(tB + b) : rank_of(p.cuts + p.cut_off[1], nB, (float)b);
+        const uint32_t rk = kv < lKV ? __ldg(tKV + kv) : rank_of(p.cuts + p.cut_off[2], nKV, (float)kv);
         skey[m] = cells ? cell_base + rb * (uint32_t)(nKV + 1) + rk : (rb | (rk << 16));
     }
     __syncthreads();
@@ -167,8 +160,19 @@ k2_runs(const __grid_constant__ K2Params p) {
         const unsigned mask = __ballot_sync(0xffffffffu, head);
         if (lane == 0) swarp[warp] = __popc(mask);
         __syncthreads();
-        int before = base;
-        for (int w = 0; w < warp; ++w) before += swarp[w];
+        if (tid < 32) {      // exclusive scan of the 8 warp counts (one warp)
+            const int c = lane < kRunsThreads / 32 ? swarp[lane] : 0;
+            int x = c;
+#pragma unroll
+            for (int o = 1; o < 8; o <<= 1) {
+                const int y = __shfl_up_sync(0xffffffffu, x, o);
+                if (lane >= o) x += y;
+            }
+            if (lane < kRunsThreads / 32) swarp_ex[lane] = x - c;
+            if (lane == kRunsThreads / 32 - 1) swarp_ex[kRunsThreads / 32] = x;
+        }
+        __syncthreads();
+        const int before = base + swarp_ex[warp];
         if (head) {
             const int pos = before + __popc(mask & ((1u << lane) - 1u));
             const uint32_t key = skey[m];
@@ -182,7 +186,7 @@ k2_runs(const __grid_constant__ K2Params p) {
                 p.cell_tab[key] = idx;
             }
         }
-        for (int w = 0; w < kRunsThreads / 32; ++w) base += swarp[w];
+        base += swarp_ex[kRunsThreads / 32];
         __syncthreads();
     }
     if (tid == 0) p.run_h[i] = base;

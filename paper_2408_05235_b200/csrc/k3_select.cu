@@ -156,7 +156,7 @@ k3_select_runs(const tp_inst* __restrict__ inst, const int4* __restrict__ req, c
     extern __shared__ long long sm[];
     __shared__ int s_pass[kMaxF];
     __shared__ int s_best;
-    __shared__ int swarp[kWarps];
+    __shared__ int swarp[kWarps], swarp_ex[kWarps + 1];
     const int i = blockIdx.x, tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const uint32_t st = status[i];
     if (st & kSkip) {
@@ -193,14 +193,25 @@ k3_select_runs(const tp_inst* __restrict__ inst, const int4* __restrict__ req, c
         const unsigned mask = __ballot_sync(0xffffffffu, has);
         if (lane == 0) swarp[warp] = __popc(mask);
         __syncthreads();
-        int before = ne;
-        for (int w = 0; w < warp; ++w) before += swarp[w];
+        if (tid < 32) {      // exclusive scan of the warp counts (one warp)
+            const int c = lane < kWarps ? swarp[lane] : 0;
+            int x = c;
+#pragma unroll
+            for (int o = 1; o < kWarps; o <<= 1) {
+                const int y = __shfl_up_sync(0xffffffffu, x, o);
+                if (lane >= o) x += y;
+            }
+            if (lane < kWarps) swarp_ex[lane] = x - c;
+            if (lane == kWarps - 1) swarp_ex[kWarps] = x;
+        }
+        __syncthreads();
+        const int before = ne + swarp_ex[warp];
         if (has) {
             const int pos = before + __popc(mask & ((1u << lane) - 1u));
             e_l[pos] = m;
             e_d[pos] = dmin[m];
         }
-        for (int w = 0; w < kWarps; ++w) ne += swarp[w];
+        ne += swarp_ex[kWarps];
         __syncthreads();
     }
 

@@ -22,6 +22,7 @@ constexpr int kRankTabMax = 1 << 16;       // rank table entries per integer fea
 // t = mulhi(m, n).  Used by K1 for the per-instance block size N.
 struct FastDiv {
     uint32_t m, s1, s2;
+    FastDiv() = default;
     __host__ __device__ explicit FastDiv(uint32_t d) {
         uint32_t l = 0;
         while (l < 32 && (1ull << l) < d) ++l;
@@ -111,6 +112,13 @@ int launch_select(const tp_inst* inst, int32_t n_inst, const tp_req* req, int32_
                   const int32_t* n, const int32_t* n_adm, const float* ips, int32_t H, int32_t F,
                   int64_t tbt_ticks, int32_t* level, uint32_t* status, int64_t* tr, const K2Params* ws,
                   cudaStream_t s);
+
+int launch_replay_advance(const Model& m, tp_inst* inst, int32_t n_inst, const tp_req* req, const double* t_dead,
+                          tp_req* req_out, double* t_dead_out, int32_t cap, int32_t H, const int32_t* B,
+                          const int32_t* KV, const int32_t* n, const int32_t* n_adm, const uint32_t* status,
+                          const int32_t* level, const float* freq, int32_t F, const double* arr_t,
+                          const tp_req* arr_req, const double* arr_dead, const int64_t* arr_off, int64_t* arr_next,
+                          unsigned long long* stats, cudaStream_t s);
 
 }  // namespace tp
 

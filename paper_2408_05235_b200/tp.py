@@ -22,7 +22,7 @@ ST_QUEUE_BLOCKED, ST_IPS_CLAMPED, ST_BAD_INPUT = 16, 32, 64
 # every symbol include/tp.h declares
 EXPORTS = ["tp_gbdt_load", "tp_gbdt_free", "tp_gbdt_get_info", "tp_project", "tp_predict_ips",
            "tp_predict_ips_workspace_size", "tp_predict_ips_runs", "tp_runs_total", "tp_cells_total", "tp_select_freq", "tp_select_freq_ws", "tp_ctx_create", "tp_ctx_free",
-           "tp_decide", "tp_decide_host", "tp_ctx_set_k2_mode", "tp_ctx_buffers", "tp_strerror", "tp_abi_version"]
+           "tp_decide", "tp_decide_host", "tp_replay_advance", "tp_ctx_set_k2_mode", "tp_ctx_buffers", "tp_strerror", "tp_abi_version"]
 K2_DIRECT, K2_RUNS = 0, 1
 
 if not os.path.exists(LIB_PATH):
@@ -50,6 +50,7 @@ _L.tp_runs_total.argtypes = [_vp, _i32, _i32, ctypes.POINTER(_i64)]
 _L.tp_cells_total.argtypes = [_vp, _vp, _i32, _i32, _i32, ctypes.POINTER(_i64)]
 _L.tp_select_freq.argtypes = [_vp, _i32, _vp, _i32, _vp, _vp, _vp, _vp, _i32, _i32, _f32, _vp, _vp, _vp, _vp]
 _L.tp_select_freq_ws.argtypes = [_vp, _vp, _vp, _i32, _vp, _i32, _vp, _vp, _vp, _i32, _i32, _f32, _vp, _vp, _vp, _vp]
+_L.tp_replay_advance.argtypes = [_vp, _vp, _i32, _vp, _vp, _vp, _vp, _i32, _i32] + [_vp] * 6 + [_vp, _i32] + [_vp] * 7
 _L.tp_ctx_create.argtypes = [ctypes.c_int, _vp, _i32, _i32, _i32, _i32, ctypes.POINTER(_vp)]
 _L.tp_ctx_free.argtypes = [_vp]
 _L.tp_decide.argtypes = [_vp, _vp, _vp, _i32, _vp, _i32, _vp, _vp, _i32, _f32, _vp, _vp, _vp]
@@ -196,6 +197,15 @@ def tp_select_freq_ws(model: Gbdt, workspace, inst, n_inst, req, n_req, t_dead, 
     _check(_L.tp_select_freq_ws(model.handle, _dp(workspace), _dp(inst), int(n_inst), _dp(req), int(n_req),
                                 _dp(t_dead), _dp(n), _dp(n_adm), int(H), int(F), float(np.float32(tbt_slo)),
                                 _dp(level), _dp(status), _dp(tr_ticks), _stream(stream)), "tp_select_freq_ws")
+
+
+def tp_replay_advance(model: Gbdt, inst, n_inst, req, t_dead, req_out, t_dead_out, slot_cap, H, B, KV, n, n_adm,
+                      status, level, freq, arr_t, arr_req, arr_dead, arr_off, arr_next, stats, stream=None):
+    f, F = _freq(freq)
+    _check(_L.tp_replay_advance(model.handle, _dp(inst), int(n_inst), _dp(req), _dp(t_dead), _dp(req_out),
+                                _dp(t_dead_out), int(slot_cap), int(H), _dp(B), _dp(KV), _dp(n), _dp(n_adm),
+                                _dp(status), _dp(level), f.ctypes.data, F, _dp(arr_t), _dp(arr_req), _dp(arr_dead),
+                                _dp(arr_off), _dp(arr_next), _dp(stats), _stream(stream)), "tp_replay_advance")
 
 
 class Ctx:
