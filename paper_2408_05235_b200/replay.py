@@ -1,0 +1,79 @@
+"""Trace replay driver (BASELINE configs[3]): every round decides ALL instances
+(tp_decide: K1 -> K2 -> K3 on the GPU) and advances every instance by one engine iteration at its
+chosen frequency (tp_replay_advance, on the GPU).  The state never leaves the device; torch only
+provides the buffers.
+"""
+from __future__ import annotations
+
+import numpy as np
+import torch
+
+from . import tp
+from . import workload as W
+
+
+def _dev(a, dev, dtype=None):
+    a = np.ascontiguousarray(a)
+    if a.dtype.fields is not None:
+        return torch.from_numpy(a.view(np.uint8).reshape(-1)).to(dev)
+    return torch.from_numpy(a if dtype is None else a.astype(dtype)).to(dev)
+
+
+class Replay:
+    STATS = ("completed", "met_deadline", "dropped_arrivals", "engine_iterations", "admissions")
+
+    def __init__(self, data: dict, model: tp.Gbdt, device="cuda:0", k2_mode=tp.K2_RUNS):
+        dev = torch.device(device)
+        self.dev, self.model = dev, model
+        self.I = len(data["inst"])
+        self.cap = int(data["slot_cap"])
+        self.H = int(data["H"])
+        self.freq = np.asarray(data["freq"], np.float32)
+        self.F = len(self.freq)
+        self.tbt = np.float32(data["tbt_slo"])
+        self.inst = _dev(data["inst"], dev)
+        self.req = [_dev(data["req"], dev), torch.empty_like(_dev(data["req"], dev))]
+        self.t_dead = [_dev(data["t_dead"], dev), torch.empty_like(_dev(data["t_dead"], dev))]
+        self.arr_t = _dev(data["arr_t"], dev, np.float64)
+        self.arr_req = _dev(data["arr_req"], dev)
+        self.arr_dead = _dev(data["arr_dead"], dev, np.float64)
+        self.arr_off = _dev(data["arr_off"], dev, np.int64)
+        self.arr_next = self.arr_off[:-1].clone()
+        self.stats = torch.zeros(5, dtype=torch.int64, device=dev)
+        self.level = torch.empty(self.I, dtype=torch.int32, device=dev)
+        self.status = torch.empty(self.I, dtype=torch.int32, device=dev)
+        self.ctx = tp.Ctx(dev.index or 0, self.I, self.I * self.cap, self.H, self.F, model)
+        self.ctx.set_k2_mode(k2_mode)
+        self.B, self.KV, self.n, self.n_adm, _ = self.ctx.buffers()
+        self.cur = 0
+        self.rounds = 0
+
+    def decide(self, stream=None):
+        self.ctx.decide(self.model, self.inst, self.I, self.req[self.cur], self.I * self.cap, self.t_dead[self.cur],
+                        self.freq, self.tbt, self.level, self.status, stream)
+
+    def advance(self, stream=None):
+        c, o = self.cur, 1 - self.cur
+        tp.tp_replay_advance(self.model, self.inst, self.I, self.req[c], self.t_dead[c], self.req[o], self.t_dead[o],
+                             self.cap, self.H, self.B, self.KV, self.n, self.n_adm, self.status, self.level, self.freq,
+                             self.arr_t, self.arr_req, self.arr_dead, self.arr_off, self.arr_next, self.stats, stream)
+        self.cur = o
+        self.rounds += 1
+
+    def round(self, stream=None):
+        self.decide(stream)
+        self.advance(stream)
+
+    def state(self):
+        """Host copies of the current state (synchronises)."""
+        inst = self.inst.cpu().numpy().view(W.INST_DTYPE).copy()
+        req = self.req[self.cur].cpu().numpy().view(W.REQ_DTYPE).copy()
+        return inst, req, self.t_dead[self.cur].cpu().numpy().copy(), self.arr_next.cpu().numpy().copy()
+
+    def finished(self) -> bool:
+        inst = self.inst.cpu().numpy().view(W.INST_DTYPE)
+        return bool((inst["n_run"] + inst["n_queue"]).sum() == 0 and
+                    torch.equal(self.arr_next, self.arr_off[1:]))
+
+    def stats_dict(self):
+        return dict(zip(self.STATS, (int(x) for x in self.stats.cpu().numpy())))

@@ -79,6 +79,8 @@ def _dp(t):
     """Device pointer of a torch tensor (or None)."""
     if t is None:
         return None
+    if isinstance(t, int):       # a raw device pointer (e.g. from Ctx.buffers())
+        return t
     if not t.is_cuda:
         raise ValueError("expected a CUDA tensor")
     if not t.is_contiguous():

@@ -295,3 +295,74 @@ def config_inputs(cfg: Config, i0: int = 0, i1: int | None = None):
     inst, req, t_dead = gen_instances(cfg, i0, i1)
     return dict(inst=inst, req=req, t_dead=t_dead, H=cfg.H,
                 freq=freq_levels(cfg.F, cfg.f_lo, cfg.f_hi), tbt_slo=np.float32(cfg.tbt_slo))
+
+
+# ----------------------------------------------------------------------------------------------
+# trace replay (BASELINE configs[3]: 1M requests across 4,096 instance states, re-decided every
+# iteration).  Inputs only: an initial state in fixed request slots and an arrival stream.
+# ----------------------------------------------------------------------------------------------
+
+# E2E SLO per engine size (Table II: p99 at max load, seconds)
+E2E_SLO = {1: 37.7, 2: 30.2, 4: 31.3, 8: 44.0}
+# relative request rate per 4-minute bin of the 60-minute Azure trace (medians 5-8
+# RPS, peak ~16 near the midpoint, never idle)
+RPS_PROFILE = np.array([5, 6, 6, 7, 8, 9, 11, 16, 12, 9, 8, 7, 6, 6, 5], dtype=np.float64)
+
+
+@dataclasses.dataclass(frozen=True)
+class ReplayConfig:
+    n_inst: int = 4096
+    n_requests: int = 1_000_000
+    span_s: float = 25.0      # the 60-minute profile time-scaled to this span
+    slot_cap: int = 512       # request slots per instance (running + queued)
+    base: Config = CONFIGS["C4"]
+    seed: int = 1004
+
+
+def gen_replay(rc: ReplayConfig):
+    """-> dict(inst, req[I*cap], t_dead[I*cap], arr_t, arr_req, arr_dead, arr_off[I+1], freq, H, ...).
+
+    Initial instance states come from the configs[3] generator (clipped to the slots); arrivals
+    are drawn over the rate profile, sorted, dealt round-robin to instances; each carries its
+    prompt length, its (exactly predicted) generation length and deadline = arrival + E2E SLO of
+    its engine size."""
+    cfg = dataclasses.replace(rc.base, n_inst=rc.n_inst)
+    inst0, req0, dead0 = gen_instances(cfg)
+    I, cap = rc.n_inst, rc.slot_cap
+    inst = inst0.copy()
+    req = np.zeros(I * cap, REQ_DTYPE)
+    dead = np.zeros(I * cap, np.float64)
+    for i in range(I):
+        b = int(inst0[i]["req_begin"])
+        nr, nq = int(inst0[i]["n_run"]), int(inst0[i]["n_queue"])
+        nr2 = min(nr, cap)
+        nq2 = min(nq, cap - nr2)
+        req[i * cap:i * cap + nr2] = req0[b:b + nr2]
+        dead[i * cap:i * cap + nr2] = dead0[b:b + nr2]
+        req[i * cap + nr2:i * cap + nr2 + nq2] = req0[b + nr:b + nr + nq2]
+        dead[i * cap + nr2:i * cap + nr2 + nq2] = dead0[b + nr:b + nr + nq2]
+        inst[i]["req_begin"] = i * cap
+        inst[i]["n_run"], inst[i]["n_queue"] = nr2, nq2
+    t0 = float(inst["t_cur"].max())
+    for i in range(I):                       # one common clock; deadlines keep their slack
+        dead[i * cap:(i + 1) * cap] += t0 - float(inst[i]["t_cur"])
+    inst["t_cur"] = t0
+    rng = np.random.default_rng([rc.seed, 99])
+    n = rc.n_requests
+    nb = len(RPS_PROFILE)
+    bins = rng.choice(nb, size=n, p=RPS_PROFILE / RPS_PROFILE.sum())
+    t = t0 + (bins + rng.random(n)) * (rc.span_s / nb)
+    t.sort()
+    owner = np.arange(n) % I                 # round-robin dealing
+    order = np.lexsort((t, owner))           # by instance, then time
+    t, owner = t[order], owner[order]
+    H = cfg.H
+    r = _lognormal_int(rng, 250.0, 0.5, 10, min(700, H), n)
+    q = _lognormal_int(rng, 600.0, 0.9, 1, 4000, n)
+    arr_req = np.zeros(n, REQ_DTYPE)
+    arr_req["q"], arr_req["r"] = q, r
+    slo = np.vectorize(E2E_SLO.get)(inst["tp"][owner]).astype(np.float64)
+    arr_off = np.concatenate([[0], np.cumsum(np.bincount(owner, minlength=I))]).astype(np.int64)
+    return dict(inst=inst, req=req, t_dead=dead, arr_t=t, arr_req=arr_req, arr_dead=t + slo, arr_off=arr_off,
+                freq=freq_levels(cfg.F, cfg.f_lo, cfg.f_hi), tbt_slo=np.float32(cfg.tbt_slo), H=H, slot_cap=cap,
+                t0=t0)

@@ -212,3 +212,65 @@ def replay_completion(box: BoxModel, inst, reqs, n_sched: int, freq_u: float, N:
                     s["blocks"] += 1
                 s["tokens"] += 1
     return done
+
+
+def replay_advance(inst, req, t_dead, arr_next, data, dec, oracle_model, freq, cap):
+    """One engine iteration per instance (the semantics include/tp.h states for tp_replay_advance),
+    written independently of replay.cu.  dec: oracle decision dict for the same state."""
+    inst = inst.copy()
+    req_out = np.zeros_like(req)
+    dead_out = np.zeros_like(t_dead)
+    arr_next = arr_next.copy()
+    stats = np.zeros(5, np.int64)
+    for i in range(len(inst)):
+        b = i * cap
+        nr, nq = int(inst[i]["n_run"]), int(inst[i]["n_queue"])
+        if dec["status"][i] & ST_BAD_INPUT:
+            req_out[b:b + nr + nq] = req[b:b + nr + nq]
+            dead_out[b:b + nr + nq] = t_dead[b:b + nr + nq]
+            continue
+        n, nadm, u = int(dec["n"][i]), int(dec["n_adm"][i]), int(dec["level"][i])
+        t_cur = float(inst[i]["t_cur"])
+        j0, j1 = int(arr_next[i]), int(data["arr_off"][i + 1])
+        if n > 0:
+            raw = oracle_model.predict_raw(inst[i]["tp"], dec["B"][i, 0], dec["KV"][i, 0], freq[u])
+            ips = np.float32(2.0 ** -4) if np.isnan(raw) else np.clip(raw, np.float32(2.0 ** -4), np.float32(2.0 ** 17))
+            t_new = t_cur + float(np.float32(1.0) / np.float32(ips))
+            it = 1
+        else:
+            t_new = t_cur
+            if j0 < j1 and data["arr_t"][j0] > t_new:
+                t_new = float(data["arr_t"][j0])
+            it = 0
+        out = []
+        for e in range(nr + nadm if it else 0):
+            r = req[b + e].copy()
+            r["a"] += 1
+            if r["r"] - r["a"] == 0:
+                stats[0] += 1
+                stats[1] += t_new < t_dead[b + e]
+            else:
+                out.append((r, t_dead[b + e]))
+        nrun = len(out)
+        q0 = nr + nadm if it else nr
+        for e in range(q0, nr + nq):
+            out.append((req[b + e], t_dead[b + e]))
+        arrived = 0
+        while j0 + arrived < j1 and data["arr_t"][j0 + arrived] <= t_new:
+            arrived += 1
+        take = min(arrived, max(cap - len(out), 0))
+        for k in range(take):
+            r = data["arr_req"][j0 + k].copy()
+            r["a"] = 0
+            out.append((r, data["arr_dead"][j0 + k]))
+        for k, (r, d) in enumerate(out):
+            req_out[b + k] = r
+            dead_out[b + k] = d
+        stats[2] += arrived - take
+        stats[3] += it
+        stats[4] += nadm if it else 0
+        inst[i]["n_run"], inst[i]["n_queue"] = nrun, len(out) - nrun
+        inst[i]["k"] += it
+        inst[i]["t_cur"] = t_new
+        arr_next[i] = j0 + arrived
+    return inst, req_out, dead_out, arr_next, stats
