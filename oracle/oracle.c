@@ -154,7 +154,39 @@ typedef struct {
     uint32_t* status;
     float* ips;
     int64_t* tr;
+    /* admission = 0: check 1 + batch cap gate (reading A-2); 1: the paper's full admission control
+     * (checks 1-3 at f_max, "lost" marking; reading A-23) */
+    int admission;
+    uint32_t* adm_lost;   /* out (admission = 1): bit c = queued candidate c admitted as lost */
 } o_job;
+
+/* T_R at level u over m = 1..n for the curves (Bv, KVv): O6 + O7.  Returns 1 if a model
+ * output was clamped. */
+static int level_times(const o_job* J, const o_inst* in, const int64_t* Bv, const int64_t* KVv, int32_t n,
+                       int32_t u, float* tcol, int64_t* trv, float* ips_out, int64_t* tr_out) {
+    int clamped = 0;
+    for (int32_t m = 1; m <= n; ++m) {
+        float x[4] = {(float)in->tp, (float)Bv[m], (float)KVv[m], J->freq[u]};
+        float acc = oracle_predict_raw(J->m, x);
+        float ips = acc;
+        if (isnan(acc)) ips = 0x1p-4f;                               /* reading A-8 */
+        else if (acc < 0x1p-4f) ips = 0x1p-4f;
+        else if (acc > 0x1p17f) ips = 0x1p17f;
+        if (isnan(acc) || ips != acc) clamped = 1;
+        if (ips_out) ips_out[m - 1] = ips;
+        tcol[m] = 1.0f / ips;
+    }
+    int64_t acc_ticks = 0;
+    for (int32_t m = 1; m <= n; ++m) {
+        double scaled = (double)tcol[m] * 0x1p40;
+        int64_t ticks = (int64_t)scaled;
+        if ((double)ticks != scaled) abort();   /* cannot happen for T' in [2^-17, 16] */
+        acc_ticks += ticks;
+        trv[m] = acc_ticks;
+        if (tr_out) tr_out[m - 1] = acc_ticks;
+    }
+    return clamped;
+}
 
 static void decide_one(const o_job* J, int64_t i, int64_t* Bv, int64_t* KVv, float* tcol, int64_t* trv) {
     const o_inst* in = &J->inst[i];
@@ -194,16 +226,53 @@ static void decide_one(const o_job* J, int64_t i, int64_t* Bv, int64_t* KVv, flo
     for (int32_t m = 1; m <= H; ++m) if (KVv[m] > in->kv_cap) st |= O_KV_OVER;
 
     /* ---- O4 FIFO gate: check 1 + batch cap, one at a time, FIFO head-of-line ---- */
+    uint32_t marked = 0;     /* admission = 1: candidates admitted as "lost" */
+    int32_t n_cur = 0;       /* horizon of the scheduled set so far */
+    for (int32_t e = 0; e < in->n_run; ++e) {
+        const o_req* q = &J->req[in->req_begin + e];
+        if (q->r - q->a > n_cur) n_cur = q->r - q->a;
+    }
     for (int32_t c = 0; c < in->n_queue; ++c) {
         const o_req* q = &J->req[in->req_begin + in->n_run + c];
+        if (J->admission && c >= 32) { st |= O_QUEUE_BLOCKED; break; }   /* reading A-23 */
         int ok = (Bv[1] + 1 <= in->max_batch);
         for (int32_t m = 1; ok && m <= H; ++m)      /* virtual append at s = k */
             if (KVv[m] + eq1_blocks(0, q->q, q->r, in->N, m) > in->kv_cap) ok = 0;
         if (!ok) { st |= O_QUEUE_BLOCKED; break; }
+        int as_lost = 0;
+        if (J->admission) {
+            /* checks 2-3 at the maximum frequency on the virtual state */
+            for (int32_t m = 1; m <= H; ++m) {      /* the candidate's curves added virtually */
+                int64_t b = eq1_blocks(0, q->q, q->r, in->N, m);
+                Bv[m] += b > 0; KVv[m] += b;
+            }
+            int32_t nv = q->r > n_cur ? q->r : n_cur;
+            level_times(J, in, Bv, KVv, nv, F - 1, tcol, trv, NULL, NULL);
+            int tbt_ok = (long double)trv[nv] <= (long double)nv * (long double)J->tbt * 0x1p40L;
+            int others_fail = 0, self_fail = 0;
+            for (int32_t e = 0; e <= in->n_run + c; ++e) {
+                const o_req* r = &J->req[in->req_begin + e];
+                int is_self = e == in->n_run + c;
+                int lost_e = (r->flags & O_LOST) || (e >= in->n_run && !is_self && ((marked >> (e - in->n_run)) & 1));
+                if (lost_e) continue;               /* lost requests are ignored */
+                int32_t l = r->r - r->a;
+                double slack = J->t_dead[in->req_begin + e] - in->t_cur;
+                int fails = !((long double)trv[l] < (long double)slack * 0x1p40L);
+                if (fails) { if (is_self) self_fail = 1; else others_fail = 1; }
+            }
+            for (int32_t m = 1; m <= H; ++m) {      /* roll back */
+                int64_t b = eq1_blocks(0, q->q, q->r, in->N, m);
+                Bv[m] -= b > 0; KVv[m] -= b;
+            }
+            if (!tbt_ok || others_fail) { st |= O_QUEUE_BLOCKED; break; }
+            as_lost = self_fail;                    /* schedulable, but its own deadline fails */
+        }
         for (int32_t m = 1; m <= H; ++m) {          /* commit */
             int64_t b = eq1_blocks(0, q->q, q->r, in->N, m);
             if (b > 0) { Bv[m] += 1; KVv[m] += b; }
         }
+        if (as_lost) marked |= 1u << c;
+        if (q->r > n_cur) n_cur = q->r;
         n_adm++;
     }
 
@@ -214,6 +283,7 @@ static void decide_one(const o_job* J, int64_t i, int64_t* Bv, int64_t* KVv, flo
         int32_t l = q->r - q->a;     /* completes at s_i + r^_i, i.e. l = s_i + r^_i - k */
         if (l > n) n = l;
         if (q->flags & O_LOST) lost = 1;
+        if (e >= in->n_run && ((marked >> (e - in->n_run)) & 1)) lost = 1;
     }
     if (n == 0) { st |= O_EMPTY; level = 0; goto write; }                 /* reading A-15 */
     if (lost) { st |= O_BYPASS_LOST; level = F - 1; goto write; }
@@ -221,29 +291,12 @@ static void decide_one(const o_job* J, int64_t i, int64_t* Bv, int64_t* KVv, flo
     /* ---- O6..O9 per frequency, ascending; lowest passing level (reading A-13) ---- */
     level = -1;
     for (int32_t u = 0; u < F; ++u) {
-        /* O6: T[m] = M(tp, B[m], KV[m], f_u); T'[m] = 1 / T[m] in fp32 (A-9) */
-        for (int32_t m = 1; m <= n; ++m) {
-            float x[4] = {(float)in->tp, (float)Bv[m], (float)KVv[m], J->freq[u]};
-            float acc = oracle_predict_raw(J->m, x);
-            float ips = acc;
-            if (isnan(acc)) ips = 0x1p-4f;                               /* reading A-8 */
-            else if (acc < 0x1p-4f) ips = 0x1p-4f;
-            else if (acc > 0x1p17f) ips = 0x1p17f;
-            if (isnan(acc) || ips != acc) st |= O_IPS_CLAMPED;
-            if (J->ips) J->ips[((int64_t)i * F + u) * H + (m - 1)] = ips;
-            tcol[m] = 1.0f / ips;
-        }
-        /* O7: Eq. 3 T_R[l] = sum_{m<=l} T'[m], exactly (A-10).  Each T' is an fp32 in
-         * [2^-17, 16], hence an integer multiple of 2^-40 s: the sum is kept in such ticks. */
-        int64_t acc_ticks = 0;
-        for (int32_t m = 1; m <= n; ++m) {
-            double scaled = (double)tcol[m] * 0x1p40;
-            int64_t ticks = (int64_t)scaled;
-            if ((double)ticks != scaled) abort();   /* cannot happen for T' in [2^-17, 16] */
-            acc_ticks += ticks;
-            trv[m] = acc_ticks;
-            if (J->tr) J->tr[((int64_t)i * F + u) * H + (m - 1)] = acc_ticks;
-        }
+        /* O6: T[m] = M(tp, B[m], KV[m], f_u); T'[m] = 1 / T[m] in fp32 (A-9).
+         * O7: Eq. 3 T_R[l] = sum_{m<=l} T'[m], exactly (A-10): each T' is an fp32 in
+         * [2^-17, 16], hence an integer multiple of 2^-40 s, so the sum is kept in such ticks. */
+        if (level_times(J, in, Bv, KVv, n, u, tcol, trv, J->ips ? J->ips + ((int64_t)i * F + u) * H : NULL,
+                        J->tr ? J->tr + ((int64_t)i * F + u) * H : NULL))
+            st |= O_IPS_CLAMPED;
         /* O8: TBT check 2: mean(T') = T_R[n] / n must not exceed the SLO (tie passes). */
         long double tr_n = (long double)trv[n];
         int pass = tr_n <= (long double)n * (long double)J->tbt * 0x1p40L;
@@ -268,6 +321,7 @@ write:
     if (J->n_adm) J->n_adm[i] = n_adm;
     if (J->level) J->level[i] = level;
     if (J->status) J->status[i] = st;
+    if (J->adm_lost) J->adm_lost[i] = marked;
 }
 
 typedef struct { const o_job* J; int64_t lo, hi, stride; } o_slice;
@@ -289,14 +343,15 @@ static void* worker(void* arg) {
 int oracle_decide(const o_model* m, const o_inst* inst, int64_t n_inst, const o_req* req, int64_t n_req,
                   const double* t_dead, int32_t H, const float* freq, int32_t F, float tbt,
                   int32_t* B, int32_t* KV, int32_t* n, int32_t* n_adm, float* ips, int64_t* tr,
-                  int32_t* level, uint32_t* status, int n_threads) {
+                  int32_t* level, uint32_t* status, int n_threads, int admission, uint32_t* adm_lost) {
     if (!m || H < 1 || H > 16384 || F < 1 || F > 32 || n_inst < 0) return -1;
     if (!(tbt >= 0x1p-17f && tbt <= 16.0f)) return -1;
     for (int32_t u = 0; u < F; ++u) {
         if (!isfinite(freq[u]) || freq[u] <= 0.0f) return -1;
         if (u > 0 && !(freq[u] > freq[u - 1])) return -1;
     }
-    o_job J = {m, inst, req, t_dead, n_req, H, F, freq, tbt, B, KV, n, n_adm, level, status, ips, tr};
+    o_job J = {m, inst, req, t_dead, n_req, H, F, freq, tbt, B, KV, n, n_adm, level, status, ips, tr,
+               admission, adm_lost};
     if (n_threads < 1) n_threads = 1;
     if (n_threads > 256) n_threads = 256;
     if (n_threads == 1) {

@@ -120,10 +120,22 @@ def valid_inputs(inst, reqs, H, n_req) -> bool:
     return foot < LIM
 
 
-def brute_decide(box: BoxModel, inst, reqs, deads, H, freq, tbt):
-    """Full decision for ONE instance with exact rationals; returns dict like the oracle's."""
+def _times(box, tpf, B, KV, n, f):
+    """Exact T_R (Fractions) at frequency f over m = 1..n, and whether a value was clamped."""
+    X = np.array([[tpf, B[m], KV[m], f] for m in range(n)], dtype=np.float32)
+    ips, clamped = box.ips(X)
+    TR, s = [], Fraction(0)
+    for v in ips:
+        s += Fraction(float(np.float32(1.0) / np.float32(v)))
+        TR.append(s)
+    return TR, bool(clamped.any())
+
+
+def brute_decide(box: BoxModel, inst, reqs, deads, H, freq, tbt, admission=0):
+    """Full decision for ONE instance with exact rationals; returns dict like the oracle's.
+    admission=1: the paper's admission control (checks 1-3 at f_max, lost marking)."""
     F = len(freq)
-    res = dict(B=[0] * H, KV=[0] * H, n=0, n_adm=0, status=0, level=0)
+    res = dict(B=[0] * H, KV=[0] * H, n=0, n_adm=0, status=0, level=0, adm_lost=0)
     if not valid_inputs(inst, reqs, H, 10 ** 12):
         res.update(status=ST_BAD_INPUT, level=F - 1)
         return res
@@ -138,38 +150,60 @@ def brute_decide(box: BoxModel, inst, reqs, deads, H, freq, tbt):
             B[m] += cur[m] > 0
     st = ST_KV_OVER if max(KV) > C else 0
     adm = 0
-    for rq in reqs[nr:nr + nq]:
-        cur = token_alloc_curve(0, int(rq["q"]), int(rq["r"]), N, H)
-        if B[0] + 1 <= mb and max(KV[m] + cur[m] for m in range(H)) <= C:
-            for m in range(H):
-                KV[m] += cur[m]
-                B[m] += cur[m] > 0
-            adm += 1
-        else:
+    marked = set()
+    tpf = float(inst["tp"])
+    for c, rq in enumerate(reqs[nr:nr + nq]):
+        if admission and c >= 32:
             st |= ST_QUEUE_BLOCKED
             break
+        cur = token_alloc_curve(0, int(rq["q"]), int(rq["r"]), N, H)
+        if not (B[0] + 1 <= mb and max(KV[m] + cur[m] for m in range(H)) <= C):
+            st |= ST_QUEUE_BLOCKED
+            break
+        lost_c = False
+        if admission:
+            B2 = [B[m] + (cur[m] > 0) for m in range(H)]
+            KV2 = [KV[m] + cur[m] for m in range(H)]
+            members = list(range(nr + c + 1))
+            nv = max(int(reqs[e]["r"]) - int(reqs[e]["a"]) for e in members)
+            TR, _ = _times(box, tpf, B2, KV2, nv, freq[F - 1])
+            ok2 = TR[-1] / nv <= Fraction(float(np.float32(tbt)))
+            others = self_ = False
+            for e in members:
+                if int(reqs[e]["flags"]) & LOST or (e >= nr and (e - nr) in marked and e != nr + c):
+                    continue
+                l = int(reqs[e]["r"]) - int(reqs[e]["a"])
+                slack = Fraction(float(np.float64(deads[e]) - np.float64(inst["t_cur"])))
+                if not TR[l - 1] < slack:
+                    if e == nr + c:
+                        self_ = True
+                    else:
+                        others = True
+            if not ok2 or others:
+                st |= ST_QUEUE_BLOCKED
+                break
+            lost_c = self_
+        for m in range(H):
+            KV[m] += cur[m]
+            B[m] += cur[m] > 0
+        if lost_c:
+            marked.add(c)
+            res["adm_lost"] |= 1 << c
+        adm += 1
     sched = list(range(nr + adm))
     n = max([int(reqs[e]["r"]) - int(reqs[e]["a"]) for e in sched], default=0)
     res.update(B=B, KV=KV, n=n, n_adm=adm)
     if n == 0:
         res.update(status=st | ST_EMPTY, level=0)
         return res
-    if any(int(reqs[e]["flags"]) & LOST for e in sched):
+    if any(int(reqs[e]["flags"]) & LOST for e in sched) or marked:
         res.update(status=st | ST_BYPASS_LOST, level=F - 1)
         return res
     level = None
-    tpf = float(inst["tp"])
     for u in range(F):
-        X = np.array([[tpf, B[m], KV[m], freq[u]] for m in range(n)], dtype=np.float32)
-        ips, clamped = box.ips(X)
-        if clamped.any():
+        TR, clamped = _times(box, tpf, B, KV, n, freq[u])
+        if clamped:
             st |= ST_IPS_CLAMPED
-        t = [Fraction(float(np.float32(1.0) / np.float32(v))) for v in ips]
-        TR = []
-        s = Fraction(0)
-        for x in t:
-            s += x
-            TR.append(s)
         ok = TR[-1] / n <= Fraction(float(np.float32(tbt)))
         for e in sched:
             l = int(reqs[e]["r"]) - int(reqs[e]["a"])
