@@ -250,6 +250,27 @@ int tp_decide_host(tp_ctx* c, const tp_gbdt* m, const tp_inst* h_inst, int32_t n
                    const float* freq_mhz, int32_t F, float tbt_slo, int32_t* h_level,
                    uint32_t* h_status, void* stream);
 
+/*
+ * Full admission control (PAPER §4.3.2) followed by the throttle.
+ * Queued requests are considered in FIFO order, one at a time, at most q_max per decision
+ * (reading A-23): a candidate is admitted iff, with it virtually appended, check 1 (KV
+ * capacity + batch cap) holds, check 2 (mean TBT at the maximum frequency)
+ * holds and check 3 (Eq. 4 at the maximum frequency) holds for every non-lost scheduled
+ * request; if check 3 fails only for the candidate itself it is admitted as "lost" and
+ * later checks ignore it; otherwise the queue stops.  Then levels are chosen as by tp_decide (a
+ * lost request present -> maximum frequency).
+ * tp_ctx_enable_admission(c, q_max) allocates the per-prefix scratch (q_max <= 32; the context must
+ * have been created for `m`, H <= 8192).
+ *   n_adm_out    [dev] optional int32 [n_inst]: queued requests admitted.
+ *   adm_lost_out [dev] optional uint32 [n_inst]: bit c = the c-th queued request admitted as lost
+ *                (the caller persists TP_REQ_LOST on it).
+ */
+int tp_ctx_enable_admission(tp_ctx* c, int32_t q_max);
+int tp_decide_admit(tp_ctx* c, const tp_gbdt* m, const tp_inst* inst, int32_t n_inst, const tp_req* req,
+                    int32_t n_req, const double* t_dead, const float* freq_mhz, int32_t F, float tbt_slo,
+                    int32_t* level, uint32_t* status, int32_t* n_adm_out, uint32_t* adm_lost_out,
+                    void* stream);
+
 /* Which K2 variant tp_decide / tp_decide_host use (default TP_K2_RUNS). */
 enum { TP_K2_DIRECT = 0, TP_K2_RUNS = 1 };
 int tp_ctx_set_k2_mode(tp_ctx* c, int mode);

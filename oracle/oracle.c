@@ -157,6 +157,7 @@ typedef struct {
     /* admission = 0: check 1 + batch cap gate (reading A-2); 1: the paper's full admission control
      * (checks 1-3 at f_max, "lost" marking; reading A-23) */
     int admission;
+    int adm_limit;        /* admission = 1: at most this many candidates (<= 32) per decision (A-23) */
     uint32_t* adm_lost;   /* out (admission = 1): bit c = queued candidate c admitted as lost */
 } o_job;
 
@@ -193,6 +194,7 @@ static void decide_one(const o_job* J, int64_t i, int64_t* Bv, int64_t* KVv, flo
     const int32_t H = J->H, F = J->F;
     uint32_t st = 0;
     int32_t n = 0, n_adm = 0, level = 0;
+    uint32_t marked = 0;     /* admission = 1: candidates admitted as "lost" (P:529) */
     for (int32_t m = 0; m <= H; ++m) Bv[m] = KVv[m] = 0;
 
     /* ---- O1 validate (reading A-3: every remaining length l in [1, H]) ---- */
@@ -226,7 +228,6 @@ static void decide_one(const o_job* J, int64_t i, int64_t* Bv, int64_t* KVv, flo
     for (int32_t m = 1; m <= H; ++m) if (KVv[m] > in->kv_cap) st |= O_KV_OVER;
 
     /* ---- O4 FIFO gate: check 1 + batch cap, one at a time, FIFO head-of-line ---- */
-    uint32_t marked = 0;     /* admission = 1: candidates admitted as "lost" (P:529) */
     int32_t n_cur = 0;       /* horizon of the scheduled set so far */
     for (int32_t e = 0; e < in->n_run; ++e) {
         const o_req* q = &J->req[in->req_begin + e];
@@ -234,7 +235,7 @@ static void decide_one(const o_job* J, int64_t i, int64_t* Bv, int64_t* KVv, flo
     }
     for (int32_t c = 0; c < in->n_queue; ++c) {
         const o_req* q = &J->req[in->req_begin + in->n_run + c];
-        if (J->admission && c >= 32) { st |= O_QUEUE_BLOCKED; break; }   /* reading A-23 */
+        if (J->admission && c >= J->adm_limit) { st |= O_QUEUE_BLOCKED; break; }   /* reading A-23 */
         int ok = (Bv[1] + 1 <= in->max_batch);
         for (int32_t m = 1; ok && m <= H; ++m)      /* virtual append at s = k */
             if (KVv[m] + eq1_blocks(0, q->q, q->r, in->N, m) > in->kv_cap) ok = 0;
@@ -343,15 +344,17 @@ static void* worker(void* arg) {
 int oracle_decide(const o_model* m, const o_inst* inst, int64_t n_inst, const o_req* req, int64_t n_req,
                   const double* t_dead, int32_t H, const float* freq, int32_t F, float tbt,
                   int32_t* B, int32_t* KV, int32_t* n, int32_t* n_adm, float* ips, int64_t* tr,
-                  int32_t* level, uint32_t* status, int n_threads, int admission, uint32_t* adm_lost) {
+                  int32_t* level, uint32_t* status, int n_threads, int admission, uint32_t* adm_lost,
+                  int adm_limit) {
     if (!m || H < 1 || H > 16384 || F < 1 || F > 32 || n_inst < 0) return -1;
     if (!(tbt >= 0x1p-17f && tbt <= 16.0f)) return -1;
     for (int32_t u = 0; u < F; ++u) {
         if (!isfinite(freq[u]) || freq[u] <= 0.0f) return -1;
         if (u > 0 && !(freq[u] > freq[u - 1])) return -1;
     }
+    if (adm_limit < 1 || adm_limit > 32) adm_limit = 32;
     o_job J = {m, inst, req, t_dead, n_req, H, F, freq, tbt, B, KV, n, n_adm, level, status, ips, tr,
-               admission, adm_lost};
+               admission, adm_limit, adm_lost};
     if (n_threads < 1) n_threads = 1;
     if (n_threads > 256) n_threads = 256;
     if (n_threads == 1) {

@@ -34,6 +34,14 @@ struct tp_ctx {
     size_t work_bytes;
     int k2_mode;
     const tp_gbdt* cells_model;   // the model the workspace was sized for (cell mode), or null
+    // admission control (tp_ctx_enable_admission): virtual prefix instances
+    int32_t qc;
+    tp_inst* vinst;
+    int32_t *vforce, *vB, *vKV, *vn, *vnadm, *adm_final;
+    uint32_t *vstatus, *lost;
+    uint2* vres;
+    void* vwork;
+    size_t vwork_bytes;
     tp_inst* inst;
     tp_req* req;
     double* t_dead;
@@ -89,6 +97,7 @@ int tp_predict_ips(const tp_gbdt* m, const tp_inst* inst, int32_t n_inst, const 
     p.n_inst = n_inst;
     p.H = H;
     p.F = F;
+    p.skip = TP_ST_BAD_INPUT | TP_ST_EMPTY | TP_ST_BYPASS_LOST;
     for (int u = 0; u < F; ++u) p.freq[u] = freq_mhz[u];
     return tp::launch_gbdt(p, false, S(stream));
 }
@@ -98,9 +107,20 @@ size_t tp_predict_ips_workspace_size(const tp_gbdt* m, int32_t n_inst, int32_t H
     return tp::runs_workspace_bytes(m ? tp::model_cells(m->m) : 0, n_inst, H, F);
 }
 
+static int predict_runs(const tp_gbdt* m, const tp_inst* inst, int32_t n_inst, const int32_t* B, const int32_t* KV,
+                        const int32_t* n, int32_t H, const float* freq_mhz, int32_t F, float* ips, uint32_t* status,
+                        void* workspace, size_t workspace_bytes, void* stream, uint32_t skip);
+
 int tp_predict_ips_runs(const tp_gbdt* m, const tp_inst* inst, int32_t n_inst, const int32_t* B, const int32_t* KV,
                         const int32_t* n, int32_t H, const float* freq_mhz, int32_t F, float* ips, uint32_t* status,
                         void* workspace, size_t workspace_bytes, void* stream) {
+    return predict_runs(m, inst, n_inst, B, KV, n, H, freq_mhz, F, ips, status, workspace, workspace_bytes, stream,
+                        TP_ST_BAD_INPUT | TP_ST_EMPTY | TP_ST_BYPASS_LOST);
+}
+
+static int predict_runs(const tp_gbdt* m, const tp_inst* inst, int32_t n_inst, const int32_t* B, const int32_t* KV,
+                        const int32_t* n, int32_t H, const float* freq_mhz, int32_t F, float* ips, uint32_t* status,
+                        void* workspace, size_t workspace_bytes, void* stream, uint32_t skip) {
     if (!m || n_inst < 0 || !H_ok(H) || !freq_ok(freq_mhz, F)) return TP_EINVAL;
     if (n_inst > 0 && (!inst || !B || !KV || !n || !status || !workspace)) return TP_EINVAL;
     const int64_t cells = tp::model_cells(m->m);
@@ -129,6 +149,7 @@ int tp_predict_ips_runs(const tp_gbdt* m, const tp_inst* inst, int32_t n_inst, c
     p.n_inst = n_inst;
     p.H = H;
     p.F = F;
+    p.skip = skip;
     for (int u = 0; u < F; ++u) p.freq[u] = freq_mhz[u];
     if (n_inst > 0) tp::runs_workspace_carve(workspace, use_cells ? cells : 0, n_inst, H, F, p);
     return tp::launch_gbdt(p, true, S(stream));
@@ -249,12 +270,77 @@ int tp_ctx_free(tp_ctx* c) {
     int prev = 0;
     cudaGetDevice(&prev);
     cudaSetDevice(c->device);
-    void* ptrs[] = {c->B, c->KV, c->n, c->n_adm, c->level, c->status, c->ips, c->work, c->inst, c->req, c->t_dead};
+    void* ptrs[] = {c->B,     c->KV,    c->n,      c->n_adm,     c->level, c->status, c->ips,   c->work,
+                    c->inst,  c->req,   c->t_dead, c->vinst,     c->vforce, c->vB,   c->vKV,   c->vn,
+                    c->vnadm, c->adm_final, c->vstatus, c->lost, c->vres,  c->vwork};
     for (void* p : ptrs)
         if (p) cudaFree(p);
     cudaSetDevice(prev);
     delete c;
     return TP_OK;
+}
+
+int tp_ctx_enable_admission(tp_ctx* c, int32_t q_max) {
+    if (!c || q_max < 1 || q_max > 32 || !c->cells_model || c->H > tp::kMaxHRunsSelect) return TP_EINVAL;
+    if (c->qc) return c->qc == q_max ? TP_OK : TP_EINVAL;
+    int prev = 0;
+    cudaGetDevice(&prev);
+    if (cudaSetDevice(c->device) != cudaSuccess) return TP_ECUDA;
+    const size_t I = (size_t)(c->n_inst_max > 0 ? c->n_inst_max : 1), V = I * q_max, H = c->H;
+    c->vwork_bytes = tp::runs_workspace_bytes(tp::model_cells(c->cells_model->m), (int32_t)V, c->H, 1);
+    const bool ok = cudaMalloc(&c->vinst, V * sizeof(tp_inst)) == cudaSuccess &&
+                    cudaMalloc(&c->vforce, V * 4) == cudaSuccess && cudaMalloc(&c->vB, V * H * 4) == cudaSuccess &&
+                    cudaMalloc(&c->vKV, V * H * 4) == cudaSuccess && cudaMalloc(&c->vn, V * 4) == cudaSuccess &&
+                    cudaMalloc(&c->vnadm, V * 4) == cudaSuccess && cudaMalloc(&c->vstatus, V * 4) == cudaSuccess &&
+                    cudaMalloc(&c->vres, V * sizeof(uint2)) == cudaSuccess &&
+                    cudaMalloc(&c->adm_final, I * 4) == cudaSuccess && cudaMalloc(&c->lost, I * 4) == cudaSuccess &&
+                    cudaMalloc(&c->vwork, c->vwork_bytes) == cudaSuccess;
+    cudaSetDevice(prev);
+    if (!ok) return TP_ENOMEM;
+    c->qc = q_max;
+    return TP_OK;
+}
+
+int tp_decide_admit(tp_ctx* c, const tp_gbdt* m, const tp_inst* inst, int32_t n_inst, const tp_req* req,
+                    int32_t n_req, const double* t_dead, const float* freq_mhz, int32_t F, float tbt_slo,
+                    int32_t* level, uint32_t* status, int32_t* n_adm_out, uint32_t* adm_lost_out, void* stream) {
+    if (!c || !m || !c->qc || m != c->cells_model || n_inst < 0 || n_inst > c->n_inst_max || F > c->F_max ||
+        !freq_ok(freq_mhz, F) || !tbt_ok(tbt_slo))
+        return TP_EINVAL;
+    if (n_inst > 0 && (!inst || !level || !status || (n_req > 0 && (!req || !t_dead)))) return TP_EINVAL;
+    if (n_inst == 0) return TP_OK;
+    cudaStream_t s = S(stream);
+    const int32_t V = n_inst * c->qc, H = c->H;
+    const int64_t tbt_ticks = (int64_t)((double)tbt_slo * 0x1p40);
+    // 1. check 1 + batch cap (K1 gate): the longest admissible prefix
+    int rc = tp::launch_project(inst, n_inst, req, n_req, H, c->B, c->KV, c->n, c->n_adm, status, s);
+    // 2. every prefix as a virtual instance, its candidates forced in
+    if (!rc) rc = tp::launch_admit_expand(inst, n_inst, c->qc, c->n_adm, status, c->vinst, c->vforce, s);
+    if (!rc) rc = tp::launch_project(c->vinst, V, req, n_req, H, c->vB, c->vKV, c->vn, c->vnadm, c->vstatus, s,
+                                     c->vforce, nullptr);
+    // 3. M at the maximum frequency on every prefix state (cell mode, LUT only)
+    // (a lost running request does not exempt the prefix from the checks: only BAD / EMPTY are skipped)
+    if (!rc) rc = predict_runs(m, c->vinst, V, c->vB, c->vKV, c->vn, H, freq_mhz + (F - 1), 1, nullptr, c->vstatus,
+                               c->vwork, c->vwork_bytes, stream, TP_ST_BAD_INPUT | TP_ST_EMPTY);
+    // 4. checks 2-3 per prefix, 5. FIFO resolution with lost marks
+    tp::K2Params w;
+    std::memset(&w, 0, sizeof(w));
+    tp::runs_workspace_carve(c->vwork, tp::model_cells(m->m), V, H, 1, w);
+    if (!rc) rc = tp::launch_admit_checks(c->vinst, V, req, t_dead, c->vn, c->vstatus, w, H, tbt_ticks, c->vres, s);
+    if (!rc) rc = tp::launch_admit_resolve(n_inst, c->qc, inst, status, c->n_adm, c->vres, c->adm_final, c->lost, s);
+    // 6. the throttle on the admitted state (lost marks applied -> bypass)
+    if (!rc) rc = tp::launch_project(inst, n_inst, req, n_req, H, c->B, c->KV, c->n, c->n_adm, status, s,
+                                     c->adm_final, c->lost);
+    if (!rc) rc = tp_predict_ips_runs(m, inst, n_inst, c->B, c->KV, c->n, H, freq_mhz, F, nullptr, status, c->work,
+                                      c->work_bytes, stream);
+    if (!rc) rc = tp_select_freq_ws(m, c->work, inst, n_inst, req, n_req, t_dead, c->n, c->n_adm, H, F, tbt_slo,
+                                    level, status, nullptr, stream);
+    if (!rc && n_adm_out && cudaMemcpyAsync(n_adm_out, c->n_adm, (size_t)n_inst * 4, cudaMemcpyDeviceToDevice, s))
+        rc = TP_ECUDA;
+    if (!rc && adm_lost_out &&
+        cudaMemcpyAsync(adm_lost_out, c->lost, (size_t)n_inst * 4, cudaMemcpyDeviceToDevice, s))
+        rc = TP_ECUDA;
+    return rc;
 }
 
 int tp_ctx_set_k2_mode(tp_ctx* c, int mode) {

@@ -46,7 +46,8 @@ __device__ __forceinline__ int block_max(int v, int* red) {
 __global__ void __launch_bounds__(kThreads)
 k1_project(const tp_inst* __restrict__ inst, const int4* __restrict__ req, int32_t n_req, int32_t H,
            int32_t* __restrict__ Bout, int32_t* __restrict__ KVout, int32_t* __restrict__ nout,
-           int32_t* __restrict__ nadm_out, uint32_t* __restrict__ status) {
+           int32_t* __restrict__ nadm_out, uint32_t* __restrict__ status, const int32_t* __restrict__ force_adm,
+           const uint32_t* __restrict__ lost_mask) {
     extern __shared__ int smem[];
     int* sB = smem;               // index m in [1, H + 1]
     int* sKV = smem + (H + 2);
@@ -167,8 +168,12 @@ k1_project(const tp_inst* __restrict__ inst, const int4* __restrict__ req, int32
     // candidate at a time, with one block reduction per batch instead of per candidate.
     int n_adm = 0;
     bool blocked = false;
-    for (int c0 = 0; c0 < nq && !blocked; c0 += kGate) {
-        const int cn = min(kGate, nq - c0);
+    // forced mode (admission control, tp_decide_admit): admit exactly force_adm[i] candidates (the
+    // SLO checks were made at f_max beforehand), with lost_mask[i] marking the "lost" ones
+    const int forced = force_adm ? min(max(force_adm[i], 0), nq) : -1;
+    const uint32_t lmask = lost_mask ? lost_mask[i] : 0u;
+    for (int c0 = 0; c0 < (forced >= 0 ? forced : nq) && !blocked; c0 += kGate) {
+        const int cn = min(kGate, (forced >= 0 ? forced : nq) - c0);
         int q[kGate], lc[kGate], mx[kGate];
         uint32_t lostmask = 0;
 #pragma unroll
@@ -180,7 +185,7 @@ k1_project(const tp_inst* __restrict__ inst, const int4* __restrict__ req, int32
                 const int4 r = __ldg(&req[rb + nr + c0 + j]);
                 q[j] = r.y;
                 lc[j] = r.z;
-                if (r.w & TP_REQ_LOST) lostmask |= 1u << j;
+                if ((r.w & TP_REQ_LOST) || (c0 + j < 32 && ((lmask >> (c0 + j)) & 1u))) lostmask |= 1u << j;
             }
         }
         // candidate j's Eq. 1 blocks over this thread's segment, incrementally: kv = ceil(t / N) with
@@ -223,7 +228,9 @@ k1_project(const tp_inst* __restrict__ inst, const int4* __restrict__ req, int32
 #pragma unroll
             for (int j = 0; j < kGate; ++j) s_gate[warp][j] = mx[j];
         __syncthreads();
-        if (tid == 0) {
+        if (tid == 0 && forced >= 0) {
+            s_admit = cn;
+        } else if (tid == 0) {
             int p = 0;
             while (p < cn) {
                 int M = 0;
@@ -274,6 +281,7 @@ k1_project(const tp_inst* __restrict__ inst, const int4* __restrict__ req, int32
         }
         __syncthreads();
     }
+    if (forced >= 0 && forced < nq) st |= TP_ST_QUEUE_BLOCKED;
     const int n = block_max(nloc, redi);
 
     if ((H & 3) == 0) {   // rows 16-byte aligned: 128-bit stores
@@ -302,7 +310,8 @@ k1_project(const tp_inst* __restrict__ inst, const int4* __restrict__ req, int32
 }  // namespace
 
 int launch_project(const tp_inst* inst, int32_t n_inst, const tp_req* req, int32_t n_req, int32_t H,
-                   int32_t* B, int32_t* KV, int32_t* n, int32_t* n_adm, uint32_t* status, cudaStream_t s) {
+                   int32_t* B, int32_t* KV, int32_t* n, int32_t* n_adm, uint32_t* status, cudaStream_t s,
+                   const int32_t* force_adm, const uint32_t* lost_mask) {
     if (n_inst == 0) return TP_OK;
     const size_t smem = (size_t)2 * (H + 2) * sizeof(int);
     int dev = 0;
@@ -315,7 +324,7 @@ int launch_project(const tp_inst* inst, int32_t n_inst, const tp_req* req, int32
         attr_done[dev] = true;
     }
     k1_project<<<n_inst, kThreads, smem, s>>>(inst, reinterpret_cast<const int4*>(req), n_req, H, B, KV, n,
-                                                n_adm, status);
+                                                n_adm, status, force_adm, lost_mask);
     return cudaPeekAtLastError() == cudaSuccess ? TP_OK : TP_ECUDA;
 }
 

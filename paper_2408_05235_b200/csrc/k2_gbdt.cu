@@ -111,7 +111,7 @@ enum Mode : int { kDirect = 0, kRuns = 1, kCells = 2 };
 // = one distinct cell x RU levels (n_cells * G in total), no instance structure.
 template <int MODE>
 __device__ __forceinline__ int64_t units_of(const K2Params& p, int i, int G) {
-    if (p.status[i] & kSkip) return 0;
+    if (p.status[i] & p.skip) return 0;
     return MODE == kRuns ? (int64_t)p.run_h[i] * G : (int64_t)((p.n[i] + 31) >> 5) * G;
 }
 
@@ -129,7 +129,7 @@ k2_runs(const __grid_constant__ K2Params p) {
     extern __shared__ uint32_t skey[];               // [H + 1]: key of iteration m at skey[m]
     __shared__ int swarp[kRunsThreads / 32], swarp_ex[kRunsThreads / 32 + 1];
     const int i = blockIdx.x, tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    const int n = (p.status[i] & kSkip) ? 0 : p.n[i];
+    const int n = (p.status[i] & p.skip) ? 0 : p.n[i];
     if (n == 0) {
         if (tid == 0) p.run_h[i] = 0;
         return;

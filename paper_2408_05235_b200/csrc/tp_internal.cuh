@@ -80,6 +80,7 @@ struct K2Params {
     uint32_t* status;
     float* ips;
     int32_t n_inst, H, F;
+    uint32_t skip;           // status bits of instances K2 does not evaluate
     float freq[kMaxF];
     const uint16_t* rtab;
     int32_t rtab_off[2], rtab_len[2];
@@ -106,7 +107,8 @@ void runs_workspace_carve(void* ws, int64_t n_cells, int32_t n_inst, int32_t H, 
 int64_t model_cells(const Model& m);
 
 int launch_project(const tp_inst* inst, int32_t n_inst, const tp_req* req, int32_t n_req, int32_t H,
-                   int32_t* B, int32_t* KV, int32_t* n, int32_t* n_adm, uint32_t* status, cudaStream_t s);
+                   int32_t* B, int32_t* KV, int32_t* n, int32_t* n_adm, uint32_t* status, cudaStream_t s,
+                   const int32_t* force_adm = nullptr, const uint32_t* lost_mask = nullptr);
 int launch_gbdt(const K2Params& p, bool runs, cudaStream_t s);
 int launch_select(const tp_inst* inst, int32_t n_inst, const tp_req* req, int32_t n_req, const double* t_dead,
                   const int32_t* n, const int32_t* n_adm, const float* ips, int32_t H, int32_t F,
@@ -119,6 +121,14 @@ int launch_replay_advance(const Model& m, tp_inst* inst, int32_t n_inst, const t
                           const int32_t* level, const float* freq, int32_t F, const double* arr_t,
                           const tp_req* arr_req, const double* arr_dead, const int64_t* arr_off, int64_t* arr_next,
                           unsigned long long* stats, cudaStream_t s);
+
+int launch_admit_expand(const tp_inst* inst, int32_t n_inst, int32_t qc, const int32_t* n_adm1,
+                        const uint32_t* status1, tp_inst* vinst, int32_t* vforce, cudaStream_t s);
+int launch_admit_checks(const tp_inst* vinst, int32_t n_v, const tp_req* req, const double* t_dead,
+                        const int32_t* vn, const uint32_t* vstatus, const K2Params& ws, int32_t H,
+                        int64_t tbt_ticks, uint2* vres, cudaStream_t s);
+int launch_admit_resolve(int32_t n_inst, int32_t qc, const tp_inst* inst, const uint32_t* status1,
+                         const int32_t* n_adm1, const uint2* vres, int32_t* n_adm, uint32_t* lost, cudaStream_t s);
 
 }  // namespace tp
 

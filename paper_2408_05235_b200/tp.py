@@ -22,7 +22,7 @@ ST_QUEUE_BLOCKED, ST_IPS_CLAMPED, ST_BAD_INPUT = 16, 32, 64
 # every symbol include/tp.h declares
 EXPORTS = ["tp_gbdt_load", "tp_gbdt_free", "tp_gbdt_get_info", "tp_project", "tp_predict_ips",
            "tp_predict_ips_workspace_size", "tp_predict_ips_runs", "tp_runs_total", "tp_cells_total", "tp_select_freq", "tp_select_freq_ws", "tp_ctx_create", "tp_ctx_free",
-           "tp_decide", "tp_decide_host", "tp_replay_advance", "tp_ctx_set_k2_mode", "tp_ctx_buffers", "tp_strerror", "tp_abi_version"]
+           "tp_decide", "tp_decide_host", "tp_replay_advance", "tp_ctx_enable_admission", "tp_decide_admit", "tp_ctx_set_k2_mode", "tp_ctx_buffers", "tp_strerror", "tp_abi_version"]
 K2_DIRECT, K2_RUNS = 0, 1
 
 if not os.path.exists(LIB_PATH):
@@ -51,6 +51,8 @@ _L.tp_cells_total.argtypes = [_vp, _vp, _i32, _i32, _i32, ctypes.POINTER(_i64)]
 _L.tp_select_freq.argtypes = [_vp, _i32, _vp, _i32, _vp, _vp, _vp, _vp, _i32, _i32, _f32, _vp, _vp, _vp, _vp]
 _L.tp_select_freq_ws.argtypes = [_vp, _vp, _vp, _i32, _vp, _i32, _vp, _vp, _vp, _i32, _i32, _f32, _vp, _vp, _vp, _vp]
 _L.tp_replay_advance.argtypes = [_vp, _vp, _i32, _vp, _vp, _vp, _vp, _i32, _i32] + [_vp] * 6 + [_vp, _i32] + [_vp] * 7
+_L.tp_ctx_enable_admission.argtypes = [_vp, _i32]
+_L.tp_decide_admit.argtypes = [_vp, _vp, _vp, _i32, _vp, _i32, _vp, _vp, _i32, _f32, _vp, _vp, _vp, _vp, _vp]
 _L.tp_ctx_create.argtypes = [ctypes.c_int, _vp, _i32, _i32, _i32, _i32, ctypes.POINTER(_vp)]
 _L.tp_ctx_free.argtypes = [_vp]
 _L.tp_decide.argtypes = [_vp, _vp, _vp, _i32, _vp, _i32, _vp, _vp, _i32, _f32, _vp, _vp, _vp]
@@ -231,6 +233,16 @@ class Ctx:
         _check(_L.tp_decide_host(self.handle, model.handle, _hp(inst), int(n_inst), _hp(req), int(n_req),
                                  _hp(t_dead), f.ctypes.data, F, float(np.float32(tbt_slo)), _hp(level), _hp(status),
                                  _stream(stream)), "tp_decide_host")
+
+    def enable_admission(self, q_max=32):
+        _check(_L.tp_ctx_enable_admission(self.handle, int(q_max)), "tp_ctx_enable_admission")
+
+    def decide_admit(self, model: Gbdt, inst, n_inst, req, n_req, t_dead, freq, tbt_slo, level, status,
+                     n_adm=None, adm_lost=None, stream=None):
+        f, F = _freq(freq)
+        _check(_L.tp_decide_admit(self.handle, model.handle, _dp(inst), int(n_inst), _dp(req), int(n_req),
+                                  _dp(t_dead), f.ctypes.data, F, float(np.float32(tbt_slo)), _dp(level), _dp(status),
+                                  _dp(n_adm), _dp(adm_lost), _stream(stream)), "tp_decide_admit")
 
     def set_k2_mode(self, mode):
         _check(_L.tp_ctx_set_k2_mode(self.handle, int(mode)), "tp_ctx_set_k2_mode")
