@@ -188,7 +188,7 @@ def bench_replay(args, cfg, rank, world, local, dist, dist_test):
     i0, i1 = shard.shard_range(rc.n_inst, rank, world)
     data = slice_replay(data, i0, i1)
     model = tp.Gbdt(W.write_blob(W.config_ensemble(cfg)), local)
-    rp = replay.Replay(data, model, dev)
+    rp = replay.Replay(data, model, dev, admission=args.admission)
     stream = torch.cuda.current_stream(dev)
     for _ in range(max(args.warmup, 3)):
         rp.round(stream)
@@ -226,6 +226,8 @@ def bench_replay(args, cfg, rank, world, local, dist, dist_test):
         "config": {"workload": DESCR["C4"], "name": "C4", "instances": I, "requests": rc.n_requests,
                    "span_s": rc.span_s, "trees": cfg.n_trees, "depth": cfg.depth, "F": cfg.F, "H": cfg.H,
                    "step": "decide all instances + advance all instances one iteration (GPU-resident replay)",
+                   "admission": (f"full admission control (checks 1-3 at f_max, lost marking), q_max={args.admission}"
+                                 if args.admission else "check 1 + batch cap gate"),
                    "l2": "not flushed: the replay state (~20 MB) is re-used every round by design"},
         "decisions_per_sec_decide_only": I * args.steps / (float(tot[1]) / 1e3),
         "per_round_ms": {"decide": dec_ms / args.steps, "advance": adv_ms / args.steps},
@@ -244,6 +246,8 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--e2e-steps", type=int, default=None)
+    ap.add_argument("--admission", type=int, default=0,
+                    help="C4 replay: run the paper's full admission control on up to N queued requests per instance")
     ap.add_argument("--k2", default="fused", choices=["fused", "cells", "runs", "direct"],
                     help="K2 variant: cell-memoised fused with K3 (default), cell-memoised with the ips grid, "
                          "run-compressed, or one evaluation per grid point")

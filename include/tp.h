@@ -294,7 +294,8 @@ int tp_ctx_buffers(tp_ctx* c, int32_t** B, int32_t** KV, int32_t** n, int32_t** 
  *   [dev] out (same slot layout; the caller swaps the buffers);  B, KV, n, n_adm, status, level
  *   [dev] the round's K1 / K3 outputs;  freq_mhz [host] the round's levels;  arr_next [dev] in/out
  *   next arrival per instance;  stats [dev] uint64[5] accumulators: completed, completed before
- *   their deadline (Eq. 4), dropped arrivals, engine iterations, admissions.
+ *   their deadline (Eq. 4), dropped arrivals, engine iterations, admissions;  adm_lost [dev]
+ *   optional (tp_decide_admit's output): admitted queued requests marked lost get TP_REQ_LOST.
  */
 int tp_replay_advance(const tp_gbdt* m, tp_inst* inst, int32_t n_inst, const tp_req* req,
                       const double* t_dead, tp_req* req_out, double* t_dead_out, int32_t slot_cap,
@@ -302,7 +303,7 @@ int tp_replay_advance(const tp_gbdt* m, tp_inst* inst, int32_t n_inst, const tp_
                       const int32_t* n_adm, const uint32_t* status, const int32_t* level,
                       const float* freq_mhz, int32_t F, const double* arr_t, const tp_req* arr_req,
                       const double* arr_dead, const int64_t* arr_off, int64_t* arr_next,
-                      uint64_t* stats, void* stream);
+                      uint64_t* stats, const uint32_t* adm_lost, void* stream);
 
 const char* tp_strerror(int code);
 int tp_abi_version(void);

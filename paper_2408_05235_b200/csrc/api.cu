@@ -216,14 +216,14 @@ int tp_replay_advance(const tp_gbdt* m, tp_inst* inst, int32_t n_inst, const tp_
                       const int32_t* KV, const int32_t* n, const int32_t* n_adm, const uint32_t* status,
                       const int32_t* level, const float* freq_mhz, int32_t F, const double* arr_t,
                       const tp_req* arr_req, const double* arr_dead, const int64_t* arr_off, int64_t* arr_next,
-                      uint64_t* stats, void* stream) {
+                      uint64_t* stats, const uint32_t* adm_lost, void* stream) {
     if (!m || n_inst < 0 || slot_cap < 1 || !H_ok(H) || !freq_ok(freq_mhz, F)) return TP_EINVAL;
     if (n_inst > 0 && (!inst || !req || !t_dead || !req_out || !t_dead_out || !B || !KV || !n || !n_adm || !status ||
                        !level || !arr_t || !arr_req || !arr_dead || !arr_off || !arr_next || !stats))
         return TP_EINVAL;
     return tp::launch_replay_advance(m->m, inst, n_inst, req, t_dead, req_out, t_dead_out, slot_cap, H, B, KV, n,
                                      n_adm, status, level, freq_mhz, F, arr_t, arr_req, arr_dead, arr_off, arr_next,
-                                     reinterpret_cast<unsigned long long*>(stats), S(stream));
+                                     reinterpret_cast<unsigned long long*>(stats), adm_lost, S(stream));
 }
 
 int tp_ctx_create(int device, const tp_gbdt* model, int32_t n_inst_max, int32_t n_req_max, int32_t H, int32_t F_max,

@@ -78,6 +78,7 @@ struct AdvParams {
     const int64_t* arr_off;
     int64_t* arr_next;
     unsigned long long* stats;  // [completed, met, dropped, iterations, admitted]
+    const uint32_t* adm_lost;   // optional: admitted queued requests marked lost (tp_decide_admit)
 };
 
 __global__ void __launch_bounds__(kThreads)
@@ -164,6 +165,8 @@ k_replay_advance(const __grid_constant__ AdvParams p) {
             if (e < n_sched) {
                 r = p.req[base + e];
                 dl = p.t_dead[base + e];
+                if (p.adm_lost && e >= nr && e - nr < 32 && ((p.adm_lost[i] >> (e - nr)) & 1u))
+                    r.flags |= TP_REQ_LOST;                 // scheduled as "lost": persisted
                 r.a += 1;                                   // one token generated this iteration
                 if (r.r - r.a == 0) {                       // completes at the end of this iteration
                     ++completed;
@@ -252,9 +255,10 @@ int launch_replay_advance(const Model& m, tp_inst* inst, int32_t n_inst, const t
                           const int32_t* KV, const int32_t* n, const int32_t* n_adm, const uint32_t* status,
                           const int32_t* level, const float* freq, int32_t F, const double* arr_t,
                           const tp_req* arr_req, const double* arr_dead, const int64_t* arr_off, int64_t* arr_next,
-                          unsigned long long* stats, cudaStream_t s) {
+                          unsigned long long* stats, const uint32_t* adm_lost, cudaStream_t s) {
     if (n_inst == 0) return TP_OK;
     AdvParams p{};
+    p.adm_lost = adm_lost;
     p.words = m.d_words;
     p.cuts = m.d_cuts;
     for (int f = 0; f < 5; ++f) p.cut_off[f] = m.cut_off[f];

@@ -120,7 +120,7 @@ int launch_replay_advance(const Model& m, tp_inst* inst, int32_t n_inst, const t
                           const int32_t* KV, const int32_t* n, const int32_t* n_adm, const uint32_t* status,
                           const int32_t* level, const float* freq, int32_t F, const double* arr_t,
                           const tp_req* arr_req, const double* arr_dead, const int64_t* arr_off, int64_t* arr_next,
-                          unsigned long long* stats, cudaStream_t s);
+                          unsigned long long* stats, const uint32_t* adm_lost, cudaStream_t s);
 
 int launch_admit_expand(const tp_inst* inst, int32_t n_inst, int32_t qc, const int32_t* n_adm1,
                         const uint32_t* status1, tp_inst* vinst, int32_t* vforce, cudaStream_t s);

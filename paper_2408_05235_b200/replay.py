@@ -22,7 +22,9 @@ def _dev(a, dev, dtype=None):
 class Replay:
     STATS = ("completed", "met_deadline", "dropped_arrivals", "engine_iterations", "admissions")
 
-    def __init__(self, data: dict, model: tp.Gbdt, device="cuda:0", k2_mode=tp.K2_RUNS):
+    def __init__(self, data: dict, model: tp.Gbdt, device="cuda:0", k2_mode=tp.K2_RUNS, admission: int = 0):
+        """admission = q_max > 0: each round runs the paper's full admission control (tp_decide_admit)
+        on at most q_max queued requests per instance before the throttle."""
         dev = torch.device(device)
         self.dev, self.model = dev, model
         self.I = len(data["inst"])
@@ -45,10 +47,20 @@ class Replay:
         self.ctx = tp.Ctx(dev.index or 0, self.I, self.I * self.cap, self.H, self.F, model)
         self.ctx.set_k2_mode(k2_mode)
         self.B, self.KV, self.n, self.n_adm, _ = self.ctx.buffers()
+        self.admission = int(admission)
+        self.adm_lost = None
+        if self.admission:
+            self.ctx.enable_admission(self.admission)
+            self.adm_lost = torch.zeros(self.I, dtype=torch.int32, device=dev)
         self.cur = 0
         self.rounds = 0
 
     def decide(self, stream=None):
+        if self.admission:
+            self.ctx.decide_admit(self.model, self.inst, self.I, self.req[self.cur], self.I * self.cap,
+                                  self.t_dead[self.cur], self.freq, self.tbt, self.level, self.status, None,
+                                  self.adm_lost, stream)
+            return
         self.ctx.decide(self.model, self.inst, self.I, self.req[self.cur], self.I * self.cap, self.t_dead[self.cur],
                         self.freq, self.tbt, self.level, self.status, stream)
 
@@ -56,7 +68,8 @@ class Replay:
         c, o = self.cur, 1 - self.cur
         tp.tp_replay_advance(self.model, self.inst, self.I, self.req[c], self.t_dead[c], self.req[o], self.t_dead[o],
                              self.cap, self.H, self.B, self.KV, self.n, self.n_adm, self.status, self.level, self.freq,
-                             self.arr_t, self.arr_req, self.arr_dead, self.arr_off, self.arr_next, self.stats, stream)
+                             self.arr_t, self.arr_req, self.arr_dead, self.arr_off, self.arr_next, self.stats,
+                             self.adm_lost, stream)
         self.cur = o
         self.rounds += 1
 

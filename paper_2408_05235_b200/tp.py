@@ -50,7 +50,7 @@ _L.tp_runs_total.argtypes = [_vp, _i32, _i32, ctypes.POINTER(_i64)]
 _L.tp_cells_total.argtypes = [_vp, _vp, _i32, _i32, _i32, ctypes.POINTER(_i64)]
 _L.tp_select_freq.argtypes = [_vp, _i32, _vp, _i32, _vp, _vp, _vp, _vp, _i32, _i32, _f32, _vp, _vp, _vp, _vp]
 _L.tp_select_freq_ws.argtypes = [_vp, _vp, _vp, _i32, _vp, _i32, _vp, _vp, _vp, _i32, _i32, _f32, _vp, _vp, _vp, _vp]
-_L.tp_replay_advance.argtypes = [_vp, _vp, _i32, _vp, _vp, _vp, _vp, _i32, _i32] + [_vp] * 6 + [_vp, _i32] + [_vp] * 7
+_L.tp_replay_advance.argtypes = [_vp, _vp, _i32, _vp, _vp, _vp, _vp, _i32, _i32] + [_vp] * 6 + [_vp, _i32] + [_vp] * 8
 _L.tp_ctx_enable_admission.argtypes = [_vp, _i32]
 _L.tp_decide_admit.argtypes = [_vp, _vp, _vp, _i32, _vp, _i32, _vp, _vp, _i32, _f32, _vp, _vp, _vp, _vp, _vp]
 _L.tp_ctx_create.argtypes = [ctypes.c_int, _vp, _i32, _i32, _i32, _i32, ctypes.POINTER(_vp)]
@@ -204,12 +204,14 @@ def tp_select_freq_ws(model: Gbdt, workspace, inst, n_inst, req, n_req, t_dead, 
 
 
 def tp_replay_advance(model: Gbdt, inst, n_inst, req, t_dead, req_out, t_dead_out, slot_cap, H, B, KV, n, n_adm,
-                      status, level, freq, arr_t, arr_req, arr_dead, arr_off, arr_next, stats, stream=None):
+                      status, level, freq, arr_t, arr_req, arr_dead, arr_off, arr_next, stats, adm_lost=None,
+                      stream=None):
     f, F = _freq(freq)
     _check(_L.tp_replay_advance(model.handle, _dp(inst), int(n_inst), _dp(req), _dp(t_dead), _dp(req_out),
                                 _dp(t_dead_out), int(slot_cap), int(H), _dp(B), _dp(KV), _dp(n), _dp(n_adm),
                                 _dp(status), _dp(level), f.ctypes.data, F, _dp(arr_t), _dp(arr_req), _dp(arr_dead),
-                                _dp(arr_off), _dp(arr_next), _dp(stats), _stream(stream)), "tp_replay_advance")
+                                _dp(arr_off), _dp(arr_next), _dp(stats), _dp(adm_lost), _stream(stream)),
+           "tp_replay_advance")
 
 
 class Ctx:

@@ -248,7 +248,7 @@ def replay_completion(box: BoxModel, inst, reqs, n_sched: int, freq_u: float, N:
     return done
 
 
-def replay_advance(inst, req, t_dead, arr_next, data, dec, oracle_model, freq, cap):
+def replay_advance(inst, req, t_dead, arr_next, data, dec, oracle_model, freq, cap, adm_lost=None):
     """One engine iteration per instance (the semantics include/tp.h states for tp_replay_advance),
     written independently of replay.cu.  dec: oracle decision dict for the same state."""
     inst = inst.copy()
@@ -279,6 +279,8 @@ def replay_advance(inst, req, t_dead, arr_next, data, dec, oracle_model, freq, c
         out = []
         for e in range(nr + nadm if it else 0):
             r = req[b + e].copy()
+            if adm_lost is not None and e >= nr and e - nr < 32 and (int(adm_lost[i]) >> (e - nr)) & 1:
+                r["flags"] |= LOST
             r["a"] += 1
             if r["r"] - r["a"] == 0:
                 stats[0] += 1

@@ -24,13 +24,13 @@ def gpu():
     return tp, replay
 
 
-def _check_rounds(gpu, oracle_mod, rc, ens_cfg, rounds, every=1):
+def _check_rounds(gpu, oracle_mod, rc, ens_cfg, rounds, every=1, admission=0):
     tp, replay = gpu
     data = W.gen_replay(rc)
     blob = W.write_blob(W.config_ensemble(ens_cfg))
     model = tp.Gbdt(blob, 0)
     om = oracle_mod.Model(blob)
-    rp = replay.Replay(data, model)
+    rp = replay.Replay(data, model, admission=admission)
     stats = np.zeros(5, np.int64)
     checked = 0
     for k in range(rounds):
@@ -38,16 +38,20 @@ def _check_rounds(gpu, oracle_mod, rc, ens_cfg, rounds, every=1):
             rp.round()
             continue
         inst, req, td, arr_next = rp.state()
-        dec = oracle_mod.decide(om, inst, req, td, data["H"], data["freq"], data["tbt_slo"], want_grid=False)
+        dec = oracle_mod.decide(om, inst, req, td, data["H"], data["freq"], data["tbt_slo"], want_grid=False,
+                                admission=1 if admission else 0, adm_limit=admission or 32)
         rp.decide()
         torch.cuda.synchronize()
         assert np.array_equal(rp.level.cpu().numpy(), dec["level"]), k
         assert np.array_equal(rp.status.cpu().numpy().view(np.uint32), dec["status"]), k
+        if admission:
+            assert np.array_equal(rp.adm_lost.cpu().numpy().view(np.uint32), dec["adm_lost"]), k
         s0 = rp.stats.cpu().numpy().copy()
         rp.advance()
         inst2, req2, td2, arr2 = rp.state()
         e_inst, e_req, e_td, e_arr, e_stats = refimpl.replay_advance(inst, req, td, arr_next, data, dec, om,
-                                                                     data["freq"], rc.slot_cap)
+                                                                     data["freq"], rc.slot_cap,
+                                                                     dec.get("adm_lost"))
         assert np.array_equal(inst2, e_inst), k
         assert np.array_equal(arr2, e_arr), k
         for i in range(rc.n_inst):
@@ -85,3 +89,12 @@ def test_replay_runs_to_completion(gpu, oracle_mod):
     st = rp.stats_dict()
     initial = int((data["inst"]["n_run"] + data["inst"]["n_queue"]).sum())
     assert st["completed"] == initial + rc.n_requests - st["dropped_arrivals"]
+
+
+def test_replay_with_admission_control(gpu, oracle_mod):
+    """The paper's full loop: admission control (checks 1-3, lost marks persisted) + throttle each round."""
+    rc = W.ReplayConfig(n_inst=24, n_requests=3000, span_s=1.5, slot_cap=300, seed=12)
+    ens = dataclasses.replace(W.CONFIGS["C4"], n_trees=30, depth=6)
+    rp, checked = _check_rounds(gpu, oracle_mod, rc, ens, rounds=40, admission=8)
+    assert checked == 40
+    assert rp.stats_dict()["admissions"] > 0
