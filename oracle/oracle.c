@@ -159,6 +159,7 @@ typedef struct {
     int admission;
     int adm_limit;        /* admission = 1: at most this many candidates (<= 32) per decision (A-23) */
     uint32_t* adm_lost;   /* out (admission = 1): bit c = queued candidate c admitted as lost */
+    int search;           /* 0: exhaustive over all F levels (A-13); 1: the paper's binary search (A-24) */
 } o_job;
 
 /* T_R at level u over m = 1..n for the curves (Bv, KVv): O6 + O7.  Returns 1 if a model
@@ -187,6 +188,33 @@ static int level_times(const o_job* J, const o_inst* in, const int64_t* Bv, cons
         if (tr_out) tr_out[m - 1] = acc_ticks;
     }
     return clamped;
+}
+
+/* O6..O8 at level u for an instance with horizon n and n_adm admitted requests: returns 1 if the
+ * TBT check and Eq. 4 for every scheduled request pass; ORs IPS_CLAMPED into *st (reading A-8);
+ * writes the level's ips / T_R rows when the caller asked for the grid. */
+static int level_passes(const o_job* J, int64_t i, const o_inst* in, const int64_t* Bv, const int64_t* KVv,
+                        int32_t n, int32_t n_adm, int32_t u, float* tcol, int64_t* trv, uint32_t* st) {
+    const int32_t F = J->F, H = J->H;
+    /* O6: T[m] = M(tp, B[m], KV[m], f_u); T'[m] = 1 / T[m] in fp32 (A-9).
+     * O7: Eq. 3 T_R[l] = sum_{m<=l} T'[m], exactly (A-10): each T' is an fp32 in
+     * [2^-17, 16], hence an integer multiple of 2^-40 s, so the sum is kept in such ticks. */
+    if (level_times(J, in, Bv, KVv, n, u, tcol, trv, J->ips ? J->ips + ((int64_t)i * F + u) * H : NULL,
+                    J->tr ? J->tr + ((int64_t)i * F + u) * H : NULL))
+        *st |= O_IPS_CLAMPED;
+    /* O8: TBT check 2: mean(T') = T_R[n] / n must not exceed the SLO (tie passes). */
+    long double tr_n = (long double)trv[n];
+    int pass = tr_n <= (long double)n * (long double)J->tbt * 0x1p40L;
+    /* E2E, Eq. 4: T_R[l] + t_cur < t_dead for every scheduled request, compared
+     * as T_R[l] < fl64(t_dead - t_cur) (A-12).  Lost requests are ignored by SLO validation
+     * (P:529), but their presence already took the bypass, so none is here. */
+    for (int32_t e = 0; pass && e < in->n_run + n_adm; ++e) {
+        const o_req* q = &J->req[in->req_begin + e];
+        int32_t l = q->r - q->a;
+        double slack = J->t_dead[in->req_begin + e] - in->t_cur;
+        if (!((long double)trv[l] < (long double)slack * 0x1p40L)) pass = 0;
+    }
+    return pass;
 }
 
 static void decide_one(const o_job* J, int64_t i, int64_t* Bv, int64_t* KVv, float* tcol, int64_t* trv) {
@@ -289,31 +317,28 @@ static void decide_one(const o_job* J, int64_t i, int64_t* Bv, int64_t* KVv, flo
     if (n == 0) { st |= O_EMPTY; level = 0; goto write; }                 /* reading A-15 */
     if (lost) { st |= O_BYPASS_LOST; level = F - 1; goto write; }
 
-    /* ---- O6..O9 per frequency, ascending; lowest passing level (reading A-13) ---- */
-    level = -1;
-    for (int32_t u = 0; u < F; ++u) {
-        /* O6: T[m] = M(tp, B[m], KV[m], f_u); T'[m] = 1 / T[m] in fp32 (A-9).
-         * O7: Eq. 3 T_R[l] = sum_{m<=l} T'[m], exactly (A-10): each T' is an fp32 in
-         * [2^-17, 16], hence an integer multiple of 2^-40 s, so the sum is kept in such ticks. */
-        if (level_times(J, in, Bv, KVv, n, u, tcol, trv, J->ips ? J->ips + ((int64_t)i * F + u) * H : NULL,
-                        J->tr ? J->tr + ((int64_t)i * F + u) * H : NULL))
-            st |= O_IPS_CLAMPED;
-        /* O8: TBT check 2: mean(T') = T_R[n] / n must not exceed the SLO (tie passes). */
-        long double tr_n = (long double)trv[n];
-        int pass = tr_n <= (long double)n * (long double)J->tbt * 0x1p40L;
-        /* E2E, Eq. 4: T_R[l] + t_cur < t_dead for every scheduled request, compared
-         * as T_R[l] < fl64(t_dead - t_cur) (A-12).  Lost requests are ignored by SLO validation
-         * (P:529), but their presence already took the bypass above, so none is here. */
-        for (int32_t e = 0; pass && e < in->n_run + n_adm; ++e) {
-            const o_req* q = &J->req[in->req_begin + e];
-            int32_t l = q->r - q->a;
-            double slack = J->t_dead[in->req_begin + e] - in->t_cur;
-            if (!((long double)trv[l] < (long double)slack * 0x1p40L)) pass = 0;
+    /* ---- O6..O9: lowest SLO-meeting level ---- */
+    if (J->search == 0) {
+        /* exhaustive (reading A-13): every level, ascending; the answer is the lowest passing one */
+        level = -1;
+        for (int32_t u = 0; u < F; ++u)
+            if (level_passes(J, i, in, Bv, KVv, n, n_adm, u, tcol, trv, &st) && level < 0) level = u;
+        if (level < 0) { level = F - 1; st |= O_INFEASIBLE; }               /* reading A-14 */
+    } else {
+        /* the paper's binary search over the frequency range (reading A-24): the maximum
+         * level must pass (the scheduler's guarantee), then lo/hi with pass(hi) invariant */
+        if (!level_passes(J, i, in, Bv, KVv, n, n_adm, F - 1, tcol, trv, &st)) {
+            level = F - 1; st |= O_INFEASIBLE;
+        } else {
+            int32_t lo = 0, hi = F - 1;
+            while (lo < hi) {
+                int32_t mid = (lo + hi) / 2;
+                if (level_passes(J, i, in, Bv, KVv, n, n_adm, mid, tcol, trv, &st)) hi = mid;
+                else lo = mid + 1;
+            }
+            level = lo;
         }
-        if (pass && level < 0) level = u;
-        if (pass && !J->ips && !J->tr) break;      /* lowest passing level found */
     }
-    if (level < 0) { level = F - 1; st |= O_INFEASIBLE; }                   /* reading A-14 */
 
 write:
     if (J->B) for (int32_t m = 1; m <= H; ++m) J->B[(int64_t)i * H + m - 1] = (int32_t)Bv[m];
@@ -345,7 +370,7 @@ int oracle_decide(const o_model* m, const o_inst* inst, int64_t n_inst, const o_
                   const double* t_dead, int32_t H, const float* freq, int32_t F, float tbt,
                   int32_t* B, int32_t* KV, int32_t* n, int32_t* n_adm, float* ips, int64_t* tr,
                   int32_t* level, uint32_t* status, int n_threads, int admission, uint32_t* adm_lost,
-                  int adm_limit) {
+                  int adm_limit, int search) {
     if (!m || H < 1 || H > 16384 || F < 1 || F > 32 || n_inst < 0) return -1;
     if (!(tbt >= 0x1p-17f && tbt <= 16.0f)) return -1;
     for (int32_t u = 0; u < F; ++u) {
@@ -353,8 +378,9 @@ int oracle_decide(const o_model* m, const o_inst* inst, int64_t n_inst, const o_
         if (u > 0 && !(freq[u] > freq[u - 1])) return -1;
     }
     if (adm_limit < 1 || adm_limit > 32) adm_limit = 32;
+    if (search != 0 && search != 1) return -1;
     o_job J = {m, inst, req, t_dead, n_req, H, F, freq, tbt, B, KV, n, n_adm, level, status, ips, tr,
-               admission, adm_limit, adm_lost};
+               admission, adm_limit, adm_lost, search};
     if (n_threads < 1) n_threads = 1;
     if (n_threads > 256) n_threads = 256;
     if (n_threads == 1) {

@@ -45,7 +45,8 @@ def lib():
         L.oracle_predict_raw.argtypes = [vp, vp]
         L.oracle_predict_raw.restype = ctypes.c_float
         L.oracle_decide.argtypes = [vp, vp, i64, vp, i64, vp, i32, vp, i32, ctypes.c_float,
-                                    vp, vp, vp, vp, vp, vp, vp, vp, ctypes.c_int, ctypes.c_int, vp, ctypes.c_int]
+                                    vp, vp, vp, vp, vp, vp, vp, vp, ctypes.c_int, ctypes.c_int, vp, ctypes.c_int,
+                                    ctypes.c_int]
         L.oracle_decide.restype = ctypes.c_int
         _lib = L
     return _lib
@@ -77,13 +78,17 @@ def _p(a):
 
 
 def decide(model: Model, inst, req, t_dead, H, freq, tbt_slo, *, want_grid=True, want_tr=False,
-           threads: int = 1, want_curves=True, admission: int = 0, adm_limit: int = 32):
+           threads: int = 1, want_curves=True, admission: int = 0, adm_limit: int = 32,
+           search: str = "exhaustive"):
     """Run O0..O9 on every instance.  Returns a dict of numpy arrays:
     B, KV [I,H] int32; n, n_adm, level [I] int32; status [I] uint32;
     ips [I,F,H] fp32 (if want_grid); tr [I,F,H] int64 ticks of 2^-40 s (if want_tr).
     Grid entries are defined for m <= n only (others stay 0).
     admission=1: the paper's full admission control (checks 1-3 at f_max, lost marking, P:500-529);
-    out["adm_lost"] bit c = queued candidate c admitted as lost."""
+    out["adm_lost"] bit c = queued candidate c admitted as lost.
+    search="exhaustive": every level is evaluated, answer = lowest passing (reading A-13);
+    search="binary": the paper's binary search (reading A-24) -- the grid then holds only
+    the levels the search visited."""
     inst = np.ascontiguousarray(inst)
     req = np.ascontiguousarray(req)
     t_dead = np.ascontiguousarray(t_dead, dtype=np.float64)
@@ -104,7 +109,7 @@ def decide(model: Model, inst, req, t_dead, H, freq, tbt_slo, *, want_grid=True,
                              float(np.float32(tbt_slo)), _p(out.get("B")), _p(out.get("KV")), _p(out["n"]),
                              _p(out["n_adm"]), _p(out.get("ips")), _p(out.get("tr")), _p(out["level"]),
                              _p(out["status"]), int(threads), int(admission), _p(out.get("adm_lost")),
-                             int(adm_limit))
+                             int(adm_limit), {"exhaustive": 0, "binary": 1}[search])
     if rc != 0:
         raise ValueError(f"oracle: invalid arguments (rc={rc})")
     return out

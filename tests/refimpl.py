@@ -131,7 +131,7 @@ def _times(box, tpf, B, KV, n, f):
     return TR, bool(clamped.any())
 
 
-def brute_decide(box: BoxModel, inst, reqs, deads, H, freq, tbt, admission=0):
+def brute_decide(box: BoxModel, inst, reqs, deads, H, freq, tbt, admission=0, search="exhaustive"):
     """Full decision for ONE instance with exact rationals; returns dict like the oracle's.
     admission=1: the paper's admission control (checks 1-3 at f_max, lost marking)."""
     F = len(freq)
@@ -199,18 +199,35 @@ def brute_decide(box: BoxModel, inst, reqs, deads, H, freq, tbt, admission=0):
     if any(int(reqs[e]["flags"]) & LOST for e in sched) or marked:
         res.update(status=st | ST_BYPASS_LOST, level=F - 1)
         return res
-    level = None
-    for u in range(F):
+    flags = [st]
+
+    def passes(u):
         TR, clamped = _times(box, tpf, B, KV, n, freq[u])
         if clamped:
-            st |= ST_IPS_CLAMPED
+            flags[0] |= ST_IPS_CLAMPED
         ok = TR[-1] / n <= Fraction(float(np.float32(tbt)))
         for e in sched:
             l = int(reqs[e]["r"]) - int(reqs[e]["a"])
             slack = Fraction(float(np.float64(deads[e]) - np.float64(inst["t_cur"])))
             ok = ok and TR[l - 1] < slack
-        if ok and level is None:
-            level = u
+        return ok
+
+    if search == "exhaustive":
+        ok = [passes(u) for u in range(F)]
+        level = ok.index(True) if any(ok) else None
+    else:
+        # binary search over the frequency range; the top level must pass
+        level = None
+        if passes(F - 1):
+            lo, hi = 0, F - 1
+            while lo < hi:
+                mid = (lo + hi) // 2
+                if passes(mid):
+                    hi = mid
+                else:
+                    lo = mid + 1
+            level = lo
+    st = flags[0]
     if level is None:
         level = F - 1
         st |= ST_INFEASIBLE

@@ -383,6 +383,9 @@ def test_binary_search_equals_exhaustive_on_monotone_models(oracle_mod):
         d = W.config_inputs(cfg)
         m = oracle_mod.Model(W.write_blob(ens))
         full = oracle_mod.decide(m, d["inst"], d["req"], d["t_dead"], d["H"], freq, 0.2, want_grid=False)
+        bs = oracle_mod.decide(m, d["inst"], d["req"], d["t_dead"], d["H"], freq, 0.2, want_grid=False,
+                               search="binary")
+        assert (bs["level"] == full["level"]).all() and (bs["status"] == full["status"]).all()
         for i in range(24):
             st = int(full["status"][i])
             if st & (refimpl.ST_BAD_INPUT | refimpl.ST_EMPTY | refimpl.ST_BYPASS_LOST):
@@ -406,6 +409,54 @@ def test_binary_search_equals_exhaustive_on_monotone_models(oracle_mod):
             assert full["level"][i] == lo
             agree += 1
     assert agree >= 200
+
+
+def test_binary_search_brute_force_tiny(oracle_mod):
+    """Reading A-24: the oracle's binary-search mode == the binary search written from
+    the paper over exact Fraction pass/fail (refimpl), on non-monotone random ensembles; and it
+    differs from the exhaustive answer on some of them (so the mode is really exercised)."""
+    rng = np.random.default_rng(24)
+    n_cmp = differ = 0
+    for trial in range(80):
+        ens, inst, req, td, H, freq, tbt = cases.random_tiny_case(rng, F=int(rng.integers(1, 9)))
+        out = run(oracle_mod, ens, inst, req, td, H, freq, tbt, search="binary", want_grid=False)
+        exh = run(oracle_mod, ens, inst, req, td, H, freq, tbt, want_grid=False)
+        box = refimpl.BoxModel(ens)
+        for i in range(len(inst)):
+            b = int(inst[i]["req_begin"]); e = b + int(inst[i]["n_run"]) + int(inst[i]["n_queue"])
+            ref = refimpl.brute_decide(box, inst[i], req[b:e], td[b:e], H, freq, tbt, search="binary")
+            got = dict(level=int(out["level"][i]), status=int(out["status"][i]), n=int(out["n"][i]),
+                       n_adm=int(out["n_adm"][i]))
+            assert got == {k: ref[k] for k in got}, (trial, i)
+            differ += int(out["level"][i] != exh["level"][i] or out["status"][i] != exh["status"][i])
+            n_cmp += 1
+    assert n_cmp >= 400 and differ >= 5
+
+
+def test_binary_search_order_and_clamp_of_visited_levels(oracle_mod):
+    """A-24: the search visits F-1, then mid = (lo + hi) // 2; IPS_CLAMPED covers visited levels
+    only.  F = 4, every level passes: visits 3, 1, 0 -> level 0; level 2 (never visited) is the
+    only one whose output clamps, so only the exhaustive scan flags it."""
+    f = np.array([1000.0, 1200.0, 1400.0, 1600.0], np.float32)
+    ens = cases.ensemble_from_nodes([{"feature": 3, "threshold": 1300.0, "left": 1, "right": 2},
+                                     {"feature": -1, "leaf": 50.0},
+                                     {"feature": 3, "threshold": 1500.0, "left": 3, "right": 4},
+                                     {"feature": -1, "leaf": 1e9}, {"feature": -1, "leaf": 50.0}])
+    inst, req, td = cases.make_instances([dict(N=16, running=[(0, 5, 4, 0, 1e6)])], 4)
+    exh = run(oracle_mod, ens, inst, req, td, 4, f, 16.0)
+    bs = run(oracle_mod, ens, inst, req, td, 4, f, 16.0, search="binary")
+    assert exh["level"][0] == 0 and bs["level"][0] == 0
+    assert exh["status"][0] == refimpl.ST_IPS_CLAMPED and bs["status"][0] == 0
+    # the grid holds the visited levels only
+    assert (bs["ips"][0, 2] == 0).all() and (bs["ips"][0, [0, 1, 3], :4] == 50.0).all()
+    # non-monotone pass pattern: only levels 0 and 3 pass -> the search (3, 1 fails, 2 fails) ends at 3
+    ens2 = cases.ensemble_from_nodes([{"feature": 3, "threshold": 1100.0, "left": 1, "right": 2},
+                                      {"feature": -1, "leaf": 64.0},
+                                      {"feature": 3, "threshold": 1500.0, "left": 3, "right": 4},
+                                      {"feature": -1, "leaf": 1.0}, {"feature": -1, "leaf": 64.0}])
+    inst, req, td = cases.make_instances([dict(N=16, running=[(0, 5, 8, 0, 1.0)])], 8)
+    assert run(oracle_mod, ens2, inst, req, td, 8, f, 16.0)["level"][0] == 0
+    assert run(oracle_mod, ens2, inst, req, td, 8, f, 16.0, search="binary")["level"][0] == 3
 
 
 def test_zero_drift_replay(oracle_mod):
