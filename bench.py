@@ -104,7 +104,7 @@ def measured_peaks():
         return {}
 
 
-def cpu_baseline(cfg, blob, inputs, budget_s=15.0):
+def cpu_baseline(cfg, blob, inputs, budget_s=15.0, search="exhaustive"):
     """The oracle, as it stands, on this host's cores, on a bounded prefix of the workload."""
     from oracle import oracle
     m = oracle.Model(blob)
@@ -116,7 +116,7 @@ def cpu_baseline(cfg, blob, inputs, budget_s=15.0):
         last = int(sub[-1]["req_begin"] + sub[-1]["n_run"] + sub[-1]["n_queue"])
         t = time.perf_counter()
         oracle.decide(m, sub, inputs["req"][:last], inputs["t_dead"][:last], inputs["H"], inputs["freq"],
-                      inputs["tbt_slo"], want_grid=False, want_curves=False, threads=threads)
+                      inputs["tbt_slo"], want_grid=False, want_curves=False, threads=threads, search=search)
         return time.perf_counter() - t
 
     k = min(len(inst), max(threads, 8))
@@ -128,8 +128,9 @@ def cpu_baseline(cfg, blob, inputs, budget_s=15.0):
         k = min(len(inst), max(k, int(k * budget_s / max(dt, 1e-3))))
         dt = run(k)
     return {"value": k / dt, "unit": "decisions/s", "cores": threads, "kind": "oracle",
-            "sample": f"first {k} of {len(inst)} instances of {cfg.name} (all levels scanned up to the lowest "
-                      f"passing one, {threads} threads), {dt:.1f} s"}
+            "sample": f"first {k} of {len(inst)} instances of {cfg.name} ("
+                      + ("all F levels evaluated" if search == "exhaustive" else "the paper's binary search")
+                      + f", {threads} threads), {dt:.1f} s"}
 
 
 def bench_reference(args, cfg):
@@ -146,7 +147,7 @@ def bench_reference(args, cfg):
 
     def step():
         oracle.decide(m, inputs["inst"], inputs["req"], inputs["t_dead"], inputs["H"], inputs["freq"],
-                      inputs["tbt_slo"], want_grid=False, want_curves=False, threads=threads)
+                      inputs["tbt_slo"], want_grid=False, want_curves=False, threads=threads, search=args.search)
     for _ in range(args.warmup):
         step()
     t = time.perf_counter()
@@ -158,7 +159,8 @@ def bench_reference(args, cfg):
             "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup, "ms_per_step": dt / args.steps * 1e3,
             "higher_is_better": True, "scaling": "weak" if cfg.name != "C5" else "strong", "vs_baseline": None,
             "dtype": "f32", "data": "synthetic",
-            "config": {"workload": DESCR[cfg.name], "instances_per_step": per_step},
+            "config": {"workload": DESCR[cfg.name], "name": cfg.name, "instances_per_step": per_step,
+                       "search": args.search},
             "cpu_baseline": {"value": v, "unit": "decisions/s", "cores": threads, "kind": "oracle",
                              "sample": f"first {per_step} instances of {cfg.name} per step"},
             "e2e": {"value": v, "unit": "decisions/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
@@ -188,7 +190,7 @@ def bench_replay(args, cfg, rank, world, local, dist, dist_test):
     i0, i1 = shard.shard_range(rc.n_inst, rank, world)
     data = slice_replay(data, i0, i1)
     model = tp.Gbdt(W.write_blob(W.config_ensemble(cfg)), local)
-    rp = replay.Replay(data, model, dev, admission=args.admission)
+    rp = replay.Replay(data, model, dev, admission=args.admission, search=args.search)
     stream = torch.cuda.current_stream(dev)
     for _ in range(max(args.warmup, 3)):
         rp.round(stream)
@@ -228,6 +230,7 @@ def bench_replay(args, cfg, rank, world, local, dist, dist_test):
                    "step": "decide all instances + advance all instances one iteration (GPU-resident replay)",
                    "admission": (f"full admission control (checks 1-3 at f_max, lost marking), q_max={args.admission}"
                                  if args.admission else "check 1 + batch cap gate"),
+                   "search": args.search,
                    "l2": "not flushed: the replay state (~20 MB) is re-used every round by design"},
         "decisions_per_sec_decide_only": I * args.steps / (float(tot[1]) / 1e3),
         "per_round_ms": {"decide": dec_ms / args.steps, "advance": adv_ms / args.steps},
@@ -248,6 +251,9 @@ def main():
     ap.add_argument("--e2e-steps", type=int, default=None)
     ap.add_argument("--admission", type=int, default=0,
                     help="C4 replay: run the paper's full admission control on up to N queued requests per instance")
+    ap.add_argument("--search", default="exhaustive", choices=["exhaustive", "binary"],
+                    help="K3 order: lowest passing level over all levels (reading A-13, default) or the "
+                         "paper's binary search (P:555, reading A-24; needs --k2 fused)")
     ap.add_argument("--k2", default="fused", choices=["fused", "cells", "runs", "direct"],
                     help="K2 variant: cell-memoised fused with K3 (default), cell-memoised with the ips grid, "
                          "run-compressed, or one evaluation per grid point")
@@ -299,7 +305,7 @@ def main():
     I, R = len(inputs["inst"]), len(inputs["req"])
     model = tp.Gbdt(blob, local)
     info = model.info()
-    rnd = runner.Round(inputs, dev, k2_mode=args.k2, model=model)
+    rnd = runner.Round(inputs, dev, k2_mode=args.k2, model=model, search=args.search)
     dec = torch.empty((2, max(I, 1)), dtype=torch.int32, device=dev)   # level, status rows
     rnd.level, rnd.status = dec[0], dec[1]
     # equal shards (C2 weak, C5 = 262144 / {1,2,4,8}): one preallocated all-gather of [2, I] rows
@@ -392,6 +398,7 @@ def main():
     if True:
         ctx = tp.Ctx(local, I, R, rnd.H, rnd.F, model if args.k2 in ("cells", "fused") else None)
         ctx.set_k2_mode(tp.K2_DIRECT if args.k2 == "direct" else tp.K2_RUNS)
+        ctx.set_search(args.search)
         h_inst = torch.from_numpy(inputs["inst"].view(np.uint8)).pin_memory()
         h_req = torch.from_numpy(inputs["req"].view(np.uint8)).pin_memory()
         h_td = torch.from_numpy(inputs["t_dead"]).pin_memory()
@@ -455,7 +462,7 @@ def main():
                              "note": "tp_predict_ips (one descent per grid point) on the same inputs"}
     cpu = None
     if world == 1 and not args.no_cpu_baseline:
-        cpu = cpu_baseline(cfg, blob, inputs)
+        cpu = cpu_baseline(cfg, blob, inputs, search=args.search)
     line = {
         "metric": "frequency decisions/sec", "value": decisions_per_s, "unit": "decisions/s",
         "n_gpus": world, "steps": args.steps, "warmup": max(args.warmup, 3), "ms_per_step": t_max_ms / args.steps,
@@ -464,14 +471,16 @@ def main():
         "config": {"workload": DESCR[cfg.name], "name": cfg.name, "instances_per_gpu": I,
                    "global_instances": int(inst_all), "H": cfg.H, "F": cfg.F, "trees": info.n_trees,
                    "depth": info.depth, "parallelism": f"instance-sharded x{world}" + (" + NCCL all-gather" if world > 1 else ""),
-                   "l2": "flushed between timed steps (256 MiB device write, untimed)", "k2": args.k2},
+                   "l2": "flushed between timed steps (256 MiB device write, untimed)", "k2": args.k2,
+                   "search": args.search},
         "grid_evals_per_sec": grid_per_s,
         "per_kernel_ms": {"k1_project": k_ms[0], "k2_gbdt": k_ms[1], "k3_select": k_ms[2],
                           "gather": k_ms[3]},
         "roofline": roof,
         "cpu_baseline": cpu,
         "e2e": e2e,
-        "gpu_launches": 3 * args.steps,
+        # our kernels per step: k1_project, [k2_runs], k2_gbdt, [k2_expand], k3_select*
+        "gpu_launches": {"direct": 3, "runs": 4, "cells": 5, "fused": 4}[args.k2] * args.steps,
         "clocks": clk,
         "paper_context": "paper controller on host CPU (A100 box): projection <2 ms, model ~3 ms per call, "
                          "scheduler+throttle 35 ms per decision (P:466, P:495, P:557)",

@@ -225,6 +225,22 @@ int tp_select_freq_ws(const tp_gbdt* m, const void* workspace, const tp_inst* in
                       uint32_t* status, int64_t* tr_ticks, void* stream);
 
 /*
+ * K3 in the paper's search order (PAPER §4.5; reading A-24): the binary
+ * search over the frequency range instead of the exhaustive scan.  Same inputs, outputs, LUT
+ * workspace and errors as tp_select_freq_ws, without the T_R output.  Per instance: the top level
+ * F-1 is checked (fails -> level F-1 + INFEASIBLE); then lo = 0, hi = F-1, and while lo < hi,
+ * mid = (lo + hi) / 2 moves hi to mid if mid passes, lo to mid + 1 otherwise; level = lo.
+ * IPS_CLAMPED covers the visited levels only.  Equals tp_select_freq_ws whenever the pass/fail
+ * outcome is monotone in the level; otherwise the answer is the one the paper's search reaches.
+ * The search is unrolled speculatively on the GPU (one warp per candidate level, 8 per round);
+ * only the levels on the search path affect the result.
+ */
+int tp_select_freq_binary(const tp_gbdt* m, const void* workspace, const tp_inst* inst, int32_t n_inst,
+                          const tp_req* req, int32_t n_req, const double* t_dead, const int32_t* n,
+                          const int32_t* n_adm, int32_t H, int32_t F, float tbt_slo, int32_t* level,
+                          uint32_t* status, void* stream);
+
+/*
  * Convenience: one decision round with library-owned scratch.
  * tp_ctx_create allocates, on `device`, B/KV/n/n_adm (n_inst_max x H), the ips grid
  * (n_inst_max x F_max x H), the K2 workspace (sized for `model`'s cell mode; NULL = run mode)
@@ -274,6 +290,13 @@ int tp_decide_admit(tp_ctx* c, const tp_gbdt* m, const tp_inst* inst, int32_t n_
 /* Which K2 variant tp_decide / tp_decide_host use (default TP_K2_RUNS). */
 enum { TP_K2_DIRECT = 0, TP_K2_RUNS = 1 };
 int tp_ctx_set_k2_mode(tp_ctx* c, int mode);
+
+/* K3 search order for tp_decide / tp_decide_host / tp_decide_admit (default exhaustive, reading
+ * A-13).  TP_SEARCH_BINARY (reading A-24, tp_select_freq_binary) needs the fused cell path: a
+ * context created for the model, TP_K2_RUNS and H <= 8192; otherwise those calls return
+ * TP_ENOTIMPL. */
+enum { TP_SEARCH_EXHAUSTIVE = 0, TP_SEARCH_BINARY = 1 };
+int tp_ctx_set_search(tp_ctx* c, int search);
 
 /* Device pointers of the context's scratch (for inspection / tests); any out may be NULL. */
 int tp_ctx_buffers(tp_ctx* c, int32_t** B, int32_t** KV, int32_t** n, int32_t** n_adm, float** ips);

@@ -33,6 +33,7 @@ struct tp_ctx {
     void* work;
     size_t work_bytes;
     int k2_mode;
+    int search;                   // TP_SEARCH_EXHAUSTIVE / TP_SEARCH_BINARY (K3 order)
     const tp_gbdt* cells_model;   // the model the workspace was sized for (cell mode), or null
     // admission control (tp_ctx_enable_admission): virtual prefix instances
     int32_t qc;
@@ -191,12 +192,12 @@ int tp_select_freq(const tp_inst* inst, int32_t n_inst, const tp_req* req, int32
         return TP_EINVAL;
     const int64_t tbt_ticks = (int64_t)((double)tbt_slo * 0x1p40);   // exact: tbt_slo >= 2^-17
     return tp::launch_select(inst, n_inst, req, n_req, t_dead, n, n_adm, ips, H, F, tbt_ticks, level, status,
-                             tr_ticks, nullptr, S(stream));
+                             tr_ticks, nullptr, TP_SEARCH_EXHAUSTIVE, S(stream));
 }
 
-int tp_select_freq_ws(const tp_gbdt* m, const void* workspace, const tp_inst* inst, int32_t n_inst, const tp_req* req,
-                      int32_t n_req, const double* t_dead, const int32_t* n, const int32_t* n_adm, int32_t H, int32_t F,
-                      float tbt_slo, int32_t* level, uint32_t* status, int64_t* tr_ticks, void* stream) {
+static int select_ws(const tp_gbdt* m, const void* workspace, const tp_inst* inst, int32_t n_inst, const tp_req* req,
+                     int32_t n_req, const double* t_dead, const int32_t* n, const int32_t* n_adm, int32_t H, int32_t F,
+                     float tbt_slo, int32_t* level, uint32_t* status, int64_t* tr_ticks, int search, void* stream) {
     if (!m || n_inst < 0 || n_req < 0 || !H_ok(H) || H > tp::kMaxHRunsSelect || F < 1 || F > tp::kMaxF ||
         !tbt_ok(tbt_slo))
         return TP_EINVAL;
@@ -208,7 +209,21 @@ int tp_select_freq_ws(const tp_gbdt* m, const void* workspace, const tp_inst* in
     if (n_inst > 0 && !p.cell_tab) return TP_EINVAL;   // the model has no cell mode
     const int64_t tbt_ticks = (int64_t)((double)tbt_slo * 0x1p40);
     return tp::launch_select(inst, n_inst, req, n_req, t_dead, n, n_adm, nullptr, H, F, tbt_ticks, level, status,
-                             tr_ticks, &p, S(stream));
+                             tr_ticks, &p, search, S(stream));
+}
+
+int tp_select_freq_ws(const tp_gbdt* m, const void* workspace, const tp_inst* inst, int32_t n_inst, const tp_req* req,
+                      int32_t n_req, const double* t_dead, const int32_t* n, const int32_t* n_adm, int32_t H, int32_t F,
+                      float tbt_slo, int32_t* level, uint32_t* status, int64_t* tr_ticks, void* stream) {
+    return select_ws(m, workspace, inst, n_inst, req, n_req, t_dead, n, n_adm, H, F, tbt_slo, level, status, tr_ticks,
+                     TP_SEARCH_EXHAUSTIVE, stream);
+}
+
+int tp_select_freq_binary(const tp_gbdt* m, const void* workspace, const tp_inst* inst, int32_t n_inst,
+                          const tp_req* req, int32_t n_req, const double* t_dead, const int32_t* n, const int32_t* n_adm,
+                          int32_t H, int32_t F, float tbt_slo, int32_t* level, uint32_t* status, void* stream) {
+    return select_ws(m, workspace, inst, n_inst, req, n_req, t_dead, n, n_adm, H, F, tbt_slo, level, status, nullptr,
+                     TP_SEARCH_BINARY, stream);
 }
 
 int tp_replay_advance(const tp_gbdt* m, tp_inst* inst, int32_t n_inst, const tp_req* req, const double* t_dead,
@@ -333,8 +348,8 @@ int tp_decide_admit(tp_ctx* c, const tp_gbdt* m, const tp_inst* inst, int32_t n_
                                      c->adm_final, c->lost);
     if (!rc) rc = tp_predict_ips_runs(m, inst, n_inst, c->B, c->KV, c->n, H, freq_mhz, F, nullptr, status, c->work,
                                       c->work_bytes, stream);
-    if (!rc) rc = tp_select_freq_ws(m, c->work, inst, n_inst, req, n_req, t_dead, c->n, c->n_adm, H, F, tbt_slo,
-                                    level, status, nullptr, stream);
+    if (!rc) rc = select_ws(m, c->work, inst, n_inst, req, n_req, t_dead, c->n, c->n_adm, H, F, tbt_slo, level,
+                            status, nullptr, c->search, stream);
     if (!rc && n_adm_out && cudaMemcpyAsync(n_adm_out, c->n_adm, (size_t)n_inst * 4, cudaMemcpyDeviceToDevice, s))
         rc = TP_ECUDA;
     if (!rc && adm_lost_out &&
@@ -346,6 +361,12 @@ int tp_decide_admit(tp_ctx* c, const tp_gbdt* m, const tp_inst* inst, int32_t n_
 int tp_ctx_set_k2_mode(tp_ctx* c, int mode) {
     if (!c || (mode != TP_K2_DIRECT && mode != TP_K2_RUNS)) return TP_EINVAL;
     c->k2_mode = mode;
+    return TP_OK;
+}
+
+int tp_ctx_set_search(tp_ctx* c, int search) {
+    if (!c || (search != TP_SEARCH_EXHAUSTIVE && search != TP_SEARCH_BINARY)) return TP_EINVAL;
+    c->search = search;
     return TP_OK;
 }
 
@@ -365,11 +386,12 @@ int tp_decide(tp_ctx* c, const tp_gbdt* m, const tp_inst* inst, int32_t n_inst, 
     if (!c || !m || n_inst < 0 || n_inst > c->n_inst_max || F > c->F_max || !freq_ok(freq_mhz, F) ||
         !tbt_ok(tbt_slo))
         return TP_EINVAL;
-    int rc = tp_project(inst, n_inst, req, n_req, c->H, c->B, c->KV, c->n, c->n_adm, status, stream);
-    if (rc) return rc;
     // cell mode (ctx created with the model): K2 leaves the IPS values in the LUT and K3 reads them
     // through the runs -- the ips grid is never materialised
     const bool fused = c->k2_mode == TP_K2_RUNS && c->cells_model == m && m != nullptr && c->H <= tp::kMaxHRunsSelect;
+    if (c->search == TP_SEARCH_BINARY && !fused) return TP_ENOTIMPL;   // binary search reads the cell LUT
+    int rc = tp_project(inst, n_inst, req, n_req, c->H, c->B, c->KV, c->n, c->n_adm, status, stream);
+    if (rc) return rc;
     if (c->k2_mode == TP_K2_RUNS)
         rc = tp_predict_ips_runs(m, inst, n_inst, c->B, c->KV, c->n, c->H, freq_mhz, F, fused ? nullptr : c->ips,
                                  status, c->work, c->work_bytes, stream);
@@ -377,8 +399,8 @@ int tp_decide(tp_ctx* c, const tp_gbdt* m, const tp_inst* inst, int32_t n_inst, 
         rc = tp_predict_ips(m, inst, n_inst, c->B, c->KV, c->n, c->H, freq_mhz, F, c->ips, status, stream);
     if (rc) return rc;
     if (fused)
-        return tp_select_freq_ws(m, c->work, inst, n_inst, req, n_req, t_dead, c->n, c->n_adm, c->H, F, tbt_slo,
-                                 level, status, nullptr, stream);
+        return select_ws(m, c->work, inst, n_inst, req, n_req, t_dead, c->n, c->n_adm, c->H, F, tbt_slo, level,
+                         status, nullptr, c->search, stream);
     return tp_select_freq(inst, n_inst, req, n_req, t_dead, c->n, c->n_adm, c->ips, c->H, F, tbt_slo, level, status,
                           nullptr, stream);
 }

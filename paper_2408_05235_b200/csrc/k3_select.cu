@@ -147,6 +147,71 @@ struct WsView {
     const uint32_t* cell_clamp;
 };
 
+// One warp: does level u pass?  T_R is formed run by run from the LUT (exact ticks) and checked at
+// the compacted end positions (e_l, e_d) and, for the TBT check, at m = n.  Without trow the scan
+// stops at the first violated deadline; with trow every T_R[m] of the level is written.
+__device__ __forceinline__ bool level_passes_runs(const WsView& ws, int F, int u, int h, int ne,
+                                                  const int* r_start, const int* r_row, const int* e_l,
+                                                  const long long* e_d, long long tbt_bound, long long* trow) {
+    const int lane = threadIdx.x & 31;
+    long long carry = 0;     // T_R at the last iteration before the current chunk of runs
+    int ep = 0;              // next end position to check
+    bool ok = true;
+    for (int kb = 0; kb < h; kb += 32) {
+        const int k = kb + lane;
+        int s = 0x7fffffff;
+        long long t = 0, own = 0;
+        if (k < h) {
+            s = r_start[k];
+            t = ticks_of(__ldg(ws.lut + (size_t)r_row[k] * F + u));
+            own = (long long)(r_start[k + 1] - s) * t;      // the run's share of T_R, exact
+        }
+        long long x = own;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const long long y = __shfl_up_sync(0xffffffffu, x, o);
+            if (lane >= o) x += y;
+        }
+        const long long before = carry + x - own;           // T_R at iteration s - 1
+        const int chunk_end = r_start[min(kb + 32, h)] - 1;  // last iteration of this chunk
+        bool bad = false;
+        // end positions inside this chunk: lane j checks e_l[ep + j]
+        while (ep < ne && e_l[ep] <= chunk_end) {
+            const int j = ep + lane;
+            const int e = (j < ne) ? e_l[j] : 0x7fffffff;
+            const bool mine = e <= chunk_end;
+            int r = 0;   // last run of the chunk with start <= e
+#pragma unroll
+            for (int step = 16; step; step >>= 1) {
+                const int cand = r + step;
+                const int sc = __shfl_sync(0xffffffffu, s, cand);
+                if (sc <= e) r = cand;
+            }
+            const long long b = __shfl_sync(0xffffffffu, before, r);
+            const long long tt = __shfl_sync(0xffffffffu, t, r);
+            const int sr = __shfl_sync(0xffffffffu, s, r);
+            if (mine) bad |= !(b + (long long)(e - sr + 1) * tt < e_d[j]);
+            ep += __popc(__ballot_sync(0xffffffffu, mine));
+        }
+        if (trow && k < h)
+            for (int m = s; m < r_start[k + 1]; ++m) trow[m - 1] = before + (long long)(m - s + 1) * t;
+        carry = __shfl_sync(0xffffffffu, carry + x, 31);
+        if (__any_sync(0xffffffffu, bad)) {
+            ok = false;
+            if (!trow) break;
+        }
+    }
+    return ok && carry <= tbt_bound;          // TBT at m = n: T_R[n] <= n * slo
+}
+
+// SEARCH = 0: exhaustive (reading A-13): levels strided over the warps, a warp skips levels above
+//             one that already passed.
+// SEARCH = 1: the paper's binary search (reading A-24), speculatively unrolled: each
+//             round evaluates, one warp per level, the next levels of the search tree from the
+//             current [lo, hi] (the top level F-1 first, then the mids of the first 3 bisection
+//             steps: 1 + 2 + 4 nodes), then walks the path the sequential search takes.  Only the
+//             path's levels count (IPS_CLAMPED included); F = 32 takes 2 rounds, 11 evaluations.
+template <int SEARCH>
 __global__ void __launch_bounds__(kThreads)
 k3_select_runs(const tp_inst* __restrict__ inst, const int4* __restrict__ req, const double* __restrict__ t_dead,
                const int32_t* __restrict__ nv, const int32_t* __restrict__ nadm, int32_t H, int32_t F,
@@ -174,16 +239,20 @@ k3_select_runs(const tp_inst* __restrict__ inst, const int4* __restrict__ req, c
     const tp_inst in = inst[i];
     if (tid < kMaxF) s_pass[tid] = 0;
     if (tid == 0) s_best = F;
-    // runs: first iteration and LUT row; clamp flag from the cells' masks
-    bool cl = false;
+    // runs: first iteration and LUT row; clamp mask from the cells' masks
+    uint32_t cl = 0;
     for (int k = tid; k < h; k += kThreads) {
         r_start[k] = __ldg(ws.run_m + row + k);
         const int rr = __ldg(ws.cell_tab + __ldg(ws.run_key + row + k));
         r_row[k] = rr;
-        cl |= __ldg(ws.cell_clamp + rr) != 0;
+        cl |= __ldg(ws.cell_clamp + rr);
     }
     if (tid == 0) r_start[h] = n + 1;
-    const uint32_t st_or = __syncthreads_or(cl) ? (uint32_t)TP_ST_IPS_CLAMPED : 0u;
+    for (int o = 16; o; o >>= 1) cl |= __shfl_xor_sync(0xffffffffu, cl, o);
+    if (lane == 0) swarp[warp] = (int)cl;
+    __syncthreads();
+    uint32_t clamp_mask = 0;     // bit u: some value of level u was clamped
+    for (int w = 0; w < kWarps; ++w) clamp_mask |= (uint32_t)swarp[w];
     build_dmin(dmin, in, in.n_run + nadm[i], n, req, t_dead);
     // compact the end positions that carry a deadline (ascending)
     int ne = 0;
@@ -216,64 +285,93 @@ k3_select_runs(const tp_inst* __restrict__ inst, const int4* __restrict__ req, c
     }
 
     const long long tbt_bound = (long long)n * tbt_ticks;
-    for (int u = warp; u < F; u += kWarps) {
-        if (!tr && u > *(volatile int*)&s_best) break;      // a lower level already passed
-        long long* trow = tr ? tr + ((size_t)i * F + u) * H : nullptr;
-        long long carry = 0;     // T_R at the last iteration before the current chunk of runs
-        int ep = 0;              // next end position to check
-        bool ok = true;
-        for (int kb = 0; kb < h; kb += 32) {
-            const int k = kb + lane;
-            int s = 0x7fffffff;
-            long long t = 0, own = 0;
-            if (k < h) {
-                s = r_start[k];
-                t = ticks_of(__ldg(ws.lut + (size_t)r_row[k] * F + u));
-                own = (long long)(r_start[k + 1] - s) * t;      // the run's share of T_R, exact
-            }
-            long long x = own;
-#pragma unroll
-            for (int o = 1; o < 32; o <<= 1) {
-                const long long y = __shfl_up_sync(0xffffffffu, x, o);
-                if (lane >= o) x += y;
-            }
-            const long long before = carry + x - own;           // T_R at iteration s - 1
-            const int chunk_end = r_start[min(kb + 32, h)] - 1;  // last iteration of this chunk
-            bool bad = false;
-            // end positions inside this chunk: lane j checks e_l[ep + j]
-            while (ep < ne && e_l[ep] <= chunk_end) {
-                const int j = ep + lane;
-                const int e = (j < ne) ? e_l[j] : 0x7fffffff;
-                const bool mine = e <= chunk_end;
-                int r = 0;   // last run of the chunk with start <= e
-#pragma unroll
-                for (int step = 16; step; step >>= 1) {
-                    const int cand = r + step;
-                    const int sc = __shfl_sync(0xffffffffu, s, cand);
-                    if (sc <= e) r = cand;
-                }
-                const long long b = __shfl_sync(0xffffffffu, before, r);
-                const long long tt = __shfl_sync(0xffffffffu, t, r);
-                const int sr = __shfl_sync(0xffffffffu, s, r);
-                if (mine) bad |= !(b + (long long)(e - sr + 1) * tt < e_d[j]);
-                ep += __popc(__ballot_sync(0xffffffffu, mine));
-            }
-            if (trow && k < h)
-                for (int m = s; m < r_start[k + 1]; ++m) trow[m - 1] = before + (long long)(m - s + 1) * t;
-            carry = __shfl_sync(0xffffffffu, carry + x, 31);
-            if (__any_sync(0xffffffffu, bad)) {
-                ok = false;
-                if (!trow) break;
+    if constexpr (SEARCH == 0) {
+        for (int u = warp; u < F; u += kWarps) {
+            if (!tr && u > *(volatile int*)&s_best) break;      // a lower level already passed
+            long long* trow = tr ? tr + ((size_t)i * F + u) * H : nullptr;
+            const bool ok = level_passes_runs(ws, F, u, h, ne, r_start, r_row, e_l, e_d, tbt_bound, trow);
+            if (lane == 0) {
+                s_pass[u] = ok;
+                if (ok) atomicMin(&s_best, u);
             }
         }
-        ok = ok && carry <= tbt_bound;          // TBT at m = n: T_R[n] <= n * slo
-        if (lane == 0) {
-            s_pass[u] = ok;
-            if (ok) atomicMin(&s_best, u);
+        __syncthreads();
+        finish(i, F, st, clamp_mask ? (uint32_t)TP_ST_IPS_CLAMPED : 0u, s_pass, level, status);
+    } else {
+        __shared__ int s_lv[kWarps], s_ok[kWarps];
+        __shared__ int s_nlv, s_lo, s_hi, s_state;   // state 0: top level pending, 1: bisecting, 2: done, 3: infeasible
+        __shared__ uint32_t s_vis;
+        if (tid == 0) {
+            s_lo = 0;
+            s_hi = F - 1;
+            s_state = 0;
+            s_vis = 0;
+        }
+        __syncthreads();
+        while (true) {
+            if (tid == 0) {          // plan: breadth-first over the bisection tree from [lo, hi]
+                int k = 0;
+                if (s_state == 0) s_lv[k++] = F - 1;
+                int qlo[16], qhi[16], qh = 0, qt = 0;
+                qlo[qt] = s_lo;
+                qhi[qt++] = s_hi;
+                while (qh < qt && k < kWarps) {
+                    const int lo = qlo[qh], hi = qhi[qh++];
+                    if (lo >= hi) continue;
+                    const int mid = (lo + hi) >> 1;
+                    s_lv[k++] = mid;
+                    if (qt + 2 <= 16) {
+                        qlo[qt] = lo; qhi[qt++] = mid;          // pass(mid) -> [lo, mid]
+                        qlo[qt] = mid + 1; qhi[qt++] = hi;      // fail      -> [mid + 1, hi]
+                    }
+                }
+                s_nlv = k;
+            }
+            __syncthreads();
+            if (warp < s_nlv) {
+                const bool ok = level_passes_runs(ws, F, s_lv[warp], h, ne, r_start, r_row, e_l, e_d, tbt_bound,
+                                                  nullptr);
+                if (lane == 0) s_ok[warp] = ok;
+            }
+            __syncthreads();
+            if (tid == 0) {          // walk the path the sequential search takes
+                int k0 = 0;
+                if (s_state == 0) {
+                    s_vis |= 1u << (F - 1);
+                    s_state = s_ok[0] ? 1 : 3;
+                    k0 = 1;
+                }
+                if (s_state == 1) {
+                    int lo = s_lo, hi = s_hi;
+                    while (lo < hi) {
+                        const int mid = (lo + hi) >> 1;
+                        int j = -1;
+                        for (int q = k0; q < s_nlv; ++q)
+                            if (s_lv[q] == mid) j = q;
+                        if (j < 0) break;    // beyond this round's plan
+                        s_vis |= 1u << mid;
+                        if (s_ok[j]) hi = mid;
+                        else lo = mid + 1;
+                    }
+                    s_lo = lo;
+                    s_hi = hi;
+                    if (lo >= hi) s_state = 2;
+                }
+            }
+            __syncthreads();
+            if (s_state >= 2) break;
+        }
+        if (tid == 0) {
+            const uint32_t st_or = (clamp_mask & s_vis) ? (uint32_t)TP_ST_IPS_CLAMPED : 0u;
+            if (s_state == 2) {
+                level[i] = s_lo;
+                if (st_or) status[i] = st | st_or;
+            } else {
+                level[i] = F - 1;
+                status[i] = st | st_or | TP_ST_INFEASIBLE;
+            }
         }
     }
-    __syncthreads();
-    finish(i, F, st, st_or, s_pass, level, status);
 }
 
 bool set_attr(const void* fn, int bytes, bool* done, int dev) {
@@ -288,9 +386,10 @@ bool set_attr(const void* fn, int bytes, bool* done, int dev) {
 int launch_select(const tp_inst* inst, int32_t n_inst, const tp_req* req, int32_t n_req, const double* t_dead,
                   const int32_t* n, const int32_t* n_adm, const float* ips, int32_t H, int32_t F,
                   int64_t tbt_ticks, int32_t* level, uint32_t* status, int64_t* tr, const K2Params* ws,
-                  cudaStream_t s) {
+                  int search, cudaStream_t s) {
     (void)n_req;
     if (n_inst == 0) return TP_OK;
+    if (search != 0 && (search != 1 || !ws)) return TP_EINVAL;   // binary search: LUT path only
     int dev = 0;
     if (cudaGetDevice(&dev) != cudaSuccess) return TP_ECUDA;
     if (!ws) {
@@ -300,15 +399,16 @@ int launch_select(const tp_inst* inst, int32_t n_inst, const tp_req* req, int32_
                                                                 n_adm, ips, H, F, (long long)tbt_ticks, level, status,
                                                                 reinterpret_cast<long long*>(tr));
     } else {
-        static bool done[64] = {};
         // dmin (H+1) + e_d H (int64) + e_l H + r_start (H+1) + r_row H (int32)
         auto bytes = [](size_t h) { return (h + 1) * 8 + h * 8 + h * 4 + (h + 1) * 4 + h * 4; };
-        if (H > kMaxHRunsSelect) return TP_EINVAL;
-        if (!set_attr((const void*)k3_select_runs, (int)bytes(kMaxHRunsSelect), done, dev)) return TP_ECUDA;
+        if (H > kMaxHRunsSelect || (search == 1 && tr)) return TP_EINVAL;
+        auto kern = search == 1 ? k3_select_runs<1> : k3_select_runs<0>;
+        static bool done[2][64] = {};
+        if (!set_attr((const void*)kern, (int)bytes(kMaxHRunsSelect), done[search == 1], dev)) return TP_ECUDA;
         WsView v{ws->run_h, ws->run_m, ws->run_key, ws->cell_tab, ws->lut, ws->cell_clamp};
-        k3_select_runs<<<n_inst, kThreads, bytes((size_t)H), s>>>(inst, reinterpret_cast<const int4*>(req), t_dead, n,
-                                                                  n_adm, H, F, (long long)tbt_ticks, level, status,
-                                                                  reinterpret_cast<long long*>(tr), v);
+        kern<<<n_inst, kThreads, bytes((size_t)H), s>>>(inst, reinterpret_cast<const int4*>(req), t_dead, n, n_adm, H,
+                                                        F, (long long)tbt_ticks, level, status,
+                                                        reinterpret_cast<long long*>(tr), v);
     }
     return cudaPeekAtLastError() == cudaSuccess ? TP_OK : TP_ECUDA;
 }

@@ -113,7 +113,7 @@ int launch_gbdt(const K2Params& p, bool runs, cudaStream_t s);
 int launch_select(const tp_inst* inst, int32_t n_inst, const tp_req* req, int32_t n_req, const double* t_dead,
                   const int32_t* n, const int32_t* n_adm, const float* ips, int32_t H, int32_t F,
                   int64_t tbt_ticks, int32_t* level, uint32_t* status, int64_t* tr, const K2Params* ws,
-                  cudaStream_t s);
+                  int search, cudaStream_t s);
 
 int launch_replay_advance(const Model& m, tp_inst* inst, int32_t n_inst, const tp_req* req, const double* t_dead,
                           tp_req* req_out, double* t_dead_out, int32_t cap, int32_t H, const int32_t* B,

@@ -22,7 +22,8 @@ def _dev(a, dev, dtype=None):
 class Replay:
     STATS = ("completed", "met_deadline", "dropped_arrivals", "engine_iterations", "admissions")
 
-    def __init__(self, data: dict, model: tp.Gbdt, device="cuda:0", k2_mode=tp.K2_RUNS, admission: int = 0):
+    def __init__(self, data: dict, model: tp.Gbdt, device="cuda:0", k2_mode=tp.K2_RUNS, admission: int = 0,
+                 search: str = "exhaustive"):
         """admission = q_max > 0: each round runs the paper's full admission control (tp_decide_admit)
         on at most q_max queued requests per instance before the throttle."""
         dev = torch.device(device)
@@ -46,6 +47,7 @@ class Replay:
         self.status = torch.empty(self.I, dtype=torch.int32, device=dev)
         self.ctx = tp.Ctx(dev.index or 0, self.I, self.I * self.cap, self.H, self.F, model)
         self.ctx.set_k2_mode(k2_mode)
+        self.ctx.set_search(search)
         self.B, self.KV, self.n, self.n_adm, _ = self.ctx.buffers()
         self.admission = int(admission)
         self.adm_lost = None

@@ -21,7 +21,8 @@ def to_device_bytes(a: np.ndarray, device) -> torch.Tensor:
 class Round:
     """One decision round's device buffers (inputs + K1/K2/K3 outputs)."""
 
-    def __init__(self, inputs: dict, device="cuda:0", want_tr=False, k2_mode="cells", model=None):
+    def __init__(self, inputs: dict, device="cuda:0", want_tr=False, k2_mode="cells", model=None,
+                 search="exhaustive"):
         dev = torch.device(device)
         self.device = dev
         inst, req, t_dead = inputs["inst"], inputs["req"], inputs["t_dead"]
@@ -46,6 +47,9 @@ class Round:
         assert k2_mode in ("fused", "cells", "runs", "direct")
         assert k2_mode not in ("cells", "fused") or model is not None, "cell mode sizes its workspace from the model"
         self.k2_mode = k2_mode
+        assert search in ("exhaustive", "binary")
+        assert search == "exhaustive" or (k2_mode == "fused" and not want_tr), "binary search reads the cell LUT"
+        self.search = search
         self.model = model
         self.work = torch.empty(tp.tp_predict_ips_workspace_size(model if k2_mode in ("cells", "fused") else None,
                                                                  I, H, F),
@@ -65,6 +69,10 @@ class Round:
                               self.status, stream)
 
     def select(self, stream=None):
+        if self.search == "binary":
+            tp.tp_select_freq_binary(self.model, self.work, self.inst, self.I, self.req, self.R, self.t_dead, self.n,
+                                     self.n_adm, self.H, self.F, self.tbt, self.level, self.status, stream)
+            return
         if self.k2_mode == "fused":
             tp.tp_select_freq_ws(self.model, self.work, self.inst, self.I, self.req, self.R, self.t_dead, self.n,
                                  self.n_adm, self.H, self.F, self.tbt, self.level, self.status, self.tr, stream)

@@ -22,8 +22,10 @@ ST_QUEUE_BLOCKED, ST_IPS_CLAMPED, ST_BAD_INPUT = 16, 32, 64
 # every symbol include/tp.h declares
 EXPORTS = ["tp_gbdt_load", "tp_gbdt_free", "tp_gbdt_get_info", "tp_project", "tp_predict_ips",
            "tp_predict_ips_workspace_size", "tp_predict_ips_runs", "tp_runs_total", "tp_cells_total", "tp_select_freq", "tp_select_freq_ws", "tp_ctx_create", "tp_ctx_free",
-           "tp_decide", "tp_decide_host", "tp_replay_advance", "tp_ctx_enable_admission", "tp_decide_admit", "tp_ctx_set_k2_mode", "tp_ctx_buffers", "tp_strerror", "tp_abi_version"]
+           "tp_decide", "tp_decide_host", "tp_replay_advance", "tp_ctx_enable_admission", "tp_decide_admit", "tp_ctx_set_k2_mode", "tp_ctx_buffers",
+           "tp_select_freq_binary", "tp_ctx_set_search", "tp_strerror", "tp_abi_version"]
 K2_DIRECT, K2_RUNS = 0, 1
+SEARCH_EXHAUSTIVE, SEARCH_BINARY = 0, 1
 
 if not os.path.exists(LIB_PATH):
     raise ImportError(f"libtp.so not built ({LIB_PATH}); run __graft_entry__.build()")
@@ -50,6 +52,8 @@ _L.tp_runs_total.argtypes = [_vp, _i32, _i32, ctypes.POINTER(_i64)]
 _L.tp_cells_total.argtypes = [_vp, _vp, _i32, _i32, _i32, ctypes.POINTER(_i64)]
 _L.tp_select_freq.argtypes = [_vp, _i32, _vp, _i32, _vp, _vp, _vp, _vp, _i32, _i32, _f32, _vp, _vp, _vp, _vp]
 _L.tp_select_freq_ws.argtypes = [_vp, _vp, _vp, _i32, _vp, _i32, _vp, _vp, _vp, _i32, _i32, _f32, _vp, _vp, _vp, _vp]
+_L.tp_select_freq_binary.argtypes = [_vp, _vp, _vp, _i32, _vp, _i32, _vp, _vp, _vp, _i32, _i32, _f32, _vp, _vp, _vp]
+_L.tp_ctx_set_search.argtypes = [_vp, ctypes.c_int]
 _L.tp_replay_advance.argtypes = [_vp, _vp, _i32, _vp, _vp, _vp, _vp, _i32, _i32] + [_vp] * 6 + [_vp, _i32] + [_vp] * 8
 _L.tp_ctx_enable_admission.argtypes = [_vp, _i32]
 _L.tp_decide_admit.argtypes = [_vp, _vp, _vp, _i32, _vp, _i32, _vp, _vp, _i32, _f32, _vp, _vp, _vp, _vp, _vp]
@@ -203,6 +207,13 @@ def tp_select_freq_ws(model: Gbdt, workspace, inst, n_inst, req, n_req, t_dead, 
                                 _dp(level), _dp(status), _dp(tr_ticks), _stream(stream)), "tp_select_freq_ws")
 
 
+def tp_select_freq_binary(model: Gbdt, workspace, inst, n_inst, req, n_req, t_dead, n, n_adm, H, F, tbt_slo, level,
+                          status, stream=None):
+    _check(_L.tp_select_freq_binary(model.handle, _dp(workspace), _dp(inst), int(n_inst), _dp(req), int(n_req),
+                                    _dp(t_dead), _dp(n), _dp(n_adm), int(H), int(F), float(np.float32(tbt_slo)),
+                                    _dp(level), _dp(status), _stream(stream)), "tp_select_freq_binary")
+
+
 def tp_replay_advance(model: Gbdt, inst, n_inst, req, t_dead, req_out, t_dead_out, slot_cap, H, B, KV, n, n_adm,
                       status, level, freq, arr_t, arr_req, arr_dead, arr_off, arr_next, stats, adm_lost=None,
                       stream=None):
@@ -248,6 +259,12 @@ class Ctx:
 
     def set_k2_mode(self, mode):
         _check(_L.tp_ctx_set_k2_mode(self.handle, int(mode)), "tp_ctx_set_k2_mode")
+
+    def set_search(self, search):
+        """search: SEARCH_EXHAUSTIVE (reading A-13) or SEARCH_BINARY (the paper's P:555, A-24)."""
+        if isinstance(search, str):
+            search = {"exhaustive": SEARCH_EXHAUSTIVE, "binary": SEARCH_BINARY}[search]
+        _check(_L.tp_ctx_set_search(self.handle, int(search)), "tp_ctx_set_search")
 
     def buffers(self):
         ptrs = [_vp() for _ in range(5)]
