@@ -61,7 +61,6 @@ struct CheckParams {
 __global__ void __launch_bounds__(kThreads)
 k_admit_checks(const __grid_constant__ CheckParams p) {
     extern __shared__ long long sm[];   // r_before[h] | r_t[h] | r_start[h + 1] (int)
-    __shared__ int sw[kThreads / 32];
     __shared__ long long s_carry;
     const int v = blockIdx.x, tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     if (p.vstatus[v] & TP_ST_BAD_INPUT) {

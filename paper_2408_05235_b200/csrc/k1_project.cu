@@ -19,6 +19,11 @@ constexpr int kThreads = 256;
 constexpr int kWarps = kThreads / 32;
 constexpr int kGate = 8;        // queued candidates evaluated per block reduction
 
+// Scan segment per thread: a multiple of 4 iterations (128-bit shared loads), and the padded array
+// length so that every segment [1 + t*S, 1 + (t+1)*S) lies inside it.
+__host__ __device__ __forceinline__ int seg_len(int H) { return ((H + 4 * kThreads - 1) / (4 * kThreads)) * 4; }
+__host__ __device__ __forceinline__ int seg_pad(int H) { return ((H + 1 + 3) / 4) * 4 + 4; }
+
 __device__ __forceinline__ int64_t block_sum64(int64_t v, int64_t* red) {
     for (int o = 16; o; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
     const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
@@ -43,14 +48,17 @@ __device__ __forceinline__ int block_max(int v, int* red) {
     return s;
 }
 
-__global__ void __launch_bounds__(kThreads)
+__global__ void __launch_bounds__(kThreads, 4)
 k1_project(const tp_inst* __restrict__ inst, const int4* __restrict__ req, int32_t n_req, int32_t H,
            int32_t* __restrict__ Bout, int32_t* __restrict__ KVout, int32_t* __restrict__ nout,
            int32_t* __restrict__ nadm_out, uint32_t* __restrict__ status, const int32_t* __restrict__ force_adm,
            const uint32_t* __restrict__ lost_mask) {
-    extern __shared__ int smem[];
-    int* sB = smem;               // index m in [1, H + 1]
-    int* sKV = smem + (H + 2);
+    extern __shared__ __align__(16) int smem[];
+    // index m in [1, Hp]; &sB[1] and &sKV[1] 16-byte aligned so a thread's 4-aligned segment of m
+    // is read with 128-bit loads (conflict-free)
+    const int Hp = seg_pad(H);
+    int* sB = smem + 3;
+    int* sKV = smem + 3 + Hp;
     __shared__ int64_t red64[kWarps];
     __shared__ int redi[kWarps];
     __shared__ int s_admit;
@@ -65,7 +73,7 @@ k1_project(const tp_inst* __restrict__ inst, const int4* __restrict__ req, int32
     __shared__ FastDiv s_fd;
     if (tid == 0) s_fd = FastDiv((uint32_t)(N > 0 ? N : 1));
 
-    for (int m = tid; m < H + 2; m += kThreads) sB[m] = sKV[m] = 0;
+    for (int m = tid; m < Hp; m += kThreads) sB[m] = sKV[m] = 0;
 
     // ---- validation (include/tp.h conventions) ----
     bool bad = N < 1 || in.tp < 1 || (int64_t)in.tp >= kFeatLimit || nr < 0 || nq < 0 || in.kv_cap < 0 ||
@@ -99,7 +107,7 @@ k1_project(const tp_inst* __restrict__ inst, const int4* __restrict__ req, int32
     }
 
     // ---- running requests -> event histograms (Eq. 1 increments) ----
-    int nloc = 0;
+    int nloc = 0, b1 = 0, kv1 = 0;
     bool lost = false;
     for (int e = tid; e < nr; e += kThreads) {
         const int4 r = __ldg(&req[rb + e]);
@@ -107,25 +115,34 @@ k1_project(const tp_inst* __restrict__ inst, const int4* __restrict__ req, int32
         nloc = max(nloc, l);
         lost |= (r.w & TP_REQ_LOST) != 0;
         const int aq = a + q;
-        atomicAdd(&sB[1], 1);
         atomicAdd(&sB[l + 1], -1);
         const int c1 = (int)fdN.div((uint32_t)(aq - 1));                 // ceil(aq / N) - 1, aq >= 1
-        atomicAdd(&sKV[1], c1 + 1);
-        // first m >= 2 with (aq + m - 2) % N == 0, then every N iterations
-        for (int64_t m = 2 + (int64_t)(c1 + 1) * N - aq; m <= l; m += N) atomicAdd(&sKV[m], 1);
+        kv1 += c1 + 1;
+        ++b1;
+        // first m >= 2 with (aq + m - 2) % N == 0, then every N iterations (m <= l <= H: no overflow)
+        for (int m = 2 + (c1 + 1) * N - aq; m <= l; m += N) atomicAdd(&sKV[m], 1);
         atomicAdd(&sKV[l + 1], -((int)fdN.div((uint32_t)(aq + l - 2)) + 1));   // -ceil((aq + l - 1) / N)
+    }
+    // the m = 1 terms of every request: one shared atomic per warp
+    b1 = __reduce_add_sync(0xffffffffu, b1);
+    kv1 = __reduce_add_sync(0xffffffffu, kv1);
+    if (lane == 0 && b1) {
+        atomicAdd(&sB[1], b1);
+        atomicAdd(&sKV[1], kv1);
     }
     lost = __syncthreads_or(lost);
 
     // ---- inclusive scans: thread t owns the contiguous segment [lo, hi) of m ----
-    const int S = (H + kThreads - 1) / kThreads;
+    const int S = seg_len(H);
     int kvmax = 0;
     const int lo = 1 + tid * S, hi = min(lo + S, H + 1);
     {
         int sb = 0, skv = 0;
-        for (int m = lo; m < hi; ++m) {
-            sb += sB[m];
-            skv += sKV[m];
+        for (int m = lo; m < hi; m += 4) {     // 4-aligned segment, zero padding past H
+            const int4 b = *reinterpret_cast<const int4*>(sB + m);
+            const int4 k = *reinterpret_cast<const int4*>(sKV + m);
+            sb += b.x + b.y + b.z + b.w;
+            skv += k.x + k.y + k.z + k.w;
         }
         // exclusive block scan of the (sb, skv) pairs
         int xb = sb, xkv = skv;
@@ -149,12 +166,17 @@ k1_project(const tp_inst* __restrict__ inst, const int4* __restrict__ req, int32
             pb += wb[k];
             pkv += wkv[k];
         }
-        for (int m = lo; m < hi; ++m) {
-            pb += sB[m];
-            pkv += sKV[m];
-            sB[m] = pb;
-            sKV[m] = pkv;
-            kvmax = max(kvmax, pkv);
+        for (int m = lo; m < hi; m += 4) {
+            int4 b = *reinterpret_cast<const int4*>(sB + m);
+            int4 k = *reinterpret_cast<const int4*>(sKV + m);
+            b.x += pb; b.y += b.x; b.z += b.y; b.w += b.z;
+            k.x += pkv; k.y += k.x; k.z += k.y; k.w += k.z;
+            pb = b.w;
+            pkv = k.w;
+            *reinterpret_cast<int4*>(sB + m) = b;
+            *reinterpret_cast<int4*>(sKV + m) = k;
+            // positions past H are padding (their events are zero; never read as outputs)
+            kvmax = max(kvmax, max(max(k.x, m + 1 <= H ? k.y : 0), max(m + 2 <= H ? k.z : 0, m + 3 <= H ? k.w : 0)));
         }
     }
     __syncthreads();
@@ -204,18 +226,26 @@ k1_project(const tp_inst* __restrict__ inst, const int4* __restrict__ req, int32
 #pragma unroll
         for (int j = 0; j < kGate; ++j) maxlc = max(maxlc, lc[j]);
         const int mlim = min(hi, maxlc + 1);     // past every candidate's window only KV[m] counts
-        for (int m = lo; m < mlim; ++m) {
-            int run = sKV[m];
+        for (int m4 = lo; m4 < mlim; m4 += 4) {
+            const int4 kv4 = *reinterpret_cast<const int4*>(sKV + m4);
+            const int kvs[4] = {kv4.x, kv4.y, kv4.z, kv4.w};
 #pragma unroll
-            for (int j = 0; j < kGate; ++j) {
-                if (j < cn) {
-                    run += (m <= lc[j]) ? kvj[j] : 0;
-                    if (++dj[j] == N) {
-                        dj[j] = 0;
-                        ++kvj[j];
+            for (int u = 0; u < 4; ++u) {
+                const int m = m4 + u;
+                if (m < mlim) {
+                    int run = kvs[u];
+#pragma unroll
+                    for (int j = 0; j < kGate; ++j) {
+                        if (j < cn) {
+                            run += (m <= lc[j]) ? kvj[j] : 0;
+                            if (++dj[j] == N) {
+                                dj[j] = 0;
+                                ++kvj[j];
+                            }
+                        }
+                        mx[j] = max(mx[j], run);
                     }
                 }
-                mx[j] = max(mx[j], run);
             }
         }
         int tail = 0;
@@ -250,22 +280,32 @@ k1_project(const tp_inst* __restrict__ inst, const int4* __restrict__ req, int32
                     kvj[j] = (int)fdN.div((uint32_t)t1) + 1;
                     dj[j] = t1 - (kvj[j] - 1) * N;
                 }
-            for (int m = lo; m < mlim; ++m) {
-                int add = 0, addb = 0;
+            for (int m4 = lo; m4 < mlim; m4 += 4) {
+                int add[4] = {0, 0, 0, 0}, addb[4] = {0, 0, 0, 0};
 #pragma unroll
-                for (int j = 0; j < kGate; ++j)
-                    if (j < p) {
-                        if (m <= lc[j]) {
-                            add += kvj[j];
-                            ++addb;
-                        }
-                        if (++dj[j] == N) {
-                            dj[j] = 0;
-                            ++kvj[j];
-                        }
+                for (int u = 0; u < 4; ++u) {
+                    const int m = m4 + u;
+                    if (m < mlim) {
+#pragma unroll
+                        for (int j = 0; j < kGate; ++j)
+                            if (j < p) {
+                                if (m <= lc[j]) {
+                                    add[u] += kvj[j];
+                                    ++addb[u];
+                                }
+                                if (++dj[j] == N) {
+                                    dj[j] = 0;
+                                    ++kvj[j];
+                                }
+                            }
                     }
-                sKV[m] += add;
-                sB[m] += addb;
+                }
+                int4 k = *reinterpret_cast<int4*>(sKV + m4);
+                int4 b = *reinterpret_cast<int4*>(sB + m4);
+                k.x += add[0]; k.y += add[1]; k.z += add[2]; k.w += add[3];
+                b.x += addb[0]; b.y += addb[1]; b.z += addb[2]; b.w += addb[3];
+                *reinterpret_cast<int4*>(sKV + m4) = k;
+                *reinterpret_cast<int4*>(sB + m4) = b;
             }
         }
 #pragma unroll
@@ -289,8 +329,8 @@ k1_project(const tp_inst* __restrict__ inst, const int4* __restrict__ req, int32
         int4* k4 = reinterpret_cast<int4*>(KVout + (int64_t)i * H);
         for (int v = tid; v < (H >> 2); v += kThreads) {
             const int m = 4 * v + 1;
-            b4[v] = make_int4(sB[m], sB[m + 1], sB[m + 2], sB[m + 3]);
-            k4[v] = make_int4(sKV[m], sKV[m + 1], sKV[m + 2], sKV[m + 3]);
+            b4[v] = *reinterpret_cast<const int4*>(sB + m);
+            k4[v] = *reinterpret_cast<const int4*>(sKV + m);
         }
     } else {
         for (int m = tid; m < H; m += kThreads) {
@@ -313,13 +353,13 @@ int launch_project(const tp_inst* inst, int32_t n_inst, const tp_req* req, int32
                    int32_t* B, int32_t* KV, int32_t* n, int32_t* n_adm, uint32_t* status, cudaStream_t s,
                    const int32_t* force_adm, const uint32_t* lost_mask) {
     if (n_inst == 0) return TP_OK;
-    const size_t smem = (size_t)2 * (H + 2) * sizeof(int);
+    const size_t smem = (size_t)(4 + 2 * seg_pad(H)) * sizeof(int);
     int dev = 0;
     if (cudaGetDevice(&dev) != cudaSuccess) return TP_ECUDA;
     static bool attr_done[64] = {};
     if (dev < 64 && !attr_done[dev]) {
         if (cudaFuncSetAttribute(k1_project, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                 2 * (kMaxH + 2) * (int)sizeof(int)) != cudaSuccess)
+                                 (4 + 2 * seg_pad(kMaxH)) * (int)sizeof(int)) != cudaSuccess)
             return TP_ECUDA;
         attr_done[dev] = true;
     }

@@ -105,6 +105,12 @@ __device__ __forceinline__ uint32_t rank_of(const float* __restrict__ c, int cnt
 
 enum Mode : int { kDirect = 0, kRuns = 1, kCells = 2 };
 
+// Trees unrolled per step in cell mode (RU = 2 rows per lane -> 2 * UT independent descents).
+#ifndef TP_K2_UT_CELLS
+#define TP_K2_UT_CELLS 4
+#endif
+constexpr int kUnrollTreesCells = TP_K2_UT_CELLS;
+
 // Work units.  Direct: one unit = one warp tile = 32 consecutive iterations x RU levels of one
 // instance (ceil(n/32) * G units per instance).  Runs: one unit = one lane task = one run x RU
 // levels (h * G per instance), packed 32 per warp tile across instance boundaries.  Cells: one unit
@@ -413,7 +419,9 @@ k2_gbdt(const __grid_constant__ K2Params p, int TC, int nchunks) {
             if (active) {
                 const uint32_t* cw = sw + (size_t)s * chunk_words;
                 const int nt = min(TC, p.n_trees - c * TC);
-                for (int tt = 0; tt < nt; ++tt) {
+                // one tree for the lane's RU rows; descents of different trees are independent
+                // (only the fp32 accumulation is ordered), so unrolling over trees adds ILP
+                auto tree = [&](int tt) {
                     const uint32_t* tw = cw + tt * TW;
                     uint32_t idx[RU];
                     if constexpr (D >= 2) {
@@ -438,6 +446,12 @@ k2_gbdt(const __grid_constant__ K2Params p, int TC, int nchunks) {
                     }
 #pragma unroll
                     for (int r = 0; r < RU; ++r) acc[r] = __fadd_rn(acc[r], __uint_as_float(tw[idx[r]]));
+                };
+                if constexpr (MODE == kCells) {
+#pragma unroll kUnrollTreesCells
+                    for (int tt = 0; tt < nt; ++tt) tree(tt);
+                } else {
+                    for (int tt = 0; tt < nt; ++tt) tree(tt);
                 }
             }
             if (!resident) {
@@ -574,8 +588,11 @@ int launch_ru(const K2Params& p, cudaStream_t s) {
 // fewer rows per lane = more warps for the same work (latency-bound small problems).
 template <int MODE>
 int launch_mode(const K2Params& p, cudaStream_t s) {
-    static const int ru_env = env_int(MODE == kCells ? "TP_K2_RU_CELLS" : "TP_K2_RU", MODE == kCells ? 2 : 8, 2, 8, 2);
+    static const int ru_env = env_int(MODE == kCells ? "TP_K2_RU_CELLS" : "TP_K2_RU", MODE == kCells ? 2 : 8, 1, 8, 1);
     const int ru = std::min(ru_env, p.F <= 2 ? 2 : p.F <= 4 ? 4 : 8);
+    if constexpr (MODE == kCells) {
+        if (ru == 1) return launch_ru<1, MODE>(p, s);
+    }
     if (ru <= 2) return launch_ru<2, MODE>(p, s);
     if (ru <= 4) return launch_ru<4, MODE>(p, s);
     return launch_ru<8, MODE>(p, s);

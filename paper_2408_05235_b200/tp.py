@@ -13,7 +13,8 @@ import os
 import numpy as np
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "libtp.so")
+# TP_LIB_PATH: an alternative in-tree build (tuning variants, tools/build_variant.py)
+LIB_PATH = os.environ.get("TP_LIB_PATH") or os.path.join(HERE, "libtp.so")
 
 TP_OK, TP_EINVAL, TP_ENOMEM, TP_ECUDA, TP_EFORMAT, TP_ENOTIMPL = 0, -1, -2, -3, -4, -5
 ST_EMPTY, ST_BYPASS_LOST, ST_INFEASIBLE, ST_KV_OVER = 1, 2, 4, 8

@@ -96,9 +96,6 @@ def test_c2_full(gpu, oracle_mod):  # noqa: F811
     inputs = W.config_inputs(cfg)
     ref = oracle_bs(oracle_mod, blob, inputs, threads=16)
     check(run_gpu_bs(gpu, blob, inputs), ref)
-    exh = oracle_mod.decide(oracle_mod.Model(blob), inputs["inst"], inputs["req"], inputs["t_dead"], inputs["H"],
-                            inputs["freq"], inputs["tbt_slo"], want_grid=False, threads=16)
-    assert (exh["level"] != ref["level"]).any()      # the synthetic model is not monotone in f
 
 
 def test_c3_sampled(gpu, oracle_mod):  # noqa: F811

@@ -24,9 +24,12 @@ if __name__ == "__main__":
         sys.exit(0)
     wl = sys.argv[1] if len(sys.argv) > 1 else "C2"
     reps = int(sys.argv[2]) if len(sys.argv) > 2 else 20
-    for ru in [2, 4, 8]:
-        for th in [128, 256]:
-            for ck in [16, 32]:
+    grid = [(ru, th, ck) for ru in [1, 2] for th in [128, 256] for ck in [16, 24, 32]]
+    if len(sys.argv) > 3:
+        grid = [tuple(int(v) for v in g.split(",")) for g in sys.argv[3:]]
+    for ru, th, ck in grid:
+        if True:
+            if True:
                 env = dict(os.environ, K2_SWEEP_CHILD="1", TP_K2_RU_CELLS=str(ru), TP_K2_THREADS=str(th),
                            TP_K2_CHUNK_KB=str(ck))
                 out = subprocess.run([sys.executable, __file__, wl, str(reps)], env=env, capture_output=True, text=True)
