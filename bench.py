@@ -254,9 +254,10 @@ def main():
     ap.add_argument("--search", default="exhaustive", choices=["exhaustive", "binary"],
                     help="K3 order: lowest passing level over all levels (reading A-13, default) or the "
                          "paper's binary search (P:555, reading A-24; needs --k2 fused)")
-    ap.add_argument("--k2", default="fused", choices=["fused", "cells", "runs", "direct"],
-                    help="K2 variant: cell-memoised fused with K3 (default), cell-memoised with the ips grid, "
-                         "run-compressed, or one evaluation per grid point")
+    ap.add_argument("--k2", default="compact", choices=["compact", "fused", "cells", "runs", "direct"],
+                    help="path: compact (K1c runs + deadline list -> K2 on the cells -> K3c, default), "
+                         "cell-memoised fused with K3, cell-memoised with the ips grid, run-compressed, or "
+                         "one evaluation per grid point")
     args = ap.parse_args()
     cfg = W.CONFIGS[args.workload]
     if args.impl == "reference":
@@ -306,6 +307,7 @@ def main():
     model = tp.Gbdt(blob, local)
     info = model.info()
     rnd = runner.Round(inputs, dev, k2_mode=args.k2, model=model, search=args.search)
+    rnd.bkv = False          # compact path: the B/KV curves stay on chip
     dec = torch.empty((2, max(I, 1)), dtype=torch.int32, device=dev)   # level, status rows
     rnd.level, rnd.status = dec[0], dec[1]
     # equal shards (C2 weak, C5 = 262144 / {1,2,4,8}): one preallocated all-gather of [2, I] rows
@@ -347,6 +349,7 @@ def main():
     evaluated = {"runs": lambda: tp.runs_total(rnd.work, I, rnd.H) * rnd.F,
                  "cells": lambda: tp.cells_total(rnd.work, model, I, rnd.H, rnd.F) * rnd.F,
                  "fused": lambda: tp.cells_total(rnd.work, model, I, rnd.H, rnd.F) * rnd.F,
+                 "compact": lambda: tp.cells_total(rnd.work, model, I, rnd.H, rnd.F) * rnd.F,
                  "direct": lambda: grid}[args.k2]()
 
     evs = [[torch.cuda.Event(enable_timing=True) for _ in range(5)] for _ in range(args.steps)]
@@ -396,8 +399,8 @@ def main():
     # end to end through the C ABI with host buffers (pinned), copies inside the timed region
     e2e = None
     if True:
-        ctx = tp.Ctx(local, I, R, rnd.H, rnd.F, model if args.k2 in ("cells", "fused") else None)
-        ctx.set_k2_mode(tp.K2_DIRECT if args.k2 == "direct" else tp.K2_RUNS)
+        ctx = tp.Ctx(local, I, R, rnd.H, rnd.F, model if args.k2 in ("cells", "fused", "compact") else None)
+        ctx.set_k2_mode({"direct": tp.K2_DIRECT, "compact": tp.K2_COMPACT}.get(args.k2, tp.K2_RUNS))
         ctx.set_search(args.search)
         h_inst = torch.from_numpy(inputs["inst"].view(np.uint8)).pin_memory()
         h_req = torch.from_numpy(inputs["req"].view(np.uint8)).pin_memory()
@@ -449,7 +452,8 @@ def main():
         pass
     roof = {"bound": "smem", "kernel": {"direct": "k2_gbdt", "runs": "k2_gbdt<runs> (+ k2_runs pre-pass)",
                                         "cells": "k2_gbdt<cells> (+ k2_runs pre-pass, k2_expand)",
-                                        "fused": "k2_gbdt<cells> (+ k2_runs pre-pass)"}[args.k2],
+                                        "fused": "k2_gbdt<cells> (+ k2_runs pre-pass)",
+                                        "compact": "k2_gbdt<cells> (runs built by K1c)"}[args.k2],
             "achieved": achieved, "peak": peak, "unit": "GB/s",
             "frac": achieved / peak, "traffic": traffic,
             "peak_basis": f"{sms} SMs x 128 B/clk (LDS) x sm_max_mhz {smax:.0f} (MEASURED_PEAKS.json clock)",
@@ -479,8 +483,8 @@ def main():
         "roofline": roof,
         "cpu_baseline": cpu,
         "e2e": e2e,
-        # our kernels per step: k1_project, [k2_runs], k2_gbdt, [k2_expand], k3_select*
-        "gpu_launches": {"direct": 3, "runs": 4, "cells": 5, "fused": 4}[args.k2] * args.steps,
+        # our kernels per step: k1_project / k1_compact, [k2_runs], k2_gbdt, [k2_expand], k3_select* / k3_compact
+        "gpu_launches": {"direct": 3, "runs": 4, "cells": 5, "fused": 4, "compact": 3}[args.k2] * args.steps,
         "clocks": clk,
         "paper_context": "paper controller on host CPU (A100 box): projection <2 ms, model ~3 ms per call, "
                          "scheduler+throttle 35 ms per decision (P:466, P:495, P:557)",

@@ -241,6 +241,40 @@ int tp_select_freq_binary(const tp_gbdt* m, const void* workspace, const tp_inst
                           uint32_t* status, void* stream);
 
 /*
+ * The compact path ("fused round"): the same decisions as K1 -> K2 -> K3 above, bit
+ * for bit, with the per-iteration curves kept on chip.  Three kernels on one cell-mode workspace
+ * (tp_predict_ips_workspace_size(m, n_inst, H, F) bytes; the model's cell space must be <= 2^22):
+ *
+ * tp_project_compact -- K1c, one warp per instance: tp_project's projection + FIFO gate (same
+ *   n / n_adm / status outputs), then, for every instance not flagged BAD_INPUT / EMPTY /
+ *   BYPASS_LOST, (a) the runs of consecutive iterations m <= n in one cell (rank_tp, rank_B[m],
+ *   rank_KV[m]) of the ensemble's thresholds, first-seen cells claimed in the workspace's cell
+ *   table, and (b) the deadline list of Eq. 4: for each end position l of a scheduled
+ *   (running or admitted) request, Dmin[l] = min ceil(fl64(t_dead - t_cur) * 2^40) (reading A-12).
+ *   B / KV [dev] optional (both NULL or both set): full [n_inst][H] rows as tp_project if
+ *   bkv_rows = 1, only the m = 1 column (B[i*H], KV[i*H]) if bkv_rows = 0.
+ *   t_dead [dev] fp64 seconds per request entry (as tp_select_freq).  H <= ~12000 (per-warp shared
+ *   histograms; larger H -> TP_EINVAL).
+ * tp_predict_cells -- K2 on the claimed cells: LUT[cell][u] = clamp(M(cell, freq_mhz[u])) (as
+ *   tp_predict_ips_runs in cell mode; no pre-pass: the runs come from tp_project_compact).
+ * tp_select_freq_compact -- K3c, one warp per instance, lane u = level u: T_R formed run by run
+ *   from the LUT (exact ticks), Eq. 4 checked at the deadline list, TBT at m = n; level = lowest
+ *   passing level (search = TP_SEARCH_EXHAUSTIVE, reading A-13) or the paper's binary search on the
+ *   pass bits (TP_SEARCH_BINARY, reading A-24; IPS_CLAMPED then covers the visited levels only).
+ *   Outputs and the BAD_INPUT / EMPTY / BYPASS_LOST / INFEASIBLE rules: as tp_select_freq.
+ * All three: asynchronous on `stream`; TP_EINVAL on bad arguments or a too-small workspace.
+ */
+int tp_project_compact(const tp_gbdt* m, void* workspace, size_t workspace_bytes, const tp_inst* inst,
+                       int32_t n_inst, const tp_req* req, int32_t n_req, const double* t_dead, int32_t H,
+                       int32_t* B, int32_t* KV, int32_t bkv_rows, int32_t* n, int32_t* n_adm,
+                       uint32_t* status, void* stream);
+int tp_predict_cells(const tp_gbdt* m, void* workspace, size_t workspace_bytes, int32_t n_inst, int32_t H,
+                     const float* freq_mhz, int32_t F, void* stream);
+int tp_select_freq_compact(const tp_gbdt* m, const void* workspace, size_t workspace_bytes, int32_t n_inst,
+                           const int32_t* n, int32_t H, int32_t F, float tbt_slo, int32_t search,
+                           int32_t* level, uint32_t* status, void* stream);
+
+/*
  * Convenience: one decision round with library-owned scratch.
  * tp_ctx_create allocates, on `device`, B/KV/n/n_adm (n_inst_max x H), the ips grid
  * (n_inst_max x F_max x H), the K2 workspace (sized for `model`'s cell mode; NULL = run mode)
@@ -251,9 +285,12 @@ int tp_ctx_create(int device, const tp_gbdt* model, int32_t n_inst_max, int32_t 
                   int32_t F_max, tp_ctx** out);
 int tp_ctx_free(tp_ctx* c);
 
-/* K1 -> K2 -> K3 on device-resident inputs; level/status [dev] out.  With TP_K2_RUNS (default) and a
+/* K1 -> K2 -> K3 on device-resident inputs; level/status [dev] out.  With TP_K2_COMPACT (the default
+ * for a context created for `m`) the compact path runs: tp_project_compact (B/KV: m = 1 column only)
+ * -> tp_predict_cells -> tp_select_freq_compact.  With TP_K2_RUNS (the default otherwise) and a
  * context created for `m`, K2 runs in cell mode without materialising the ips grid
- * (tp_predict_ips_runs with ips = NULL, then tp_select_freq_ws). */
+ * (tp_predict_ips_runs with ips = NULL, then tp_select_freq_ws); without the model, run mode and
+ * tp_select_freq.  TP_K2_COMPACT without the context's model -> TP_ENOTIMPL. */
 int tp_decide(tp_ctx* c, const tp_gbdt* m, const tp_inst* inst, int32_t n_inst, const tp_req* req,
               int32_t n_req, const double* t_dead, const float* freq_mhz, int32_t F, float tbt_slo,
               int32_t* level, uint32_t* status, void* stream);
@@ -287,8 +324,9 @@ int tp_decide_admit(tp_ctx* c, const tp_gbdt* m, const tp_inst* inst, int32_t n_
                     int32_t* level, uint32_t* status, int32_t* n_adm_out, uint32_t* adm_lost_out,
                     void* stream);
 
-/* Which K2 variant tp_decide / tp_decide_host use (default TP_K2_RUNS). */
-enum { TP_K2_DIRECT = 0, TP_K2_RUNS = 1 };
+/* Which path tp_decide / tp_decide_host use (default TP_K2_COMPACT for a context created for a model
+ * with a cell mode, TP_K2_RUNS otherwise). */
+enum { TP_K2_DIRECT = 0, TP_K2_RUNS = 1, TP_K2_COMPACT = 2 };
 int tp_ctx_set_k2_mode(tp_ctx* c, int mode);
 
 /* K3 search order for tp_decide / tp_decide_host / tp_decide_admit (default exhaustive, reading
@@ -298,7 +336,8 @@ int tp_ctx_set_k2_mode(tp_ctx* c, int mode);
 enum { TP_SEARCH_EXHAUSTIVE = 0, TP_SEARCH_BINARY = 1 };
 int tp_ctx_set_search(tp_ctx* c, int search);
 
-/* Device pointers of the context's scratch (for inspection / tests); any out may be NULL. */
+/* Device pointers of the context's scratch (for inspection / tests); any out may be NULL.  After a
+ * TP_K2_COMPACT tp_decide only the m = 1 column of B / KV is written, and ips is not. */
 int tp_ctx_buffers(tp_ctx* c, int32_t** B, int32_t** KV, int32_t** n, int32_t** n_adm, float** ips);
 
 /*

@@ -19,14 +19,6 @@ namespace tp {
 namespace {
 
 constexpr int kThreads = 128;
-constexpr long long kNoDeadline = 0x7fffffffffffffffLL;
-
-__device__ __forceinline__ long long slack_ticks(double s) {
-    const double d = s * 0x1p40;
-    if (!(d > 0.0)) return 0;
-    if (d >= 0x1p62) return kNoDeadline;
-    return (long long)ceil(d);
-}
 
 __global__ void k_admit_expand(const tp_inst* __restrict__ inst, int32_t n_inst, int32_t qc,
                                const int32_t* __restrict__ n_adm1, const uint32_t* __restrict__ status1,

@@ -180,7 +180,7 @@ int tp_cells_total(const tp_gbdt* m, const void* workspace, int32_t n_inst, int3
     if (!p.cell_count || n_inst == 0) return TP_OK;
     int32_t c = 0;
     if (cudaMemcpy(&c, p.cell_count, 4, cudaMemcpyDeviceToHost) != cudaSuccess) return TP_ECUDA;
-    *total = c;
+    *total = (int64_t)c + 1;   // stored as count - 1
     return TP_OK;
 }
 
@@ -226,6 +226,76 @@ int tp_select_freq_binary(const tp_gbdt* m, const void* workspace, const tp_inst
                      TP_SEARCH_BINARY, stream);
 }
 
+static void fill_model(const tp_gbdt* m, tp::K2Params& p) {
+    p.words = m->m.d_words;
+    p.cuts = m->m.d_cuts;
+    for (int f = 0; f < 5; ++f) p.cut_off[f] = m->m.cut_off[f];
+    p.rtab = m->m.d_rtab;
+    for (int w = 0; w < 2; ++w) {
+        p.rtab_off[w] = m->m.rtab_off[w];
+        p.rtab_len[w] = m->m.rtab_len[w];
+    }
+    p.n_trees = m->m.n_trees;
+    p.depth = m->m.depth;
+    p.base = m->m.base;
+}
+
+static bool compact_ws_ok(const tp_gbdt* m, size_t bytes, int32_t n_inst, int32_t H, int32_t F) {
+    const int64_t cells = tp::model_cells(m->m);
+    return cells <= tp::kMaxCells && bytes >= tp::runs_workspace_bytes(cells, n_inst, H, F);
+}
+
+int tp_project_compact(const tp_gbdt* m, void* workspace, size_t workspace_bytes, const tp_inst* inst,
+                       int32_t n_inst, const tp_req* req, int32_t n_req, const double* t_dead, int32_t H, int32_t* B,
+                       int32_t* KV, int32_t bkv_rows, int32_t* n, int32_t* n_adm, uint32_t* status, void* stream) {
+    if (!m || n_inst < 0 || n_req < 0 || !H_ok(H) || (bkv_rows != 0 && bkv_rows != 1) || (!B) != (!KV))
+        return TP_EINVAL;
+    if (n_inst == 0) return TP_OK;
+    if (!workspace || !inst || !n || !n_adm || !status || (n_req > 0 && (!req || !t_dead)) ||
+        !compact_ws_ok(m, workspace_bytes, n_inst, H, 1))
+        return TP_EINVAL;
+    tp::K2Params p;
+    std::memset(&p, 0, sizeof(p));
+    fill_model(m, p);
+    tp::runs_workspace_carve(workspace, tp::model_cells(m->m), n_inst, H, 1, p);
+    return tp::launch_project_compact(p, inst, n_inst, req, n_req, t_dead, H, B, KV, bkv_rows, n, n_adm, status,
+                                      TP_ST_BAD_INPUT | TP_ST_EMPTY | TP_ST_BYPASS_LOST, S(stream));
+}
+
+int tp_predict_cells(const tp_gbdt* m, void* workspace, size_t workspace_bytes, int32_t n_inst, int32_t H,
+                     const float* freq_mhz, int32_t F, void* stream) {
+    if (!m || n_inst < 0 || !H_ok(H) || !freq_ok(freq_mhz, F)) return TP_EINVAL;
+    if (n_inst == 0) return TP_OK;
+    if (!workspace || !compact_ws_ok(m, workspace_bytes, n_inst, H, F)) return TP_EINVAL;
+    tp::K2Params p;
+    std::memset(&p, 0, sizeof(p));
+    fill_model(m, p);
+    p.n_inst = n_inst;
+    p.H = H;
+    p.F = F;
+    p.skip = TP_ST_BAD_INPUT | TP_ST_EMPTY | TP_ST_BYPASS_LOST;
+    p.runs_ready = 1;
+    for (int u = 0; u < F; ++u) p.freq[u] = freq_mhz[u];
+    tp::runs_workspace_carve(workspace, tp::model_cells(m->m), n_inst, H, F, p);
+    return tp::launch_gbdt(p, true, S(stream));
+}
+
+int tp_select_freq_compact(const tp_gbdt* m, const void* workspace, size_t workspace_bytes, int32_t n_inst,
+                           const int32_t* n, int32_t H, int32_t F, float tbt_slo, int32_t search, int32_t* level,
+                           uint32_t* status, void* stream) {
+    if (!m || n_inst < 0 || !H_ok(H) || F < 1 || F > tp::kMaxF || !tbt_ok(tbt_slo) ||
+        (search != TP_SEARCH_EXHAUSTIVE && search != TP_SEARCH_BINARY))
+        return TP_EINVAL;
+    if (n_inst == 0) return TP_OK;
+    if (!workspace || !n || !level || !status || !compact_ws_ok(m, workspace_bytes, n_inst, H, F)) return TP_EINVAL;
+    tp::K2Params p;
+    std::memset(&p, 0, sizeof(p));
+    tp::runs_workspace_carve(const_cast<void*>(workspace), tp::model_cells(m->m), n_inst, H, F, p);
+    const int64_t tbt_ticks = (int64_t)((double)tbt_slo * 0x1p40);   // exact: tbt_slo >= 2^-17
+    return tp::launch_select_compact(p, n_inst, n, H, F, tbt_ticks, search,
+                                     TP_ST_BAD_INPUT | TP_ST_EMPTY | TP_ST_BYPASS_LOST, level, status, S(stream));
+}
+
 int tp_replay_advance(const tp_gbdt* m, tp_inst* inst, int32_t n_inst, const tp_req* req, const double* t_dead,
                       tp_req* req_out, double* t_dead_out, int32_t slot_cap, int32_t H, const int32_t* B,
                       const int32_t* KV, const int32_t* n, const int32_t* n_adm, const uint32_t* status,
@@ -253,8 +323,8 @@ int tp_ctx_create(int device, const tp_gbdt* model, int32_t n_inst_max, int32_t 
     c->n_req_max = n_req_max;
     c->H = H;
     c->F_max = F_max;
-    c->k2_mode = TP_K2_RUNS;
     c->cells_model = (model && tp::model_cells(model->m) <= tp::kMaxCells) ? model : nullptr;
+    c->k2_mode = c->cells_model ? TP_K2_COMPACT : TP_K2_RUNS;
     int prev = 0;
     cudaGetDevice(&prev);
     if (cudaSetDevice(device) != cudaSuccess) {
@@ -359,7 +429,7 @@ int tp_decide_admit(tp_ctx* c, const tp_gbdt* m, const tp_inst* inst, int32_t n_
 }
 
 int tp_ctx_set_k2_mode(tp_ctx* c, int mode) {
-    if (!c || (mode != TP_K2_DIRECT && mode != TP_K2_RUNS)) return TP_EINVAL;
+    if (!c || (mode != TP_K2_DIRECT && mode != TP_K2_RUNS && mode != TP_K2_COMPACT)) return TP_EINVAL;
     c->k2_mode = mode;
     return TP_OK;
 }
@@ -386,9 +456,20 @@ int tp_decide(tp_ctx* c, const tp_gbdt* m, const tp_inst* inst, int32_t n_inst, 
     if (!c || !m || n_inst < 0 || n_inst > c->n_inst_max || F > c->F_max || !freq_ok(freq_mhz, F) ||
         !tbt_ok(tbt_slo))
         return TP_EINVAL;
+    const bool cells = c->k2_mode != TP_K2_DIRECT && c->cells_model == m && m != nullptr;
+    if (c->k2_mode == TP_K2_COMPACT) {
+        // K1c -> K2 (cells) -> K3c: B/KV stay on chip (only m = 1 is written, for tp_replay_advance)
+        if (!cells) return TP_ENOTIMPL;
+        int rc = tp_project_compact(m, c->work, c->work_bytes, inst, n_inst, req, n_req, t_dead, c->H, c->B, c->KV,
+                                    0, c->n, c->n_adm, status, stream);
+        if (!rc) rc = tp_predict_cells(m, c->work, c->work_bytes, n_inst, c->H, freq_mhz, F, stream);
+        if (!rc) rc = tp_select_freq_compact(m, c->work, c->work_bytes, n_inst, c->n, c->H, F, tbt_slo, c->search,
+                                             level, status, stream);
+        return rc;
+    }
     // cell mode (ctx created with the model): K2 leaves the IPS values in the LUT and K3 reads them
     // through the runs -- the ips grid is never materialised
-    const bool fused = c->k2_mode == TP_K2_RUNS && c->cells_model == m && m != nullptr && c->H <= tp::kMaxHRunsSelect;
+    const bool fused = c->k2_mode == TP_K2_RUNS && cells && c->H <= tp::kMaxHRunsSelect;
     if (c->search == TP_SEARCH_BINARY && !fused) return TP_ENOTIMPL;   // binary search reads the cell LUT
     int rc = tp_project(inst, n_inst, req, n_req, c->H, c->B, c->KV, c->n, c->n_adm, status, stream);
     if (rc) return rc;

@@ -1,0 +1,435 @@
+// K1c -- the compact path's first kernel: KV usage & batch-size projection (PAPER §4.2, Eq. 1-2,
+// P:432-469) with the FIFO admission gate (check 1 + batch cap, §4.3.2, one request at a
+// time P:755), fused with what the two later kernels need from it:
+//   * run compression + cell claims (what k2_runs does from the B/KV rows): M depends on m only
+//     through the cell (rank_tp, rank_B[m], rank_KV[m]) of the grid row (reading A-7), so
+//     consecutive iterations in one cell form a run; first-seen cells are appended to the cell list
+//     K2 evaluates;
+//   * the deadline list of Eq. 4: Dmin[l] = min over the scheduled requests ending at
+//     l of ceil(fl64(t_dead - t_cur) * 2^40) (reading A-12), compacted to the end positions that
+//     carry one, ascending.
+// The B/KV curves never leave the SM unless the caller asks for them (bkv_rows).
+//
+// One WARP per instance (the CTA-per-instance K1 spends most of its issue slots on block-wide
+// phases and barriers at large batches): the events go to a per-warp shared histogram, the scans
+// and the gate use warp shuffles only (no __syncthreads anywhere).  Lane t owns the contiguous
+// segment m in [1 + t*S, 1 + (t+1)*S) (S a power of two >= 4); segments are padded by P = 4 words
+// when S/4 is even so that 8 consecutive lanes' 128-bit accesses fall in distinct bank quads.
+#include <algorithm>
+
+#include "tp_internal.cuh"
+
+namespace tp {
+namespace {
+
+constexpr int kWarpsPerCta = 4;
+constexpr unsigned kFull = 0xffffffffu;
+
+struct SegGeom {
+    int S_log2, P, arr;         // segment length 2^S_log2, pad words, ints per array
+};
+
+SegGeom seg_geom(int H) {
+    const int need = (H + 31) / 32;
+    int S = 4, l = 2;
+    while (S < need) {
+        S <<= 1;
+        ++l;
+    }
+    const int P = ((S / 4) % 2 == 0) ? 4 : 0;
+    return {l, P, 32 * (S + P) + 8};
+}
+
+struct K1cParams {
+    const tp_inst* inst;
+    const int4* req;
+    const double* t_dead;
+    int32_t n_inst, n_req, H;
+    int32_t* B;
+    int32_t* KV;
+    int32_t bkv_rows;
+    int32_t* n;
+    int32_t* n_adm;
+    uint32_t* status;
+    const int32_t* force_adm;
+    const uint32_t* lost_mask;
+    uint32_t skip;
+    int32_t S_log2, P, arr;
+    const float* cuts;
+    int32_t cut_off[5];
+    const uint16_t* rtab;
+    int32_t rtab_off[2], rtab_len[2];
+    int32_t* run_h;
+    int32_t* run_m;
+    uint32_t* run_key;
+    int32_t* cell_tab;
+    uint32_t* cell_list;
+    int32_t* cell_count;
+    uint32_t* cell_clamp;
+    int32_t* end_n;
+    int32_t* end_l;
+    long long* end_d;
+};
+
+__device__ __forceinline__ uint32_t rank_of(const float* __restrict__ c, int cnt, float x) {
+    int lo = 0, hi = cnt;   // number of cuts <= x
+    while (lo < hi) {
+        const int mid = (lo + hi) >> 1;
+        if (__ldg(c + mid) <= x) lo = mid + 1;
+        else hi = mid;
+    }
+    return (uint32_t)lo;
+}
+
+__device__ __forceinline__ int warp_max(int v) { return __reduce_max_sync(kFull, v); }
+
+__global__ void __launch_bounds__(kWarpsPerCta * 32)
+k1_compact(const __grid_constant__ K1cParams p) {
+    extern __shared__ __align__(16) int smem[];
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    const int i = blockIdx.x * (int)(blockDim.x >> 5) + w;
+    if (i >= p.n_inst) return;                        // warp-uniform
+    int* sB = smem + (size_t)w * 2 * p.arr;
+    int* sKV = sB + p.arr;
+    const int SL = p.S_log2, S = 1 << SL, P = p.P, H = p.H;
+    auto ph = [&](int m) { return (m - 1) + P * ((m - 1) >> SL); };   // physical index of m >= 1
+
+    const tp_inst in = p.inst[i];
+    const int64_t rb = in.req_begin;
+    const int nr = in.n_run, nq = in.n_queue, N = in.N;
+    const FastDiv fdN((uint32_t)(N > 0 ? N : 1));
+    for (int k = lane * 4; k + 3 < p.arr; k += 128) {
+        *reinterpret_cast<int4*>(sB + k) = make_int4(0, 0, 0, 0);
+        *reinterpret_cast<int4*>(sKV + k) = make_int4(0, 0, 0, 0);
+    }
+    __syncwarp();
+
+    // ---- validation (include/tp.h conventions) + running requests -> event histograms ----
+    bool bad = N < 1 || in.tp < 1 || (int64_t)in.tp >= kFeatLimit || nr < 0 || nq < 0 || in.kv_cap < 0 ||
+               in.max_batch < 0 || rb < 0 || rb + (int64_t)nr + nq > (int64_t)p.n_req;
+    int64_t foot = 0;
+    int nloc = 0, b1 = 0, kv1 = 0;
+    bool lost = false;
+    if (!bad) {
+        for (int e = lane; e < nr + nq; e += 32) {
+            const int4 r = __ldg(&p.req[rb + e]);
+            const int64_t l64 = (int64_t)r.z - r.x;
+            const bool eb = r.x < 0 || r.y < 1 || r.z < 1 || r.x >= kFeatLimit || r.y >= kFeatLimit || l64 < 1 ||
+                            l64 > H || (e >= nr && r.x != 0);
+            bad |= eb;
+            if (eb) continue;
+            const int a = r.x, q = r.y, l = (int)l64, aq = a + q;
+            foot += (int64_t)fdN.div((uint32_t)(aq + l - 2)) + 1;            // ceil((a+l-1+q)/N)
+            if (e < nr) {
+                nloc = max(nloc, l);
+                lost |= (r.w & TP_REQ_LOST) != 0;
+                atomicAdd(&sB[ph(l + 1)], -1);
+                const int c1 = (int)fdN.div((uint32_t)(aq - 1));              // ceil(aq / N) - 1
+                kv1 += c1 + 1;
+                ++b1;
+                // first m >= 2 with (aq + m - 2) % N == 0, then every N iterations
+                for (int m = 2 + (c1 + 1) * N - aq; m <= l; m += N) atomicAdd(&sKV[ph(m)], 1);
+                atomicAdd(&sKV[ph(l + 1)], -((int)fdN.div((uint32_t)(aq + l - 2)) + 1));
+            }
+        }
+    }
+    bad = __any_sync(kFull, bad);
+    if (!bad) {
+        for (int o = 16; o; o >>= 1) foot += __shfl_xor_sync(kFull, foot, o);
+        bad = foot >= kFeatLimit;
+    }
+    if (bad) {
+        if (p.B) {
+            const int lim = p.bkv_rows ? H : 1;
+            for (int m = lane; m < lim; m += 32) {
+                p.B[(int64_t)i * H + m] = 0;
+                p.KV[(int64_t)i * H + m] = 0;
+            }
+        }
+        if (lane == 0) {
+            p.n[i] = 0;
+            p.n_adm[i] = 0;
+            p.status[i] = TP_ST_BAD_INPUT;
+            if (p.run_h) p.run_h[i] = 0;
+            if (p.end_n) p.end_n[i] = 0;
+        }
+        return;
+    }
+    // the m = 1 terms of every running request (index ph(1) = 0 gets no other event)
+    b1 = __reduce_add_sync(kFull, b1);
+    kv1 = __reduce_add_sync(kFull, kv1);
+    lost = __any_sync(kFull, lost);
+    __syncwarp();
+    if (lane == 0) {
+        sB[0] += b1;
+        sKV[0] += kv1;
+    }
+    __syncwarp();
+
+    // ---- inclusive scans over the lane segments ----
+    int* segB = sB + lane * (S + P);
+    int* segKV = sKV + lane * (S + P);
+    const int lo = 1 + lane * S, hi = min(lo + S, H + 1);    // the lane's valid m (may be empty)
+    int kvmax = 0;
+    {
+        int sb = 0, skv = 0;
+        for (int k = 0; k < S; k += 4) {
+            const int4 b = *reinterpret_cast<const int4*>(segB + k);
+            const int4 v = *reinterpret_cast<const int4*>(segKV + k);
+            sb += b.x + b.y + b.z + b.w;
+            skv += v.x + v.y + v.z + v.w;
+        }
+        int xb = sb, xkv = skv;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const int yb = __shfl_up_sync(kFull, xb, o), ykv = __shfl_up_sync(kFull, xkv, o);
+            if (lane >= o) {
+                xb += yb;
+                xkv += ykv;
+            }
+        }
+        int pb = xb - sb, pkv = xkv - skv;
+        for (int k = 0; k < S; k += 4) {
+            int4 b = *reinterpret_cast<const int4*>(segB + k);
+            int4 v = *reinterpret_cast<const int4*>(segKV + k);
+            b.x += pb; b.y += b.x; b.z += b.y; b.w += b.z;
+            v.x += pkv; v.y += v.x; v.z += v.y; v.w += v.z;
+            pb = b.w;
+            pkv = v.w;
+            *reinterpret_cast<int4*>(segB + k) = b;
+            *reinterpret_cast<int4*>(segKV + k) = v;
+            const int m = lo + k;   // positions past H are padding (never outputs)
+            kvmax = max(kvmax, max(max(m <= H ? v.x : 0, m + 1 <= H ? v.y : 0),
+                                   max(m + 2 <= H ? v.z : 0, m + 3 <= H ? v.w : 0)));
+        }
+    }
+    __syncwarp();
+    uint32_t st = warp_max(kvmax) > in.kv_cap ? TP_ST_KV_OVER : 0u;
+
+    // ---- FIFO gate: queued c admitted iff B[1]+1 <= max_batch and max_m KV + KV_c <= kv_cap ----
+    // One candidate at a time, lane-strided over its window m = 1..l_c.  Only the window
+    // needs checking: if max_m KV[m] > kv_cap already (KV_OVER) every candidate fails, and every
+    // admission keeps max_m KV[m] <= kv_cap, so past l_c (where KV_c = 0) the check always holds.
+    int n_adm = 0;
+    const int forced = p.force_adm ? min(max(p.force_adm[i], 0), nq) : -1;
+    const uint32_t lmask = p.lost_mask ? p.lost_mask[i] : 0u;
+    const int ncand = forced >= 0 ? forced : nq;
+    if (forced < 0 && ncand > 0 && (st & TP_ST_KV_OVER)) {
+        st |= TP_ST_QUEUE_BLOCKED;
+    } else {
+        int B1 = sB[0];                                  // B[1] (uniform)
+        for (int c = 0; c < ncand; ++c) {
+            const int4 r = __ldg(&p.req[rb + nr + c]);  // a = 0 (validated)
+            const int q = r.y, lc = r.z;
+            if (forced < 0) {
+                bool admit = B1 + 1 <= in.max_batch;
+                if (admit) {
+                    int mx = 0;
+                    for (int m = 1 + lane; m <= lc; m += 32)   // Eq. 1: KV_c[m] = ceil((m - 1 + q) / N)
+                        mx = max(mx, sKV[ph(m)] + (int)fdN.div((uint32_t)(m + q - 2)) + 1);
+                    admit = warp_max(mx) <= in.kv_cap;
+                }
+                if (!admit) {
+                    st |= TP_ST_QUEUE_BLOCKED;
+                    break;
+                }
+            }
+            for (int m = 1 + lane; m <= lc; m += 32) {
+                const int pi = ph(m);
+                sKV[pi] += (int)fdN.div((uint32_t)(m + q - 2)) + 1;
+                sB[pi] += 1;
+            }
+            __syncwarp();
+            ++B1;
+            ++n_adm;
+            nloc = max(nloc, lc);
+            lost |= (r.w & TP_REQ_LOST) || (c < 32 && ((lmask >> c) & 1u));
+        }
+    }
+    if (forced >= 0 && forced < nq) st |= TP_ST_QUEUE_BLOCKED;
+    const int n = warp_max(nloc);
+    if (n == 0) st |= TP_ST_EMPTY;
+    else if (lost) st |= TP_ST_BYPASS_LOST;
+
+    if (p.B) {
+        int* Bo = p.B + (int64_t)i * H;
+        int* Ko = p.KV + (int64_t)i * H;
+        if (!p.bkv_rows) {
+            if (lane == 0) {
+                Bo[0] = sB[0];
+                Ko[0] = sKV[0];
+            }
+        } else if ((H & 3) == 0) {   // rows 16-byte aligned: 128-bit stores (groups never straddle)
+            for (int v = lane; v < (H >> 2); v += 32) {
+                const int m = 4 * v + 1;
+                reinterpret_cast<int4*>(Bo)[v] = *reinterpret_cast<const int4*>(sB + ph(m));
+                reinterpret_cast<int4*>(Ko)[v] = *reinterpret_cast<const int4*>(sKV + ph(m));
+            }
+        } else {
+            for (int m = 1 + lane; m <= H; m += 32) {
+                Bo[m - 1] = sB[ph(m)];
+                Ko[m - 1] = sKV[ph(m)];
+            }
+        }
+    }
+    if (lane == 0) {
+        p.n[i] = n;
+        p.n_adm[i] = n_adm;
+        p.status[i] = st;
+    }
+    const int nn = (st & p.skip) ? 0 : n;    // iterations K2 / K3 evaluate
+
+    // ---- runs of equal cells over m = 1..nn (lane segments), first-seen cells claimed ----
+    if (p.run_h) {
+        const int nB = p.cut_off[2] - p.cut_off[1], nKV = p.cut_off[3] - p.cut_off[2];
+        const int lB = p.rtab_len[0], lKV = p.rtab_len[1];
+        const uint16_t* tB = p.rtab + p.rtab_off[0];
+        const uint16_t* tKV = p.rtab + p.rtab_off[1];
+        const uint32_t rtp = rank_of(p.cuts + p.cut_off[0], p.cut_off[1] - p.cut_off[0], (float)in.tp);
+        const uint32_t nk1 = (uint32_t)nKV + 1;
+        const uint32_t cell_base = rtp * (uint32_t)(nB + 1) * nk1;
+        auto key_at = [&](int pidx) {
+            const int b = sB[pidx], kv = sKV[pidx];
+            const uint32_t rbk = b < lB ? __ldg(tB + b) : rank_of(p.cuts + p.cut_off[1], nB, (float)b);
+            const uint32_t rkv = kv < lKV ? __ldg(tKV + kv) : rank_of(p.cuts + p.cut_off[2], nKV, (float)kv);
+            return cell_base + rbk * nk1 + rkv;
+        };
+        // lane-strided over m: key, head flag (key != key of m - 1), ballot compaction; the heads
+        // (m, key) are staged in place at plain indices j < #heads so far, which never reach a
+        // position a later iteration still reads (ph(m) >= m - 1)
+        int h = 0;
+        uint32_t carry = 0xffffffffu;      // key of m0 - 1 (m = 1 always starts a run)
+        for (int m0 = 1; m0 <= nn; m0 += 32) {
+            const int m = m0 + lane;
+            const uint32_t k = m <= nn ? key_at(ph(m)) : 0u;
+            uint32_t pk = __shfl_up_sync(kFull, k, 1);
+            if (lane == 0) pk = carry;
+            carry = __shfl_sync(kFull, k, 31);
+            const bool head = m <= nn && k != pk;
+            const unsigned mask = __ballot_sync(kFull, head);
+            __syncwarp();                  // every lane has read its B / KV before the staging writes
+            if (head) {
+                const int pos = h + __popc(mask & ((1u << lane) - 1u));
+                sKV[pos] = m;
+                sB[pos] = (int)k;
+            }
+            h += __popc(mask);
+        }
+        __syncwarp();
+        // coalesced run records; claims lane-parallel (first claimant appends the cell)
+        const size_t row = (size_t)i * H;
+        for (int k = lane; k < h; k += 32) {
+            const int m = sKV[k];
+            const uint32_t key = (uint32_t)sB[k];
+            p.run_m[row + k] = m;
+            p.run_key[row + k] = key;
+            if (__ldcg(p.cell_tab + key) == -1 && atomicCAS(p.cell_tab + key, -1, -2) == -1) {
+                const int idx = atomicAdd(p.cell_count, 1) + 1;   // cell_count holds count - 1
+                p.cell_list[idx] = key;
+                p.cell_clamp[idx] = 0u;
+                p.cell_tab[key] = idx;
+            }
+        }
+        if (lane == 0) p.run_h[i] = h;
+    }
+
+    // ---- Eq. 4 deadline list: Dmin over end positions (the histogram space is reused) ----
+    if (p.end_n) {
+        __syncwarp();
+        long long* dmin = reinterpret_cast<long long*>(sB);     // [0, nn], 8 (H + 1) <= 8 arr bytes
+        for (int m = lane; m <= nn; m += 32) dmin[m] = kNoDeadline;
+        __syncwarp();
+        if (nn > 0) {
+            for (int e = lane; e < nr + n_adm; e += 32) {
+                const int64_t j = rb + e;
+                const int4 r = __ldg(&p.req[j]);
+                atomicMin(&dmin[r.z - r.x], slack_ticks(__ldg(&p.t_dead[j]) - in.t_cur));
+            }
+        }
+        __syncwarp();
+        int ne = 0;
+        const size_t row = (size_t)i * H;
+        for (int m0 = 1; m0 <= nn; m0 += 32) {
+            const int m = m0 + lane;
+            const long long d = m <= nn ? dmin[m] : kNoDeadline;
+            const bool has = d != kNoDeadline;
+            const unsigned mask = __ballot_sync(kFull, has);
+            if (has) {
+                const int pos = ne + __popc(mask & ((1u << lane) - 1u));
+                p.end_l[row + pos] = m;
+                p.end_d[row + pos] = d;
+            }
+            ne += __popc(mask);
+        }
+        if (lane == 0) p.end_n[i] = ne;
+    }
+}
+
+}  // namespace
+
+int project_compact_smem_per_warp(int32_t H) { return 2 * seg_geom(H).arr * (int)sizeof(int); }
+
+int launch_project_compact(const K2Params& w, const tp_inst* inst, int32_t n_inst, const tp_req* req,
+                           int32_t n_req, const double* t_dead, int32_t H, int32_t* B, int32_t* KV, int bkv_rows,
+                           int32_t* n, int32_t* n_adm, uint32_t* status, uint32_t skip, cudaStream_t s,
+                           const int32_t* force_adm, const uint32_t* lost_mask) {
+    if (n_inst == 0) return TP_OK;
+    if (!w.cell_tab || !w.end_n) return TP_EINVAL;
+    const SegGeom g = seg_geom(H);
+    K1cParams p;
+    p.inst = inst;
+    p.req = reinterpret_cast<const int4*>(req);
+    p.t_dead = t_dead;
+    p.n_inst = n_inst;
+    p.n_req = n_req;
+    p.H = H;
+    p.B = B;
+    p.KV = KV;
+    p.bkv_rows = bkv_rows;
+    p.n = n;
+    p.n_adm = n_adm;
+    p.status = status;
+    p.force_adm = force_adm;
+    p.lost_mask = lost_mask;
+    p.skip = skip;
+    p.S_log2 = g.S_log2;
+    p.P = g.P;
+    p.arr = g.arr;
+    p.cuts = w.cuts;
+    for (int k = 0; k < 5; ++k) p.cut_off[k] = w.cut_off[k];
+    p.rtab = w.rtab;
+    for (int k = 0; k < 2; ++k) {
+        p.rtab_off[k] = w.rtab_off[k];
+        p.rtab_len[k] = w.rtab_len[k];
+    }
+    p.run_h = w.run_h;
+    p.run_m = w.run_m;
+    p.run_key = w.run_key;
+    p.cell_tab = w.cell_tab;
+    p.cell_list = w.cell_list;
+    p.cell_count = w.cell_count;
+    p.cell_clamp = w.cell_clamp;
+    p.end_n = w.end_n;
+    p.end_l = w.end_l;
+    p.end_d = w.end_d;
+    // cell_count (count - 1) and cell_tab are contiguous: one reset; claimers zero their clamp masks
+    if (cudaMemsetAsync(w.cell_count, 0xFF, 4 + (size_t)w.n_cells * 4, s) != cudaSuccess) return TP_ECUDA;
+    // warps per CTA: up to kWarpsPerCta, fewer for long horizons (per-warp histograms)
+    const size_t per_warp = (size_t)2 * g.arr * sizeof(int);
+    if (per_warp > 200 * 1024) return TP_EINVAL;
+    const int wpb = (int)std::max<size_t>(1, std::min<size_t>(kWarpsPerCta, (100 * 1024) / per_warp));
+    const size_t smem = (size_t)wpb * per_warp;
+    int dev = 0;
+    if (cudaGetDevice(&dev) != cudaSuccess) return TP_ECUDA;
+    static int attr_bytes[64] = {};
+    if (dev < 64 && attr_bytes[dev] < (int)smem) {
+        if (cudaFuncSetAttribute(k1_compact, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess)
+            return TP_EINVAL;   // H too large for the per-warp histograms
+        attr_bytes[dev] = (int)smem;
+    }
+    const int grid = (n_inst + wpb - 1) / wpb;
+    k1_compact<<<grid, wpb * 32, smem, s>>>(p);
+    return cudaPeekAtLastError() == cudaSuccess ? TP_OK : TP_ECUDA;
+}
+
+}  // namespace tp

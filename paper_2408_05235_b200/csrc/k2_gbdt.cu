@@ -104,6 +104,7 @@ __device__ __forceinline__ uint32_t rank_of(const float* __restrict__ c, int cnt
 
 
 enum Mode : int { kDirect = 0, kRuns = 1, kCells = 2 };
+int env_int(const char* name, int dflt, int lo, int hi, int mult);
 
 // Trees unrolled per step in cell mode (RU = 2 rows per lane -> 2 * UT independent descents).
 #ifndef TP_K2_UT_CELLS
@@ -187,8 +188,9 @@ k2_runs(const __grid_constant__ K2Params p) {
             // first claimant of a cell appends it to the list; the LUT row index is published in
             // cell_tab after the claim and read only by later kernels
             if (cells && __ldcg(p.cell_tab + key) == -1 && atomicCAS(p.cell_tab + key, -1, -2) == -1) {
-                const int idx = atomicAdd(p.cell_count, 1);
+                const int idx = atomicAdd(p.cell_count, 1) + 1;   // cell_count holds count - 1
                 p.cell_list[idx] = key;
+                p.cell_clamp[idx] = 0u;
                 p.cell_tab[key] = idx;
             }
         }
@@ -268,7 +270,7 @@ k2_gbdt(const __grid_constant__ K2Params p, int TC, int nchunks) {
     int64_t U = 0;
     int ncell = 0;
     if constexpr (MODE == kCells) {
-        ncell = *p.cell_count;
+        ncell = *p.cell_count + 1;
         U = (int64_t)ncell * G;
     } else {
         for (int i = tid; i < I; i += nthreads) U += units_of<MODE>(p, i, G);
@@ -476,7 +478,10 @@ k2_gbdt(const __grid_constant__ K2Params p, int TC, int nchunks) {
                 if (cidx >= 0) {
 #pragma unroll
                     for (int r = 0; r < RU; ++r)
-                        if (u0 + r < p.F) p.lut[(size_t)cidx * p.F + u0 + r] = acc[r];
+                        if (u0 + r < p.F) {
+                            p.lut[(size_t)cidx * p.F + u0 + r] = acc[r];
+                            p.lut_ticks[(size_t)cidx * p.F + u0 + r] = ticks_of(acc[r]);
+                        }
                     if (cmask) atomicOr(p.cell_clamp + cidx, cmask);
                 }
             } else if constexpr (MODE == kRuns) {
@@ -498,6 +503,142 @@ k2_gbdt(const __grid_constant__ K2Params p, int TC, int nchunks) {
             }
         }
     }
+}
+
+// ---------------------------------------------------------------------------------------------
+// K2p (cell mode, tree-resident phases): the ensemble is cut into phases of consecutive trees that
+// fit in one SM's shared memory (<= ~200 KB); one launch per phase, one CTA per SM.  Each CTA
+// TMA-loads its phase once (one mbarrier per 8-tree chunk, so descents start as soon as the first
+// chunk lands; no buffer is ever reused, so no __syncthreads after the prologue) and evaluates its
+// contiguous share of the (cell, level-group) tasks for every tree of the phase.  The running fp32
+// sum of a row is carried from phase to phase in the LUT itself (the first phase starts from the
+// base score, the last one clamps, writes the tick LUT and the clamp masks), so every row's leaves
+// are still added one by one in tree order (reading A-7).
+constexpr int kPhaseChunkTrees = 8;
+constexpr int kMaxPhaseChunks = 64;
+constexpr int kPhaseThreads = 1024;
+
+template <int D, int RU>
+__global__ void __launch_bounds__(kPhaseThreads, 1)
+k2_cells_phase(const __grid_constant__ K2Params p, int t_begin, int t_count, int first, int last) {
+    extern __shared__ __align__(128) uint32_t sw[];
+    __shared__ __align__(8) uint64_t bar[kMaxPhaseChunks];
+    __shared__ uint32_t s_rf[kMaxF];
+    constexpr int TW = (2 << D) < 4 ? 4 : (2 << D);
+    const int tid = threadIdx.x;
+    const int G = (p.F + RU - 1) / RU;
+    const int ncell = *p.cell_count + 1;
+    const int64_t U = (int64_t)ncell * G;
+    const int64_t t0 = U * blockIdx.x / gridDim.x, t1 = U * (blockIdx.x + 1) / gridDim.x;
+    if (t0 >= t1) return;                      // uniform: no task, no TMA issued
+    const int nchunks = (t_count + kPhaseChunkTrees - 1) / kPhaseChunkTrees;
+    if (tid == 0) {
+        for (int c = 0; c < nchunks; ++c) mbar_init(&bar[c], 1);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+        for (int c = 0; c < nchunks; ++c) {
+            const int nt = min(kPhaseChunkTrees, t_count - c * kPhaseChunkTrees);
+            const uint32_t bytes = (uint32_t)nt * TW * 4u;
+            mbar_expect_tx(&bar[c], bytes);
+            tma_load(sw + (size_t)c * kPhaseChunkTrees * TW, p.words + (size_t)(t_begin + c * kPhaseChunkTrees) * TW,
+                     bytes, &bar[c]);
+        }
+    }
+    if (tid < p.F) s_rf[tid] = rank_of(p.cuts + p.cut_off[3], p.cut_off[4] - p.cut_off[3], p.freq[tid]);
+    __syncthreads();                           // barriers initialised, s_rf visible
+    const int nB = p.cut_off[2] - p.cut_off[1], nKV = p.cut_off[3] - p.cut_off[2];
+    const uint32_t nk1 = (uint32_t)nKV + 1, nb1 = (uint32_t)nB + 1;
+    for (int64_t task = t0 + tid; task < t1; task += blockDim.x) {
+        const int ug = (int)(task / ncell);
+        const int cidx = (int)(task - (int64_t)ug * ncell);
+        const int u0 = ug * RU;
+        const uint32_t c = p.cell_list[cidx];
+        const uint32_t rkv = c % nk1;
+        const uint32_t rb = (c / nk1) % nb1, rtp = c / (nk1 * nb1);
+        const uint32_t xlo = rtp | (rb << 16);
+        uint32_t xhi[RU];
+        float acc[RU];
+#pragma unroll
+        for (int r = 0; r < RU; ++r) {
+            const int u = min(u0 + r, p.F - 1);
+            xhi[r] = rkv | (s_rf[u] << 16);
+            acc[r] = first ? p.base : p.lut[(size_t)cidx * p.F + u];
+        }
+        for (int ch = 0; ch < nchunks; ++ch) {
+            mbar_wait(&bar[ch], 0u);
+            const uint32_t* cw = sw + (size_t)ch * kPhaseChunkTrees * TW;
+            const int nt = min(kPhaseChunkTrees, t_count - ch * kPhaseChunkTrees);
+            auto tree = [&](int tt) {
+                const uint32_t* tw = cw + tt * TW;
+                uint32_t idx[RU];
+                if constexpr (D >= 2) {
+                    const uint32_t w1 = tw[1];
+                    const uint2 w23 = *reinterpret_cast<const uint2*>(tw + 2);
+#pragma unroll
+                    for (int r = 0; r < RU; ++r) {
+                        const bool c0 = prmt(xlo, xhi[r], w1) > ~w1;
+                        idx[r] = step_from(c0 ? 6u : 4u, c0 ? w23.y : w23.x, xlo, xhi[r]);
+                    }
+                } else {
+#pragma unroll
+                    for (int r = 0; r < RU; ++r) idx[r] = 1u;
+                }
+#pragma unroll
+                for (int d = (D >= 2 ? 2 : 0); d < D; ++d) {
+#pragma unroll
+                    for (int r = 0; r < RU; ++r) idx[r] = descend(idx[r], tw[idx[r]], xlo, xhi[r]);
+                }
+#pragma unroll
+                for (int r = 0; r < RU; ++r) acc[r] = __fadd_rn(acc[r], __uint_as_float(tw[idx[r]]));
+            };
+            if (nt == kPhaseChunkTrees) {
+#pragma unroll
+                for (int tt = 0; tt < kPhaseChunkTrees; ++tt) tree(tt);
+            } else {
+                for (int tt = 0; tt < nt; ++tt) tree(tt);
+            }
+        }
+        if (last) {
+            uint32_t cmask = 0;
+#pragma unroll
+            for (int r = 0; r < RU; ++r) {
+                const float v = acc[r];
+                const float cl = isnan(v) ? 0x1p-4f : fminf(fmaxf(v, 0x1p-4f), 0x1p17f);
+                if (u0 + r < p.F) {
+                    if (isnan(v) || cl != v) cmask |= 1u << (u0 + r);
+                    p.lut[(size_t)cidx * p.F + u0 + r] = cl;
+                    if (p.lut_ticks) p.lut_ticks[(size_t)cidx * p.F + u0 + r] = ticks_of(cl);
+                }
+            }
+            if (cmask) atomicOr(p.cell_clamp + cidx, cmask);
+        } else {
+#pragma unroll
+            for (int r = 0; r < RU; ++r)
+                if (u0 + r < p.F) p.lut[(size_t)cidx * p.F + u0 + r] = acc[r];
+        }
+    }
+}
+
+template <int D, int RU>
+int launch_phases(const K2Params& p, cudaStream_t s) {
+    const int TW = (2 << D) < 4 ? 4 : (2 << D);
+    const int tree_bytes = TW * 4;
+    static const int budget = env_int("TP_K2_PHASE_KB", 200, 8, 220, 1) * 1024;
+    const int max_trees = std::max(1, std::min(budget / tree_bytes, kMaxPhaseChunks * kPhaseChunkTrees));
+    const int nphase = p.n_trees == 0 ? 1 : (p.n_trees + max_trees - 1) / max_trees;
+    const int per = p.n_trees == 0 ? 0 : (p.n_trees + nphase - 1) / nphase;   // balanced phases
+    const size_t smem = (size_t)std::max(per, 1) * tree_bytes;
+    auto kern = k2_cells_phase<D, RU>;
+    int dev = 0, sms = 0;
+    if (cudaGetDevice(&dev) != cudaSuccess) return TP_ECUDA;
+    if (cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess) return TP_ECUDA;
+    if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess)
+        return TP_ECUDA;
+    for (int ph = 0; ph < nphase; ++ph) {
+        const int tb = ph * per, tc = std::max(0, std::min(per, p.n_trees - tb));
+        kern<<<sms, kPhaseThreads, smem, s>>>(p, tb, tc, ph == 0, ph == nphase - 1);
+        if (cudaPeekAtLastError() != cudaSuccess) return TP_ECUDA;
+    }
+    return TP_OK;
 }
 
 // Tuning knobs (read once): TP_K2_THREADS (CTA size, multiple of 32), TP_K2_CHUNK_KB (tree chunk).
@@ -536,18 +677,22 @@ int launch_d(const K2Params& p, cudaStream_t s) {
     auto kern = k2_gbdt<D, RU, MODE>;
     int dev = 0, sms = 0, per_sm = 0;
     if (cudaGetDevice(&dev) != cudaSuccess) return TP_ECUDA;
-    if (MODE != kDirect) {
+    if (MODE != kDirect && !p.runs_ready) {
         static bool runs_attr[64] = {};
         if (!set_smem_attr((const void*)k2_runs, (kMaxH + 1) * 4, runs_attr, dev)) return TP_ECUDA;
         if (MODE == kCells) {
-            if (cudaMemsetAsync(p.cell_tab, 0xFF, (size_t)p.n_cells * 4, s) != cudaSuccess ||
-                cudaMemsetAsync(p.cell_count, 0, 4, s) != cudaSuccess ||
-                cudaMemsetAsync(p.cell_clamp, 0, (size_t)p.cell_cap * 4, s) != cudaSuccess)
+            if (cudaMemsetAsync(p.cell_count, 0xFF, 4 + (size_t)p.n_cells * 4, s) != cudaSuccess)   // + cell_tab
                 return TP_ECUDA;
         }
         k2_runs<<<p.n_inst, kRunsThreads, (size_t)(p.H + 1) * 4, s>>>(p);
         if (cudaPeekAtLastError() != cudaSuccess) return TP_ECUDA;
     }
+    static const bool chunked = env_int("TP_K2_CELLS_CHUNKED", 0, 0, 1, 1) == 1;
+    if (MODE == kCells && !chunked && RU <= 2) {
+        // tree-resident phases (the chunked kernel below stays selectable for comparisons)
+        const int rc = launch_phases<D, RU>(p, s);
+        if (rc != TP_OK) return rc;
+    } else {
     if (cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess) return TP_ECUDA;
     if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess)
         return TP_ECUDA;
@@ -555,6 +700,7 @@ int launch_d(const K2Params& p, cudaStream_t s) {
     const int grid = std::max(1, sms * std::max(1, per_sm));
     kern<<<grid, threads, smem, s>>>(p, TC, nchunks);
     if (cudaPeekAtLastError() != cudaSuccess) return TP_ECUDA;
+    }
     if (MODE == kCells && p.ips) {   // ips == NULL: values stay in the LUT (tp_select_freq_ws)
         static bool exp_attr[64] = {};
         if (!set_smem_attr((const void*)k2_expand, 2 * kMaxH * 4, exp_attr, dev)) return TP_ECUDA;
@@ -612,43 +758,60 @@ int64_t model_cells(const Model& m) {
     return (int64_t)(m.n_cuts[0] + 1) * (m.n_cuts[1] + 1) * (m.n_cuts[2] + 1);
 }
 
-// Workspace: run_h [I], run_m [I][H], run_key [I][H]; cell mode adds cell_tab [n_cells],
-// cell_list [cap], cell_count, cell_clamp [cap], lut [cap][F] with cap = min(n_cells, I * H).
-size_t runs_workspace_bytes(int64_t n_cells, int32_t n_inst, int32_t H, int32_t F) {
-    K2Params p{};
-    runs_workspace_carve(nullptr, n_cells, n_inst, H, F, p);
-    return (size_t)reinterpret_cast<uintptr_t>(p.lut ? (void*)(p.lut + (size_t)p.cell_cap * F) : (void*)(p.run_key + (size_t)(n_inst > 0 ? n_inst : 1) * H)) + 256;
-}
-
-void runs_workspace_carve(void* ws, int64_t n_cells, int32_t n_inst, int32_t H, int32_t F, K2Params& p) {
+// Workspace: run_h [I], run_m [I][H], run_key [I][H], end_n [I], end_l [I][H], end_d [I][H]
+// (compact path); cell mode adds cell_tab [n_cells], cell_list [cap], cell_count, cell_clamp [cap],
+// lut [cap][F] with cap = min(n_cells, I * H).  Returns the bytes used past `ws`.
+static size_t carve(void* ws, int64_t n_cells, int32_t n_inst, int32_t H, int32_t F, K2Params& p) {
     const size_t I = (size_t)(n_inst > 0 ? n_inst : 1);
-    uintptr_t a = align256((uintptr_t)ws);
+    const uintptr_t a0 = (uintptr_t)ws;
+    uintptr_t a = align256(a0);
     p.run_h = reinterpret_cast<int32_t*>(a);
     a = align256(a + I * 4);
     p.run_m = reinterpret_cast<int32_t*>(a);
     a = align256(a + I * (size_t)H * 4);
     p.run_key = reinterpret_cast<uint32_t*>(a);
     a = align256(a + I * (size_t)H * 4);
+    p.end_n = reinterpret_cast<int32_t*>(a);
+    a = align256(a + I * 4);
+    p.end_l = reinterpret_cast<int32_t*>(a);
+    a = align256(a + I * (size_t)H * 4);
+    p.end_d = reinterpret_cast<long long*>(a);
+    a = align256(a + I * (size_t)H * 8);
     p.cell_tab = nullptr;
     p.cell_list = nullptr;
     p.cell_count = nullptr;
     p.cell_clamp = nullptr;
     p.lut = nullptr;
+    p.lut_ticks = nullptr;
     p.n_cells = 0;
     p.cell_cap = 0;
-    if (n_cells <= 0 || n_cells > kMaxCells) return;
-    const int64_t cap = std::min<int64_t>(n_cells, (int64_t)I * H);
-    p.n_cells = (int32_t)n_cells;
-    p.cell_cap = (int32_t)cap;
-    p.cell_tab = reinterpret_cast<int32_t*>(a);
-    a = align256(a + (size_t)n_cells * 4);
-    p.cell_list = reinterpret_cast<uint32_t*>(a);
-    a = align256(a + (size_t)cap * 4);
-    p.cell_count = reinterpret_cast<int32_t*>(a);
-    a = align256(a + 4);
-    p.cell_clamp = reinterpret_cast<uint32_t*>(a);
-    a = align256(a + (size_t)cap * 4);
-    p.lut = reinterpret_cast<float*>(a);
+    if (n_cells > 0 && n_cells <= kMaxCells) {
+        const int64_t cap = std::min<int64_t>(n_cells, (int64_t)I * H);
+        p.n_cells = (int32_t)n_cells;
+        p.cell_cap = (int32_t)cap;
+        // cell_count (stored as count - 1) directly before cell_tab: one 0xFF memset resets both
+        p.cell_count = reinterpret_cast<int32_t*>(a);
+        p.cell_tab = reinterpret_cast<int32_t*>(a + 4);
+        a = align256(a + 4 + (size_t)n_cells * 4);
+        p.cell_list = reinterpret_cast<uint32_t*>(a);
+        a = align256(a + (size_t)cap * 4);
+        p.cell_clamp = reinterpret_cast<uint32_t*>(a);
+        a = align256(a + (size_t)cap * 4);
+        p.lut = reinterpret_cast<float*>(a);
+        a = align256(a + (size_t)cap * F * 4);
+        p.lut_ticks = reinterpret_cast<long long*>(a);
+        a = align256(a + (size_t)cap * F * 8);
+    }
+    return (size_t)(a - a0);
+}
+
+size_t runs_workspace_bytes(int64_t n_cells, int32_t n_inst, int32_t H, int32_t F) {
+    K2Params p{};
+    return carve(nullptr, n_cells, n_inst, H, F, p) + 256;
+}
+
+void runs_workspace_carve(void* ws, int64_t n_cells, int32_t n_inst, int32_t H, int32_t F, K2Params& p) {
+    carve(ws, n_cells, n_inst, H, F, p);
 }
 
 }  // namespace tp

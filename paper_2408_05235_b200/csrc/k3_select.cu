@@ -24,23 +24,6 @@ namespace {
 constexpr int kThreads = 256;
 constexpr int kWarps = kThreads / 32;
 constexpr uint32_t kSkip = TP_ST_BAD_INPUT | TP_ST_EMPTY | TP_ST_BYPASS_LOST;
-constexpr long long kNoDeadline = 0x7fffffffffffffffLL;
-
-// ceil(s * 2^40) for the E2E compare T_R < s (T_R integer ticks): <= 0 / NaN -> 0 (never passes),
-// >= 2^62 -> INT64_MAX (always passes; T_R < 2^58).
-__device__ __forceinline__ long long slack_ticks(double s) {
-    const double d = s * 0x1p40;
-    if (!(d > 0.0)) return 0;
-    if (d >= 0x1p62) return kNoDeadline;
-    return (long long)ceil(d);
-}
-
-// T' of one IPS value in ticks of 2^-40 s: fl32 reciprocal (reading A-9), exact scaling.
-__device__ __forceinline__ long long ticks_of(float ips) {
-    const float t = __frcp_rn(ips);
-    return (long long)(t * 0x1p40f);    // exact: t in [2^-17, 16]
-}
-
 // Per instance: dense Dmin table over m in [1, n] (shared memory).
 __device__ __forceinline__ void build_dmin(long long* dmin, const tp_inst& in, int n_sched, int n,
                                            const int4* __restrict__ req, const double* __restrict__ t_dead) {

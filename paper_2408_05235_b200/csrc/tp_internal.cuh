@@ -93,10 +93,19 @@ struct K2Params {
     // rank_KV) (and the level); distinct cells are evaluated once into a LUT, then expanded.
     int32_t* cell_tab;       // [n_cells] dense cell id -> LUT row (-1 = absent), or null
     uint32_t* cell_list;     // [cap] LUT row -> cell id
-    int32_t* cell_count;     // [1] distinct cells
+    int32_t* cell_count;     // [1] distinct cells - 1 (directly before cell_tab: one reset for both)
     float* lut;              // [cap][F] clamped IPS
+    long long* lut_ticks;    // [cap][F] T' = fl32(1 / ips) in ticks of 2^-40 s (readings A-9, A-10)
     uint32_t* cell_clamp;    // [cap] bit u set if level u's value was clamped
     int32_t n_cells, cell_cap;
+    // compact path (K1c -> K2 cells -> K3c): K1c already built the runs and claimed the cells, so
+    // the K2 launch skips its k2_runs pre-pass and the cell-table resets
+    int32_t runs_ready;
+    // compact path: per instance, the end positions l that carry a deadline (ascending) and
+    // Dmin[l] in ticks of 2^-40 s (reading A-12), written by K1c, read by K3c
+    int32_t* end_n;          // [n_inst]
+    int32_t* end_l;          // [n_inst][H]
+    long long* end_d;        // [n_inst][H]
 };
 
 // workspace for tp_predict_ips_runs; cell mode is used when the model's dense cell space
@@ -105,6 +114,39 @@ constexpr int64_t kMaxCells = 1LL << 22;
 size_t runs_workspace_bytes(int64_t n_cells, int32_t n_inst, int32_t H, int32_t F);
 void runs_workspace_carve(void* ws, int64_t n_cells, int32_t n_inst, int32_t H, int32_t F, K2Params& p);
 int64_t model_cells(const Model& m);
+
+#ifdef __CUDACC__
+constexpr long long kNoDeadline = 0x7fffffffffffffffLL;
+// ceil(s * 2^40) for the E2E compare T_R < s (T_R integer ticks of 2^-40 s, reading A-12):
+// <= 0 / NaN -> 0 (never passes), >= 2^62 -> INT64_MAX (always passes; T_R < 2^58).
+__device__ __forceinline__ long long slack_ticks(double s) {
+    const double d = s * 0x1p40;
+    if (!(d > 0.0)) return 0;
+    if (d >= 0x1p62) return kNoDeadline;
+    return (long long)ceil(d);
+}
+// T' of one IPS value in ticks of 2^-40 s: fl32 reciprocal (reading A-9), exact scaling.
+__device__ __forceinline__ long long ticks_of(float ips) {
+    const float t = __frcp_rn(ips);
+    return (long long)(t * 0x1p40f);    // exact: t in [2^-17, 16]
+}
+#endif
+
+// Compact path.  K1c: projection + FIFO gate (as launch_project) + run compression, cell claims
+// and the per-instance deadline list, one warp per instance.  `w` carries the model's cut / rank
+// tables and the workspace (cell mode required).  B/KV: NULL, m = 1 only (bkv_rows = 0) or full
+// rows (bkv_rows = 1).
+int launch_project_compact(const K2Params& w, const tp_inst* inst, int32_t n_inst, const tp_req* req,
+                           int32_t n_req, const double* t_dead, int32_t H, int32_t* B, int32_t* KV, int bkv_rows,
+                           int32_t* n, int32_t* n_adm, uint32_t* status, uint32_t skip, cudaStream_t s,
+                           const int32_t* force_adm = nullptr, const uint32_t* lost_mask = nullptr);
+// K3c: one warp per instance, lane u = level u; T_R formed run by run from the LUT, checked at the
+// deadline list's end positions; search 0 = exhaustive (A-13), 1 = the paper's binary search (A-24).
+int launch_select_compact(const K2Params& w, int32_t n_inst, const int32_t* n, int32_t H, int32_t F,
+                          int64_t tbt_ticks, int search, uint32_t skip, int32_t* level, uint32_t* status,
+                          cudaStream_t s);
+// K1c's shared memory per warp for horizon H (bytes)
+int project_compact_smem_per_warp(int32_t H);
 
 int launch_project(const tp_inst* inst, int32_t n_inst, const tp_req* req, int32_t n_req, int32_t H,
                    int32_t* B, int32_t* KV, int32_t* n, int32_t* n_adm, uint32_t* status, cudaStream_t s,

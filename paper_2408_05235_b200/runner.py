@@ -44,22 +44,36 @@ class Round:
         self.level = torch.empty(I, dtype=torch.int32, device=dev)
         self.ips = torch.zeros((I, F, H), dtype=torch.float32, device=dev)
         self.tr = torch.zeros((I, F, H), dtype=torch.int64, device=dev) if want_tr else None
-        assert k2_mode in ("fused", "cells", "runs", "direct")
-        assert k2_mode not in ("cells", "fused") or model is not None, "cell mode sizes its workspace from the model"
+        assert k2_mode in ("compact", "fused", "cells", "runs", "direct")
+        assert k2_mode not in ("cells", "fused", "compact") or model is not None, \
+            "cell mode sizes its workspace from the model"
         self.k2_mode = k2_mode
         assert search in ("exhaustive", "binary")
-        assert search == "exhaustive" or (k2_mode == "fused" and not want_tr), "binary search reads the cell LUT"
+        assert search == "exhaustive" or (k2_mode in ("fused", "compact") and not want_tr), \
+            "binary search reads the cell LUT"
+        assert not (want_tr and k2_mode == "compact"), "the compact path emits no T_R"
         self.search = search
         self.model = model
-        self.work = torch.empty(tp.tp_predict_ips_workspace_size(model if k2_mode in ("cells", "fused") else None,
+        self.bkv = True             # compact mode: K1c writes the full B/KV rows (tests); bench turns it off
+        self.work = torch.empty(tp.tp_predict_ips_workspace_size(model if k2_mode in ("cells", "fused", "compact")
+                                                                 else None,
                                                                  I, H, F),
                                 dtype=torch.uint8, device=dev) if k2_mode != "direct" else None
 
     def project(self, stream=None):
+        if self.k2_mode == "compact":
+            # K1c: full B/KV rows too, so results() can compare them (bench.py passes bkv_rows=False)
+            tp.tp_project_compact(self.model, self.work, self.inst, self.I, self.req, self.R, self.t_dead, self.H,
+                                  self.B if self.bkv else None, self.KV if self.bkv else None, 1, self.n, self.n_adm,
+                                  self.status, stream)
+            return
         tp.tp_project(self.inst, self.I, self.req, self.R, self.H, self.B, self.KV, self.n, self.n_adm, self.status,
                       stream)
 
     def predict(self, model, stream=None):
+        if self.k2_mode == "compact":
+            tp.tp_predict_cells(model, self.work, self.I, self.H, self.freq, stream)
+            return
         if self.k2_mode in ("runs", "cells", "fused"):
             # fused: cell mode without the ips grid (values stay in the workspace for K3)
             tp.tp_predict_ips_runs(model, self.inst, self.I, self.B, self.KV, self.n, self.H, self.freq,
@@ -69,6 +83,10 @@ class Round:
                               self.status, stream)
 
     def select(self, stream=None):
+        if self.k2_mode == "compact":
+            tp.tp_select_freq_compact(self.model, self.work, self.I, self.n, self.H, self.F, self.tbt, self.search,
+                                      self.level, self.status, stream)
+            return
         if self.search == "binary":
             tp.tp_select_freq_binary(self.model, self.work, self.inst, self.I, self.req, self.R, self.t_dead, self.n,
                                      self.n_adm, self.H, self.F, self.tbt, self.level, self.status, stream)

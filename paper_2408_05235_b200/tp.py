@@ -24,8 +24,9 @@ ST_QUEUE_BLOCKED, ST_IPS_CLAMPED, ST_BAD_INPUT = 16, 32, 64
 EXPORTS = ["tp_gbdt_load", "tp_gbdt_free", "tp_gbdt_get_info", "tp_project", "tp_predict_ips",
            "tp_predict_ips_workspace_size", "tp_predict_ips_runs", "tp_runs_total", "tp_cells_total", "tp_select_freq", "tp_select_freq_ws", "tp_ctx_create", "tp_ctx_free",
            "tp_decide", "tp_decide_host", "tp_replay_advance", "tp_ctx_enable_admission", "tp_decide_admit", "tp_ctx_set_k2_mode", "tp_ctx_buffers",
-           "tp_select_freq_binary", "tp_ctx_set_search", "tp_strerror", "tp_abi_version"]
-K2_DIRECT, K2_RUNS = 0, 1
+           "tp_select_freq_binary", "tp_ctx_set_search", "tp_project_compact", "tp_predict_cells",
+           "tp_select_freq_compact", "tp_strerror", "tp_abi_version"]
+K2_DIRECT, K2_RUNS, K2_COMPACT = 0, 1, 2
 SEARCH_EXHAUSTIVE, SEARCH_BINARY = 0, 1
 
 if not os.path.exists(LIB_PATH):
@@ -55,6 +56,10 @@ _L.tp_select_freq.argtypes = [_vp, _i32, _vp, _i32, _vp, _vp, _vp, _vp, _i32, _i
 _L.tp_select_freq_ws.argtypes = [_vp, _vp, _vp, _i32, _vp, _i32, _vp, _vp, _vp, _i32, _i32, _f32, _vp, _vp, _vp, _vp]
 _L.tp_select_freq_binary.argtypes = [_vp, _vp, _vp, _i32, _vp, _i32, _vp, _vp, _vp, _i32, _i32, _f32, _vp, _vp, _vp]
 _L.tp_ctx_set_search.argtypes = [_vp, ctypes.c_int]
+_L.tp_project_compact.argtypes = [_vp, _vp, ctypes.c_size_t, _vp, _i32, _vp, _i32, _vp, _i32, _vp, _vp, _i32, _vp,
+                                  _vp, _vp, _vp]
+_L.tp_predict_cells.argtypes = [_vp, _vp, ctypes.c_size_t, _i32, _i32, _vp, _i32, _vp]
+_L.tp_select_freq_compact.argtypes = [_vp, _vp, ctypes.c_size_t, _i32, _vp, _i32, _i32, _f32, _i32, _vp, _vp, _vp]
 _L.tp_replay_advance.argtypes = [_vp, _vp, _i32, _vp, _vp, _vp, _vp, _i32, _i32] + [_vp] * 6 + [_vp, _i32] + [_vp] * 8
 _L.tp_ctx_enable_admission.argtypes = [_vp, _i32]
 _L.tp_decide_admit.argtypes = [_vp, _vp, _vp, _i32, _vp, _i32, _vp, _vp, _i32, _f32, _vp, _vp, _vp, _vp, _vp]
@@ -213,6 +218,30 @@ def tp_select_freq_binary(model: Gbdt, workspace, inst, n_inst, req, n_req, t_de
     _check(_L.tp_select_freq_binary(model.handle, _dp(workspace), _dp(inst), int(n_inst), _dp(req), int(n_req),
                                     _dp(t_dead), _dp(n), _dp(n_adm), int(H), int(F), float(np.float32(tbt_slo)),
                                     _dp(level), _dp(status), _stream(stream)), "tp_select_freq_binary")
+
+
+def tp_project_compact(model: Gbdt, workspace, inst, n_inst, req, n_req, t_dead, H, B, KV, bkv_rows, n, n_adm,
+                       status, stream=None):
+    """K1c: projection + gate + runs / cell claims + deadline list (B, KV may be None)."""
+    _check(_L.tp_project_compact(model.handle, _dp(workspace), workspace.numel(), _dp(inst), int(n_inst), _dp(req),
+                                 int(n_req), _dp(t_dead), int(H), _dp(B), _dp(KV), int(bkv_rows), _dp(n),
+                                 _dp(n_adm), _dp(status), _stream(stream)), "tp_project_compact")
+
+
+def tp_predict_cells(model: Gbdt, workspace, n_inst, H, freq, stream=None):
+    """K2 on the cells tp_project_compact claimed (LUT in the workspace)."""
+    f, F = _freq(freq)
+    _check(_L.tp_predict_cells(model.handle, _dp(workspace), workspace.numel(), int(n_inst), int(H), f.ctypes.data,
+                               F, _stream(stream)), "tp_predict_cells")
+
+
+def tp_select_freq_compact(model: Gbdt, workspace, n_inst, n, H, F, tbt_slo, search, level, status, stream=None):
+    """K3c: one warp per instance, lane = level; search 0 exhaustive (A-13) / 1 binary (A-24)."""
+    if isinstance(search, str):
+        search = {"exhaustive": SEARCH_EXHAUSTIVE, "binary": SEARCH_BINARY}[search]
+    _check(_L.tp_select_freq_compact(model.handle, _dp(workspace), workspace.numel(), int(n_inst), _dp(n), int(H),
+                                     int(F), float(np.float32(tbt_slo)), int(search), _dp(level), _dp(status),
+                                     _stream(stream)), "tp_select_freq_compact")
 
 
 def tp_replay_advance(model: Gbdt, inst, n_inst, req, t_dead, req_out, t_dead_out, slot_cap, H, B, KV, n, n_adm,

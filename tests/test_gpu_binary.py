@@ -20,10 +20,17 @@ torch = pytest.importorskip("torch")
 pytestmark = pytest.mark.gpu
 
 
-def run_gpu_bs(gpu, blob, inputs, idx=None):  # noqa: F811
+@pytest.fixture(params=["fused", "compact"])
+def lut_mode(request):
+    """Both paths that read the cell LUT: the speculative warp-per-level K3 (fused) and K3c
+    (compact: every level at once, the search replayed on the pass bits)."""
+    return request.param
+
+
+def run_gpu_bs(gpu, blob, inputs, idx=None, mode="fused"):  # noqa: F811
     tp, runner = gpu
     model = tp.Gbdt(blob, 0)
-    r = runner.Round(inputs, "cuda:0", k2_mode="fused", model=model, search="binary")
+    r = runner.Round(inputs, "cuda:0", k2_mode=mode, model=model, search="binary")
     r.run(model)
     out = r.results(idx)
     del out["ips"]
@@ -46,7 +53,7 @@ def check(got, ref, idx=None):
         assert np.array_equal(got[k][idx], ref[k]), k
 
 
-def test_tiny_random_non_monotone(gpu, oracle_mod):  # noqa: F811
+def test_tiny_random_non_monotone(gpu, oracle_mod, lut_mode):  # noqa: F811
     rng = np.random.default_rng(2424)
     differ = 0
     for trial in range(120):
@@ -54,13 +61,13 @@ def test_tiny_random_non_monotone(gpu, oracle_mod):  # noqa: F811
         inputs = dict(inst=inst, req=req, t_dead=td, H=H, freq=freq, tbt_slo=tbt)
         blob = W.write_blob(ens)
         ref = oracle_bs(oracle_mod, blob, inputs, threads=1)
-        check(run_gpu_bs(gpu, blob, inputs), ref)
+        check(run_gpu_bs(gpu, blob, inputs, mode=lut_mode), ref)
         exh = oracle_mod.decide(oracle_mod.Model(blob), inst, req, td, H, freq, tbt, want_grid=False)
         differ += int((exh["level"] != ref["level"]).sum())
     assert differ >= 5
 
 
-def test_visited_levels_clamp_and_non_monotone_path(gpu, oracle_mod):  # noqa: F811
+def test_visited_levels_clamp_and_non_monotone_path(gpu, oracle_mod, lut_mode):  # noqa: F811
     f = np.array([1000.0, 1200.0, 1400.0, 1600.0], np.float32)
     ens = cases.ensemble_from_nodes([{"feature": 3, "threshold": 1300.0, "left": 1, "right": 2},
                                      {"feature": -1, "leaf": 50.0},
@@ -68,7 +75,7 @@ def test_visited_levels_clamp_and_non_monotone_path(gpu, oracle_mod):  # noqa: F
                                      {"feature": -1, "leaf": 1e9}, {"feature": -1, "leaf": 50.0}])
     inst, req, td = cases.make_instances([dict(N=16, running=[(0, 5, 4, 0, 1e6)])], 4)
     inputs = dict(inst=inst, req=req, t_dead=td, H=4, freq=f, tbt_slo=16.0)
-    got = run_gpu_bs(gpu, W.write_blob(ens), inputs)
+    got = run_gpu_bs(gpu, W.write_blob(ens), inputs, mode=lut_mode)
     assert got["level"][0] == 0 and got["status"][0] == 0      # level 2 clamps but is never visited
     check(got, oracle_bs(oracle_mod, W.write_blob(ens), inputs))
     ens2 = cases.ensemble_from_nodes([{"feature": 3, "threshold": 1100.0, "left": 1, "right": 2},
@@ -77,34 +84,34 @@ def test_visited_levels_clamp_and_non_monotone_path(gpu, oracle_mod):  # noqa: F
                                       {"feature": -1, "leaf": 1.0}, {"feature": -1, "leaf": 64.0}])
     inst, req, td = cases.make_instances([dict(N=16, running=[(0, 5, 8, 0, 1.0)])], 8)
     inputs = dict(inst=inst, req=req, t_dead=td, H=8, freq=f, tbt_slo=16.0)
-    assert run_gpu_bs(gpu, W.write_blob(ens2), inputs)["level"][0] == 3
+    assert run_gpu_bs(gpu, W.write_blob(ens2), inputs, mode=lut_mode)["level"][0] == 3
 
 
 @pytest.mark.parametrize("name", ["P1", "P2", "C1"])
-def test_configs(gpu, oracle_mod, name):  # noqa: F811
+def test_configs(gpu, oracle_mod, name, lut_mode):  # noqa: F811
     cfg = W.CONFIGS[name]
     if name == "C1":
         cfg = dataclasses.replace(cfg, n_inst=4096)
     blob = W.write_blob(W.config_ensemble(cfg))
     inputs = W.config_inputs(cfg)
-    check(run_gpu_bs(gpu, blob, inputs), oracle_bs(oracle_mod, blob, inputs))
+    check(run_gpu_bs(gpu, blob, inputs, mode=lut_mode), oracle_bs(oracle_mod, blob, inputs))
 
 
-def test_c2_full(gpu, oracle_mod):  # noqa: F811
+def test_c2_full(gpu, oracle_mod, lut_mode):  # noqa: F811
     cfg = W.CONFIGS["C2"]
     blob = W.write_blob(W.config_ensemble(cfg))
     inputs = W.config_inputs(cfg)
     ref = oracle_bs(oracle_mod, blob, inputs, threads=16)
-    check(run_gpu_bs(gpu, blob, inputs), ref)
+    check(run_gpu_bs(gpu, blob, inputs, mode=lut_mode), ref)
 
 
-def test_c3_sampled(gpu, oracle_mod):  # noqa: F811
+def test_c3_sampled(gpu, oracle_mod, lut_mode):  # noqa: F811
     """BASELINE configs[2] at full size, 32 levels (2 speculative rounds); stratified sample."""
     cfg = W.CONFIGS["C3"]
     blob = W.write_blob(W.config_ensemble(cfg))
     inputs = W.config_inputs(cfg)
     sub = np.arange(5, cfg.n_inst, 512)
-    got = run_gpu_bs(gpu, blob, inputs, idx=sub)
+    got = run_gpu_bs(gpu, blob, inputs, idx=sub, mode=lut_mode)
     check(got, oracle_bs(oracle_mod, blob, _subset(inputs, sub)))
 
 

@@ -30,21 +30,22 @@ def gpu():
     return tp, runner
 
 
-@pytest.fixture(params=["direct", "runs", "cells", "fused"])
+@pytest.fixture(params=["direct", "runs", "cells", "fused", "compact"])
 def mode(request):
-    """All K2 variants: tp_predict_ips (direct), tp_predict_ips_runs in run and cell mode, and cell
-    mode fused with K3 (tp_predict_ips_runs without the ips grid + tp_select_freq_ws)."""
+    """All K2 variants: tp_predict_ips (direct), tp_predict_ips_runs in run and cell mode, cell
+    mode fused with K3 (tp_predict_ips_runs without the ips grid + tp_select_freq_ws), and the
+    compact path (tp_project_compact -> tp_predict_cells -> tp_select_freq_compact)."""
     return request.param
 
 
 def run_gpu(gpu, blob, inputs, want_tr=True, idx=None, mode="runs"):
     tp, runner = gpu
     model = tp.Gbdt(blob, 0)
-    r = runner.Round(inputs, "cuda:0", want_tr=want_tr, k2_mode=mode, model=model)
+    r = runner.Round(inputs, "cuda:0", want_tr=want_tr and mode != "compact", k2_mode=mode, model=model)
     r.run(model)
     out = r.results(idx)
-    if mode == "fused":
-        del out["ips"]          # never materialised; T_R (tr) is still produced by K3
+    if mode in ("fused", "compact"):
+        del out["ips"]          # never materialised; T_R (tr) is still produced by K3 in fused mode
     del r
     model.free()
     return out
@@ -233,7 +234,7 @@ def test_clamp_and_bad_input(gpu, oracle_mod, mode):
     assert got["status"][0] & 32 and got["status"].tolist()[1:] == [64, 64, 64, 1]
 
 
-@pytest.mark.parametrize("k2,cells", [(0, False), (1, False), (1, True)])
+@pytest.mark.parametrize("k2,cells", [(0, False), (1, False), (1, True), (2, True)])
 def test_decide_entry_points_agree(gpu, oracle_mod, k2, cells):
     """tp_decide (device) and tp_decide_host (host buffers, e2e path) == the oracle, both K2 modes."""
     tp, runner = gpu
