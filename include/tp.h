@@ -327,7 +327,7 @@ int tp_decide_admit(tp_ctx* c, const tp_gbdt* m, const tp_inst* inst, int32_t n_
 /* Which path tp_decide / tp_decide_host use (default TP_K2_COMPACT for a context created for a model
  * with a cell mode, TP_K2_RUNS otherwise). */
 enum { TP_K2_DIRECT = 0, TP_K2_RUNS = 1, TP_K2_COMPACT = 2 };
-int tp_ctx_set_k2_mode(tp_ctx* c, int mode);
+int tp_ctx_set_k2_mode(tp_ctx* c, int mode);   /* may allocate the ips grid: TP_ENOMEM */
 
 /* K3 search order for tp_decide / tp_decide_host / tp_decide_admit (default exhaustive, reading
  * A-13).  TP_SEARCH_BINARY (reading A-24, tp_select_freq_binary) needs the fused cell path: a
@@ -337,7 +337,9 @@ enum { TP_SEARCH_EXHAUSTIVE = 0, TP_SEARCH_BINARY = 1 };
 int tp_ctx_set_search(tp_ctx* c, int search);
 
 /* Device pointers of the context's scratch (for inspection / tests); any out may be NULL.  After a
- * TP_K2_COMPACT tp_decide only the m = 1 column of B / KV is written, and ips is not. */
+ * TP_K2_COMPACT tp_decide only the m = 1 column of B / KV is written, and ips is not (a context
+ * created for a cell-mode model allocates the ips grid only when tp_ctx_set_k2_mode selects a
+ * mode that writes it; before that, *ips is NULL). */
 int tp_ctx_buffers(tp_ctx* c, int32_t** B, int32_t** KV, int32_t** n, int32_t** n_adm, float** ips);
 
 /*

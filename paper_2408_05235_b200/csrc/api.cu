@@ -335,7 +335,8 @@ int tp_ctx_create(int device, const tp_gbdt* model, int32_t n_inst_max, int32_t 
     bool ok = cudaMalloc(&c->B, I * H * 4) == cudaSuccess && cudaMalloc(&c->KV, I * H * 4) == cudaSuccess &&
               cudaMalloc(&c->n, I * 4) == cudaSuccess && cudaMalloc(&c->n_adm, I * 4) == cudaSuccess &&
               cudaMalloc(&c->level, I * 4) == cudaSuccess && cudaMalloc(&c->status, I * 4) == cudaSuccess &&
-              cudaMalloc(&c->ips, I * F_max * H * 4) == cudaSuccess &&
+              // the ips grid only for the paths that write it (allocated on demand by set_k2_mode)
+              (c->cells_model || cudaMalloc(&c->ips, I * F_max * H * 4) == cudaSuccess) &&
               cudaMalloc(&c->work, c->work_bytes = tp::runs_workspace_bytes(model ? tp::model_cells(model->m) : 0,
                                                                             (int32_t)I, H, F_max)) == cudaSuccess &&
               cudaMalloc(&c->inst, I * sizeof(tp_inst)) == cudaSuccess &&
@@ -430,6 +431,18 @@ int tp_decide_admit(tp_ctx* c, const tp_gbdt* m, const tp_inst* inst, int32_t n_
 
 int tp_ctx_set_k2_mode(tp_ctx* c, int mode) {
     if (!c || (mode != TP_K2_DIRECT && mode != TP_K2_RUNS && mode != TP_K2_COMPACT)) return TP_EINVAL;
+    if (mode != TP_K2_COMPACT && !c->ips) {   // direct / run / cell modes may write the ips grid
+        const size_t I = (size_t)(c->n_inst_max > 0 ? c->n_inst_max : 1);
+        int prev = 0;
+        cudaGetDevice(&prev);
+        if (cudaSetDevice(c->device) != cudaSuccess) return TP_ECUDA;
+        const bool ok = cudaMalloc(&c->ips, I * c->F_max * c->H * 4) == cudaSuccess;
+        cudaSetDevice(prev);
+        if (!ok) {
+            c->ips = nullptr;
+            return TP_ENOMEM;
+        }
+    }
     c->k2_mode = mode;
     return TP_OK;
 }

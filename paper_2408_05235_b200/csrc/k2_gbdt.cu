@@ -527,11 +527,9 @@ k2_cells_phase(const __grid_constant__ K2Params p, int t_begin, int t_count, int
     constexpr int TW = (2 << D) < 4 ? 4 : (2 << D);
     const int tid = threadIdx.x;
     const int G = (p.F + RU - 1) / RU;
-    const int ncell = *p.cell_count + 1;
-    const int64_t U = (int64_t)ncell * G;
-    const int64_t t0 = U * blockIdx.x / gridDim.x, t1 = U * (blockIdx.x + 1) / gridDim.x;
-    if (t0 >= t1) return;                      // uniform: no task, no TMA issued
     const int nchunks = (t_count + kPhaseChunkTrees - 1) / kPhaseChunkTrees;
+    // the phase's trees are model constants: their TMA loads are issued before waiting on the
+    // previous kernel (programmatic dependent launch), overlapping its tail
     if (tid == 0) {
         for (int c = 0; c < nchunks; ++c) mbar_init(&bar[c], 1);
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
@@ -545,9 +543,13 @@ k2_cells_phase(const __grid_constant__ K2Params p, int t_begin, int t_count, int
     }
     if (tid < p.F) s_rf[tid] = rank_of(p.cuts + p.cut_off[3], p.cut_off[4] - p.cut_off[3], p.freq[tid]);
     __syncthreads();                           // barriers initialised, s_rf visible
+    pdl_wait();                                // cell list / LUT of the previous kernel
+    const int ncell = *p.cell_count + 1;
+    const int64_t U = (int64_t)ncell * G;
+    const int64_t t0 = U * blockIdx.x / gridDim.x, t1 = U * (blockIdx.x + 1) / gridDim.x;
     const int nB = p.cut_off[2] - p.cut_off[1], nKV = p.cut_off[3] - p.cut_off[2];
     const uint32_t nk1 = (uint32_t)nKV + 1, nb1 = (uint32_t)nB + 1;
-    for (int64_t task = t0 + tid; task < t1; task += blockDim.x) {
+    for (int64_t task = t0 + tid; task < t1; task += blockDim.x) {   // (no task: the CTA still drains its TMA)
         const int ug = (int)(task / ncell);
         const int cidx = (int)(task - (int64_t)ug * ncell);
         const int u0 = ug * RU;
@@ -616,6 +618,8 @@ k2_cells_phase(const __grid_constant__ K2Params p, int t_begin, int t_count, int
                 if (u0 + r < p.F) p.lut[(size_t)cidx * p.F + u0 + r] = acc[r];
         }
     }
+    if (tid == 0 && t0 + tid >= t1)            // no task: wait for the bulk copies before exiting
+        for (int ch = 0; ch < nchunks; ++ch) mbar_wait(&bar[ch], 0u);
 }
 
 template <int D, int RU>
@@ -635,8 +639,9 @@ int launch_phases(const K2Params& p, cudaStream_t s) {
         return TP_ECUDA;
     for (int ph = 0; ph < nphase; ++ph) {
         const int tb = ph * per, tc = std::max(0, std::min(per, p.n_trees - tb));
-        kern<<<sms, kPhaseThreads, smem, s>>>(p, tb, tc, ph == 0, ph == nphase - 1);
-        if (cudaPeekAtLastError() != cudaSuccess) return TP_ECUDA;
+        if (launch_pdl(kern, dim3(sms), dim3(kPhaseThreads), smem, s, p, tb, tc, (int)(ph == 0),
+                       (int)(ph == nphase - 1)) != cudaSuccess)
+            return TP_ECUDA;
     }
     return TP_OK;
 }

@@ -22,7 +22,14 @@ namespace {
 
 constexpr int kWarpsPerCta = 8;
 constexpr unsigned kFull = 0xffffffffu;
-constexpr int kPrefetch = 8;      // LUT values loaded ahead per lane
+// W = 1 (large batches, throughput): 8 CTAs per SM and 4 LUT rows prefetched; W > 1 (small
+// batches, latency): 4 CTAs per SM and 8 rows prefetched (measured on C3 / C2)
+#ifndef TP_K3C_PREFETCH
+#define TP_K3C_PREFETCH 4
+#endif
+#ifndef TP_K3C_MINB
+#define TP_K3C_MINB 8
+#endif      // LUT values loaded ahead per lane
 
 // TP_K3C_WARPS (1/2/4/8): warps per instance override (tuning)
 int env_warps() {
@@ -74,7 +81,7 @@ __device__ __forceinline__ int warp_lower_bound(const int* __restrict__ a, int c
 // iff P_w < M_w for every w, P_w = S_0 + ... + S_{w-1} (T_R[l] = P_w + T_local(l) < Dmin[l]), and
 // the TBT check holds on the total.  W = 1 keeps the early exit once every level has failed.
 template <int W>
-__global__ void __launch_bounds__(kWarpsPerCta * 32, 4)
+__global__ void __launch_bounds__(kWarpsPerCta * 32, W == 1 ? TP_K3C_MINB : 4)
 k3_compact(const __grid_constant__ K3cParams p) {
     constexpr int IPC = kWarpsPerCta / W;            // instances per CTA
     __shared__ long long s_S[W > 1 ? kWarpsPerCta : 1][32], s_M[W > 1 ? kWarpsPerCta : 1][32];
@@ -83,6 +90,7 @@ k3_compact(const __grid_constant__ K3cParams p) {
     const int g = warp / W, w = warp % W;             // instance slot in the CTA, segment
     const int i = blockIdx.x * IPC + g;
     const bool live = i < p.n_inst;
+    pdl_wait();                                       // K1c / K2 outputs
     const int F = p.F;
     uint32_t st = 0;
     bool skipped = true;
@@ -139,23 +147,26 @@ k3_compact(const __grid_constant__ K3cParams p) {
         for (int kb = ka; kb < kz; kb += 32) {
             const int s_k = nx_s, len_k = nx_len;
             const int rr = (kb + lane < kz) ? __ldcg(p.cell_tab + nx_key) : 0;
+            const int roff = rr * F;                  // the run's LUT row offset (< 2^27)
             if (kb + 32 < kz) load_chunk(kb + 32);
             if (kb + lane < kz) cm |= __ldcg(p.cell_clamp + rr);
             const int cnt = min(32, kz - kb);
+            constexpr int kPrefetch = W == 1 ? TP_K3C_PREFETCH : 8;
             for (int j0 = 0; j0 < cnt; j0 += kPrefetch) {
                 long long tv[kPrefetch];
 #pragma unroll
                 for (int q = 0; q < kPrefetch; ++q) {
-                    const int r_ = __shfl_sync(kFull, rr, (j0 + q) & 31);
-                    tv[q] = act ? __ldcg(lt + (size_t)r_ * F) : 0;     // rows past cnt: row 0, unused
+                    const int o_ = __shfl_sync(kFull, roff, (j0 + q) & 31);
+                    tv[q] = act ? __ldcg(lt + o_) : 0;     // rows past cnt: row 0, unused
                 }
 #pragma unroll
                 for (int q = 0; q < kPrefetch; ++q) {
                     if (j0 + q < cnt) {                  // uniform
                         const int s = __shfl_sync(kFull, s_k, j0 + q), len = __shfl_sync(kFull, len_k, j0 + q);
                         const long long t = tv[q];
+                        const long long Tm = T - (long long)(s - 1) * t;   // T_R(l) = Tm + l * t on the run
                         while (cur_l < s + len) {        // end positions inside this run (>= s: sorted)
-                            const long long tl = T + (long long)(cur_l - s + 1) * t;
+                            const long long tl = Tm + (long long)cur_l * t;
                             if (W == 1) ok &= tl < cur_d;
                             else M = min(M, cur_d - tl);
                             if (++ep - eb == 32) {
@@ -260,7 +271,7 @@ int launch_select_compact(const K2Params& w, int32_t n_inst, const int32_t* n, i
     int W = w_env > 0 ? w_env : (n_inst * 8 <= slots ? 8 : n_inst * 4 <= slots ? 4 : n_inst * 2 <= slots ? 2 : 1);
     auto launch = [&](auto kern, int ipc) {
         const int grid = (n_inst + ipc - 1) / ipc;
-        kern<<<grid, kWarpsPerCta * 32, 0, s>>>(p);
+        launch_pdl(kern, dim3(grid), dim3(kWarpsPerCta * 32), 0, s, p);
     };
     switch (W) {
         case 8: launch(k3_compact<8>, 1); break;

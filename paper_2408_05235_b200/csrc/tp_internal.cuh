@@ -4,6 +4,8 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <utility>
+
 #include "tp.h"
 
 namespace tp {
@@ -116,6 +118,27 @@ void runs_workspace_carve(void* ws, int64_t n_cells, int32_t n_inst, int32_t H, 
 int64_t model_cells(const Model& m);
 
 #ifdef __CUDACC__
+// Programmatic dependent launch (sm_90+): a kernel launched with launch_pdl may start while the
+// previous kernel on the stream drains; it must execute pdl_wait() before touching anything the
+// previous kernel writes (a no-op when launched without the attribute).
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+
+template <typename... KArgs, typename... Args>
+cudaError_t launch_pdl(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t s, Args&&... args) {
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = grid;
+    cfg.blockDim = block;
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = s;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    return cudaLaunchKernelEx(&cfg, kern, std::forward<Args>(args)...);
+}
+
 constexpr long long kNoDeadline = 0x7fffffffffffffffLL;
 // ceil(s * 2^40) for the E2E compare T_R < s (T_R integer ticks of 2^-40 s, reading A-12):
 // <= 0 / NaN -> 0 (never passes), >= 2^62 -> INT64_MAX (always passes; T_R < 2^58).

@@ -42,7 +42,10 @@ class Round:
         self.n_adm = torch.empty(I, dtype=torch.int32, device=dev)
         self.status = torch.empty(I, dtype=torch.int32, device=dev)
         self.level = torch.empty(I, dtype=torch.int32, device=dev)
-        self.ips = torch.zeros((I, F, H), dtype=torch.float32, device=dev)
+        # the ips grid exists only on the paths that write it (the fused and compact paths keep the
+        # values in the workspace's cell LUT)
+        self.ips = torch.zeros((I, F, H), dtype=torch.float32, device=dev) \
+            if k2_mode in ("direct", "runs", "cells") else None
         self.tr = torch.zeros((I, F, H), dtype=torch.int64, device=dev) if want_tr else None
         assert k2_mode in ("compact", "fused", "cells", "runs", "direct")
         assert k2_mode not in ("cells", "fused", "compact") or model is not None, \
@@ -110,7 +113,9 @@ class Round:
         sel = slice(0, I) if idx is None else torch.as_tensor(np.asarray(idx), device=self.device, dtype=torch.long)
         get = lambda t: t[sel].cpu().numpy()   # noqa: E731
         out = dict(B=get(self.B), KV=get(self.KV), n=get(self.n), n_adm=get(self.n_adm),
-                   status=get(self.status).view(np.uint32), level=get(self.level), ips=get(self.ips))
+                   status=get(self.status).view(np.uint32), level=get(self.level))
+        if self.ips is not None:
+            out["ips"] = get(self.ips)
         if self.tr is not None:
             out["tr"] = get(self.tr)
         return out

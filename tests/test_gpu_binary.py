@@ -33,7 +33,6 @@ def run_gpu_bs(gpu, blob, inputs, idx=None, mode="fused"):  # noqa: F811
     r = runner.Round(inputs, "cuda:0", k2_mode=mode, model=model, search="binary")
     r.run(model)
     out = r.results(idx)
-    del out["ips"]
     del r
     model.free()
     return out

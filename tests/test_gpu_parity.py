@@ -44,8 +44,7 @@ def run_gpu(gpu, blob, inputs, want_tr=True, idx=None, mode="runs"):
     r = runner.Round(inputs, "cuda:0", want_tr=want_tr and mode != "compact", k2_mode=mode, model=model)
     r.run(model)
     out = r.results(idx)
-    if mode in ("fused", "compact"):
-        del out["ips"]          # never materialised; T_R (tr) is still produced by K3 in fused mode
+    assert ("ips" in out) == (mode not in ("fused", "compact"))   # fused / compact: never materialised
     del r
     model.free()
     return out
@@ -316,3 +315,17 @@ def test_imported_sklearn_model(gpu, oracle_mod, mode):
     blob = model_io.to_blob(model_io.from_sklearn(est))
     inputs = W.config_inputs(dataclasses.replace(W.CONFIGS["P1"], n_inst=48, seed=777))
     assert_parity(run_gpu(gpu, blob, inputs, mode=mode), run_oracle(oracle_mod, blob, inputs))
+
+
+# ------------------------------------------------------------------ compact-path geometry
+
+@pytest.mark.parametrize("n_inst,H", [(2000, 512), (300, 2000), (40, 8192), (7, 16384)])
+def test_compact_geometry(gpu, oracle_mod, n_inst, H):
+    """The compact path's launch geometry against the oracle: K3c with W = 2 warps per instance
+    (2,000 instances), K1c segments longer than 32 iterations (H = 2,000: S = 64; H = 8,192 / 16,384:
+    one warp per CTA, 66 / 132 KB of per-warp histograms)."""
+    cfg = dataclasses.replace(W.CONFIGS["P2"], n_inst=n_inst, H=H, seed=8100 + H)
+    blob = W.write_blob(W.config_ensemble(cfg))
+    inputs = W.config_inputs(cfg)
+    assert_parity(run_gpu(gpu, blob, inputs, want_tr=False, mode="compact"),
+                  run_oracle(oracle_mod, blob, inputs, want_tr=False))

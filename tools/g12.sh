@@ -1,0 +1,4 @@
+timeout 300 python -c "import __graft_entry__ as g; g.smoke()"
+timeout 300 python bench.py --no-cpu-baseline --steps 50 --e2e-steps 5 2>/dev/null | python -c "import json,sys; d=json.loads(sys.stdin.read().strip().splitlines()[-1]); print('C2', round(d['ms_per_step']*1e3,1), {k: round(v*1e3,1) for k,v in d['per_kernel_ms'].items()})"
+timeout 300 python bench.py --workload C3 --no-cpu-baseline --steps 5 --e2e-steps 1 2>/dev/null | python -c "import json,sys; d=json.loads(sys.stdin.read().strip().splitlines()[-1]); print('C3', round(d['ms_per_step']*1e3,1), {k: round(v*1e3,1) for k,v in d['per_kernel_ms'].items()})"
+timeout 900 python -m pytest tests -m gpu -x -q 2>&1 | tail -3
