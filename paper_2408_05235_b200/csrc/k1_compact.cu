@@ -16,6 +16,7 @@
 // segment m in [1 + t*S, 1 + (t+1)*S) (S a power of two >= 4); segments are padded by P = 4 words
 // when S/4 is even so that 8 consecutive lanes' 128-bit accesses fall in distinct bank quads.
 #include <algorithm>
+#include <cstdlib>
 
 #include "tp_internal.cuh"
 
@@ -29,15 +30,17 @@ struct SegGeom {
     int S_log2, P, arr;         // segment length 2^S_log2, pad words, ints per array
 };
 
-SegGeom seg_geom(int H) {
-    const int need = (H + 31) / 32;
+// G group lanes (32 per warp of the instance's group) share the horizon: lane t owns the segment
+// m in [1 + t*S, 1 + (t+1)*S), S = 2^k >= 4 with G*S >= H.
+SegGeom seg_geom(int H, int G) {
+    const int need = (H + G - 1) / G;
     int S = 4, l = 2;
     while (S < need) {
         S <<= 1;
         ++l;
     }
     const int P = ((S / 4) % 2 == 0) ? 4 : 0;
-    return {l, P, 32 * (S + P) + 8};
+    return {l, P, G * (S + P) + 8};
 }
 
 struct K1cParams {
@@ -83,13 +86,60 @@ __device__ __forceinline__ uint32_t rank_of(const float* __restrict__ c, int cnt
 
 __device__ __forceinline__ int warp_max(int v) { return __reduce_max_sync(kFull, v); }
 
+// The WPI warps that own one instance: a named barrier and double-buffered exchange slots in
+// shared memory (warp-level values -> every warp of the group sees all WPI of them).
+template <int WPI>
+struct Group {
+    int gw;                     // warp index in the group
+    int bar;                    // named barrier id
+    long long* xs;              // [2][WPI][4]
+    int par = 0;
+    __device__ __forceinline__ void sync() const {
+        if (WPI == 1) __syncwarp();
+        else asm volatile("bar.sync %0, %1;" ::"r"(bar), "r"(WPI * 32) : "memory");
+    }
+    // publish 4 warp-level values (lane 0 writes), barrier, return the slot array of this round
+    __device__ __forceinline__ const long long* exchange(long long a, long long b, long long c, long long d) {
+        if (WPI == 1) return nullptr;
+        long long* x = xs + (size_t)par * WPI * 4;
+        if ((threadIdx.x & 31) == 0) {
+            x[gw * 4 + 0] = a;
+            x[gw * 4 + 1] = b;
+            x[gw * 4 + 2] = c;
+            x[gw * 4 + 3] = d;
+        }
+        sync();
+        par ^= 1;
+        return x;
+    }
+    __device__ __forceinline__ int max(int v) {
+        v = warp_max(v);
+        if (WPI == 1) return v;
+        const long long* x = exchange(v, 0, 0, 0);
+        int r = (int)x[0];
+#pragma unroll
+        for (int k = 1; k < WPI; ++k) r = ::max(r, (int)x[k * 4]);
+        return r;
+    }
+};
+
+template <int WPI>
 __global__ void __launch_bounds__(kWarpsPerCta * 32)
 k1_compact(const __grid_constant__ K1cParams p) {
     extern __shared__ __align__(16) int smem[];
+    constexpr int GL = 32 * WPI;                       // group lanes
+    constexpr int NG = kWarpsPerCta / WPI;             // groups (instances) per full CTA
+    __shared__ long long s_x[WPI > 1 ? NG : 1][2 * WPI * 4];
     const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-    const int i = blockIdx.x * (int)(blockDim.x >> 5) + w;
-    if (i >= p.n_inst) return;                        // warp-uniform
-    int* sB = smem + (size_t)w * 2 * p.arr;
+    const int g = w / WPI;
+    Group<WPI> grp;
+    grp.gw = w % WPI;
+    grp.bar = 1 + g;
+    grp.xs = s_x[WPI > 1 ? g : 0];
+    const int gl = grp.gw * 32 + lane;                 // lane within the group
+    const int i = blockIdx.x * (int)((blockDim.x >> 5) / WPI) + g;
+    if (i >= p.n_inst) return;                         // group-uniform
+    int* sB = smem + (size_t)g * 2 * p.arr;
     int* sKV = sB + p.arr;
     const int SL = p.S_log2, S = 1 << SL, P = p.P, H = p.H;
     auto ph = [&](int m) { return (m - 1) + P * ((m - 1) >> SL); };   // physical index of m >= 1
@@ -98,11 +148,11 @@ k1_compact(const __grid_constant__ K1cParams p) {
     const int64_t rb = in.req_begin;
     const int nr = in.n_run, nq = in.n_queue, N = in.N;
     const FastDiv fdN((uint32_t)(N > 0 ? N : 1));
-    for (int k = lane * 4; k + 3 < p.arr; k += 128) {
+    for (int k = gl * 4; k + 3 < p.arr; k += 4 * GL) {
         *reinterpret_cast<int4*>(sB + k) = make_int4(0, 0, 0, 0);
         *reinterpret_cast<int4*>(sKV + k) = make_int4(0, 0, 0, 0);
     }
-    __syncwarp();
+    grp.sync();
 
     // ---- validation (include/tp.h conventions) + running requests -> event histograms ----
     bool bad = N < 1 || in.tp < 1 || (int64_t)in.tp >= kFeatLimit || nr < 0 || nq < 0 || in.kv_cap < 0 ||
@@ -111,7 +161,7 @@ k1_compact(const __grid_constant__ K1cParams p) {
     int nloc = 0, b1 = 0, kv1 = 0;
     bool lost = false;
     if (!bad) {
-        for (int e = lane; e < nr + nq; e += 32) {
+        for (int e = gl; e < nr + nq; e += GL) {
             const int4 r = __ldg(&p.req[rb + e]);
             const int64_t l64 = (int64_t)r.z - r.x;
             const bool eb = r.x < 0 || r.y < 1 || r.z < 1 || r.x >= kFeatLimit || r.y >= kFeatLimit || l64 < 1 ||
@@ -133,20 +183,42 @@ k1_compact(const __grid_constant__ K1cParams p) {
             }
         }
     }
-    bad = __any_sync(kFull, bad);
-    if (!bad) {
+    // group totals: flags (bad | lost << 1), footprint, b1 | kv1 << 32 (both < 2^31), max l
+    {
+        unsigned fl = __ballot_sync(kFull, bad) ? 1u : 0u;
+        fl |= __ballot_sync(kFull, lost) ? 2u : 0u;
         for (int o = 16; o; o >>= 1) foot += __shfl_xor_sync(kFull, foot, o);
-        bad = foot >= kFeatLimit;
+        b1 = __reduce_add_sync(kFull, b1);
+        kv1 = __reduce_add_sync(kFull, kv1);
+        nloc = warp_max(nloc);
+        if (WPI > 1) {
+            const long long* x = grp.exchange(fl, foot, (long long)b1 | ((long long)kv1 << 32), nloc);
+            fl = 0;
+            foot = 0;
+            long long bk = 0;
+            nloc = 0;
+#pragma unroll
+            for (int k = 0; k < WPI; ++k) {
+                fl |= (unsigned)x[k * 4];
+                foot += x[k * 4 + 1];
+                bk += x[k * 4 + 2];
+                nloc = max(nloc, (int)x[k * 4 + 3]);
+            }
+            b1 = (int)(bk & 0xffffffffLL);
+            kv1 = (int)(bk >> 32);
+        }
+        bad = (fl & 1u) || foot >= kFeatLimit;
+        lost = (fl & 2u) != 0;
     }
     if (bad) {
         if (p.B) {
             const int lim = p.bkv_rows ? H : 1;
-            for (int m = lane; m < lim; m += 32) {
+            for (int m = gl; m < lim; m += GL) {
                 p.B[(int64_t)i * H + m] = 0;
                 p.KV[(int64_t)i * H + m] = 0;
             }
         }
-        if (lane == 0) {
+        if (gl == 0) {
             p.n[i] = 0;
             p.n_adm[i] = 0;
             p.status[i] = TP_ST_BAD_INPUT;
@@ -156,20 +228,17 @@ k1_compact(const __grid_constant__ K1cParams p) {
         return;
     }
     // the m = 1 terms of every running request (index ph(1) = 0 gets no other event)
-    b1 = __reduce_add_sync(kFull, b1);
-    kv1 = __reduce_add_sync(kFull, kv1);
-    lost = __any_sync(kFull, lost);
-    __syncwarp();
-    if (lane == 0) {
+    grp.sync();
+    if (gl == 0) {
         sB[0] += b1;
         sKV[0] += kv1;
     }
-    __syncwarp();
+    grp.sync();
 
     // ---- inclusive scans over the lane segments ----
-    int* segB = sB + lane * (S + P);
-    int* segKV = sKV + lane * (S + P);
-    const int lo = 1 + lane * S, hi = min(lo + S, H + 1);    // the lane's valid m (may be empty)
+    int* segB = sB + gl * (S + P);
+    int* segKV = sKV + gl * (S + P);
+    const int lo = 1 + gl * S, hi = min(lo + S, H + 1);    // the lane's valid m (may be empty)
     int kvmax = 0;
     {
         int sb = 0, skv = 0;
@@ -189,6 +258,15 @@ k1_compact(const __grid_constant__ K1cParams p) {
             }
         }
         int pb = xb - sb, pkv = xkv - skv;
+        if (WPI > 1) {          // add the totals of the group's earlier warps
+            const long long* x = grp.exchange(__shfl_sync(kFull, xb, 31), __shfl_sync(kFull, xkv, 31), 0, 0);
+#pragma unroll
+            for (int k = 0; k < WPI; ++k)
+                if (k < grp.gw) {
+                    pb += (int)x[k * 4];
+                    pkv += (int)x[k * 4 + 1];
+                }
+        }
         for (int k = 0; k < S; k += 4) {
             int4 b = *reinterpret_cast<const int4*>(segB + k);
             int4 v = *reinterpret_cast<const int4*>(segKV + k);
@@ -203,8 +281,7 @@ k1_compact(const __grid_constant__ K1cParams p) {
                                    max(m + 2 <= H ? v.z : 0, m + 3 <= H ? v.w : 0)));
         }
     }
-    __syncwarp();
-    uint32_t st = warp_max(kvmax) > in.kv_cap ? TP_ST_KV_OVER : 0u;
+    uint32_t st = grp.max(kvmax) > in.kv_cap ? TP_ST_KV_OVER : 0u;   // (its barrier also publishes the scan)
 
     // ---- FIFO gate: queued c admitted iff B[1]+1 <= max_batch and max_m KV + KV_c <= kv_cap ----
     // One candidate at a time, lane-strided over its window m = 1..l_c.  Only the window
@@ -214,6 +291,7 @@ k1_compact(const __grid_constant__ K1cParams p) {
     const int forced = p.force_adm ? min(max(p.force_adm[i], 0), nq) : -1;
     const uint32_t lmask = p.lost_mask ? p.lost_mask[i] : 0u;
     const int ncand = forced >= 0 ? forced : nq;
+    if (WPI == 1) __syncwarp();
     if (forced < 0 && ncand > 0 && (st & TP_ST_KV_OVER)) {
         st |= TP_ST_QUEUE_BLOCKED;
     } else {
@@ -225,21 +303,23 @@ k1_compact(const __grid_constant__ K1cParams p) {
                 bool admit = B1 + 1 <= in.max_batch;
                 if (admit) {
                     int mx = 0;
-                    for (int m = 1 + lane; m <= lc; m += 32)   // Eq. 1: KV_c[m] = ceil((m - 1 + q) / N)
+#pragma unroll 4
+                    for (int m = 1 + gl; m <= lc; m += GL)   // Eq. 1: KV_c[m] = ceil((m - 1 + q) / N)
                         mx = max(mx, sKV[ph(m)] + (int)fdN.div((uint32_t)(m + q - 2)) + 1);
-                    admit = warp_max(mx) <= in.kv_cap;
+                    admit = grp.max(mx) <= in.kv_cap;
                 }
                 if (!admit) {
                     st |= TP_ST_QUEUE_BLOCKED;
                     break;
                 }
             }
-            for (int m = 1 + lane; m <= lc; m += 32) {
+#pragma unroll 4
+            for (int m = 1 + gl; m <= lc; m += GL) {
                 const int pi = ph(m);
                 sKV[pi] += (int)fdN.div((uint32_t)(m + q - 2)) + 1;
                 sB[pi] += 1;
             }
-            __syncwarp();
+            grp.sync();
             ++B1;
             ++n_adm;
             nloc = max(nloc, lc);
@@ -247,39 +327,41 @@ k1_compact(const __grid_constant__ K1cParams p) {
         }
     }
     if (forced >= 0 && forced < nq) st |= TP_ST_QUEUE_BLOCKED;
-    const int n = warp_max(nloc);
+    const int n = nloc;                              // group-uniform (admitted l's are uniform)
     if (n == 0) st |= TP_ST_EMPTY;
     else if (lost) st |= TP_ST_BYPASS_LOST;
+    grp.sync();
 
     if (p.B) {
         int* Bo = p.B + (int64_t)i * H;
         int* Ko = p.KV + (int64_t)i * H;
         if (!p.bkv_rows) {
-            if (lane == 0) {
+            if (gl == 0) {
                 Bo[0] = sB[0];
                 Ko[0] = sKV[0];
             }
         } else if ((H & 3) == 0) {   // rows 16-byte aligned: 128-bit stores (groups never straddle)
-            for (int v = lane; v < (H >> 2); v += 32) {
+            for (int v = gl; v < (H >> 2); v += GL) {
                 const int m = 4 * v + 1;
                 reinterpret_cast<int4*>(Bo)[v] = *reinterpret_cast<const int4*>(sB + ph(m));
                 reinterpret_cast<int4*>(Ko)[v] = *reinterpret_cast<const int4*>(sKV + ph(m));
             }
         } else {
-            for (int m = 1 + lane; m <= H; m += 32) {
+            for (int m = 1 + gl; m <= H; m += GL) {
                 Bo[m - 1] = sB[ph(m)];
                 Ko[m - 1] = sKV[ph(m)];
             }
         }
     }
-    if (lane == 0) {
+    if (gl == 0) {
         p.n[i] = n;
         p.n_adm[i] = n_adm;
         p.status[i] = st;
     }
     const int nn = (st & p.skip) ? 0 : n;    // iterations K2 / K3 evaluate
+    const unsigned ltm = (1u << lane) - 1u;
 
-    // ---- runs of equal cells over m = 1..nn (lane segments), first-seen cells claimed ----
+    // ---- runs of equal cells over m = 1..nn, first-seen cells claimed ----
     if (p.run_h) {
         const int nB = p.cut_off[2] - p.cut_off[1], nKV = p.cut_off[3] - p.cut_off[2];
         const int lB = p.rtab_len[0], lKV = p.rtab_len[1];
@@ -294,31 +376,66 @@ k1_compact(const __grid_constant__ K1cParams p) {
             const uint32_t rkv = kv < lKV ? __ldg(tKV + kv) : rank_of(p.cuts + p.cut_off[2], nKV, (float)kv);
             return cell_base + rbk * nk1 + rkv;
         };
-        // lane-strided over m: key, head flag (key != key of m - 1), ballot compaction; the heads
-        // (m, key) are staged in place at plain indices j < #heads so far, which never reach a
-        // position a later iteration still reads (ph(m) >= m - 1)
+        // Group-strided over m (warp gw takes the 32 iterations m0 + 32 gw + lane): key, head flag
+        // (key != key of m - 1), ballot compaction; the heads (m, key) are staged in place at plain
+        // indices j < #heads so far, which never reach a position a later step still reads
+        // (ph(m) >= m - 1).  Across warps: first / last keys and head counts through the exchange
+        // (whose barrier also orders every read of this step before the staging writes).
         int h = 0;
         uint32_t carry = 0xffffffffu;      // key of m0 - 1 (m = 1 always starts a run)
-        for (int m0 = 1; m0 <= nn; m0 += 32) {
-            const int m = m0 + lane;
+        for (int m0 = 1; m0 <= nn; m0 += GL) {
+            const int m = m0 + gl;
             const uint32_t k = m <= nn ? key_at(ph(m)) : 0u;
             uint32_t pk = __shfl_up_sync(kFull, k, 1);
-            if (lane == 0) pk = carry;
-            carry = __shfl_sync(kFull, k, 31);
-            const bool head = m <= nn && k != pk;
-            const unsigned mask = __ballot_sync(kFull, head);
+            const uint32_t kfirst = __shfl_sync(kFull, k, 0), klast = __shfl_sync(kFull, k, 31);
+            const bool head_rest = lane > 0 && m <= nn && k != pk;       // lanes 1..31
+            const unsigned mrest = __ballot_sync(kFull, head_rest);
+            int before = 0;                 // heads of this step in earlier warps
+            bool head0;                     // this warp's lane-0 head flag
+            if (WPI == 1) {
+                head0 = m0 <= nn && kfirst != carry;
+                carry = klast;
+            } else {
+                const long long* x = grp.exchange(kfirst, klast, __popc(mrest), 0);
+                uint32_t prevlast = carry;
+                head0 = false;
+#pragma unroll
+                for (int v = 0; v < WPI; ++v) {
+                    const bool hv = m0 + 32 * v <= nn && (uint32_t)x[v * 4] != prevlast;
+                    if (v < grp.gw) before += (int)x[v * 4 + 2] + hv;
+                    if (v == grp.gw) head0 = hv;
+                    prevlast = (uint32_t)x[v * 4 + 1];
+                }
+                int tot = 0;
+#pragma unroll
+                for (int v = 0; v < WPI; ++v) {
+                    const uint32_t pl = v == 0 ? carry : (uint32_t)x[(v - 1) * 4 + 1];
+                    tot += (int)x[v * 4 + 2] + (m0 + 32 * v <= nn && (uint32_t)x[v * 4] != pl);
+                }
+                carry = prevlast;
+                if (WPI == 1) __syncwarp();
+                const unsigned mask = mrest | (head0 ? 1u : 0u);
+                if (lane == 0 ? head0 : head_rest) {
+                    const int pos = h + before + __popc(mask & ltm);
+                    sKV[pos] = m;
+                    sB[pos] = (int)k;
+                }
+                h += tot;
+                continue;
+            }
             __syncwarp();                  // every lane has read its B / KV before the staging writes
-            if (head) {
-                const int pos = h + __popc(mask & ((1u << lane) - 1u));
+            const unsigned mask = mrest | (head0 ? 1u : 0u);
+            if (lane == 0 ? head0 : head_rest) {
+                const int pos = h + __popc(mask & ltm);
                 sKV[pos] = m;
                 sB[pos] = (int)k;
             }
             h += __popc(mask);
         }
-        __syncwarp();
+        grp.sync();
         // coalesced run records; claims lane-parallel (first claimant appends the cell)
         const size_t row = (size_t)i * H;
-        for (int k = lane; k < h; k += 32) {
+        for (int k = gl; k < h; k += GL) {
             const int m = sKV[k];
             const uint32_t key = (uint32_t)sB[k];
             p.run_m[row + k] = m;
@@ -330,44 +447,88 @@ k1_compact(const __grid_constant__ K1cParams p) {
                 p.cell_tab[key] = idx;
             }
         }
-        if (lane == 0) p.run_h[i] = h;
+        if (gl == 0) p.run_h[i] = h;
     }
 
     // ---- Eq. 4 deadline list: Dmin over end positions (the histogram space is reused) ----
     if (p.end_n) {
-        __syncwarp();
+        grp.sync();
         long long* dmin = reinterpret_cast<long long*>(sB);     // [0, nn], 8 (H + 1) <= 8 arr bytes
-        for (int m = lane; m <= nn; m += 32) dmin[m] = kNoDeadline;
-        __syncwarp();
+        for (int m = gl; m <= nn; m += GL) dmin[m] = kNoDeadline;
+        grp.sync();
         if (nn > 0) {
-            for (int e = lane; e < nr + n_adm; e += 32) {
+            for (int e = gl; e < nr + n_adm; e += GL) {
                 const int64_t j = rb + e;
                 const int4 r = __ldg(&p.req[j]);
                 atomicMin(&dmin[r.z - r.x], slack_ticks(__ldg(&p.t_dead[j]) - in.t_cur));
             }
         }
-        __syncwarp();
+        grp.sync();
         int ne = 0;
         const size_t row = (size_t)i * H;
-        for (int m0 = 1; m0 <= nn; m0 += 32) {
-            const int m = m0 + lane;
+        for (int m0 = 1; m0 <= nn; m0 += GL) {
+            const int m = m0 + gl;
             const long long d = m <= nn ? dmin[m] : kNoDeadline;
-            const bool has = d != kNoDeadline;
-            const unsigned mask = __ballot_sync(kFull, has);
-            if (has) {
-                const int pos = ne + __popc(mask & ((1u << lane) - 1u));
+            const unsigned mask = __ballot_sync(kFull, d != kNoDeadline);
+            int before = 0, tot = __popc(mask);
+            if (WPI > 1) {
+                const long long* x = grp.exchange(__popc(mask), 0, 0, 0);
+                tot = 0;
+#pragma unroll
+                for (int v = 0; v < WPI; ++v) {
+                    if (v < grp.gw) before += (int)x[v * 4];
+                    tot += (int)x[v * 4];
+                }
+            }
+            if (d != kNoDeadline) {
+                const int pos = ne + before + __popc(mask & ltm);
                 p.end_l[row + pos] = m;
                 p.end_d[row + pos] = d;
             }
-            ne += __popc(mask);
+            ne += tot;
         }
-        if (lane == 0) p.end_n[i] = ne;
+        if (gl == 0) p.end_n[i] = ne;
     }
 }
 
 }  // namespace
 
-int project_compact_smem_per_warp(int32_t H) { return 2 * seg_geom(H).arr * (int)sizeof(int); }
+int project_compact_smem_per_warp(int32_t H) { return 2 * seg_geom(H, 32).arr * (int)sizeof(int); }
+
+namespace {
+// TP_K1C_WARPS (1/2/4): warps per instance override (tuning)
+int env_wpi() {
+    const char* v = std::getenv("TP_K1C_WARPS");
+    const int x = v ? std::atoi(v) : 0;
+    return (x == 1 || x == 2 || x == 4) ? x : 0;
+}
+
+template <int WPI>
+int launch_wpi(const K1cParams& p0, int32_t n_inst, int32_t H, cudaStream_t s) {
+    K1cParams p = p0;
+    const SegGeom g = seg_geom(H, 32 * WPI);
+    p.S_log2 = g.S_log2;
+    p.P = g.P;
+    p.arr = g.arr;
+    // instances per CTA: up to kWarpsPerCta / WPI, fewer for long horizons (per-group histograms)
+    const size_t per_group = (size_t)2 * g.arr * sizeof(int);
+    if (per_group > 200 * 1024) return TP_EINVAL;
+    const int gpb = (int)std::max<size_t>(1, std::min<size_t>(kWarpsPerCta / WPI, (100 * 1024) / per_group));
+    const size_t smem = (size_t)gpb * per_group;
+    int dev = 0;
+    if (cudaGetDevice(&dev) != cudaSuccess) return TP_ECUDA;
+    static int attr_bytes[64] = {};
+    if (dev < 64 && attr_bytes[dev] < (int)smem) {
+        if (cudaFuncSetAttribute(k1_compact<WPI>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) !=
+            cudaSuccess)
+            return TP_EINVAL;   // H too large for the per-group histograms
+        attr_bytes[dev] = (int)smem;
+    }
+    const int grid = (n_inst + gpb - 1) / gpb;
+    k1_compact<WPI><<<grid, gpb * WPI * 32, smem, s>>>(p);
+    return cudaPeekAtLastError() == cudaSuccess ? TP_OK : TP_ECUDA;
+}
+}  // namespace
 
 int launch_project_compact(const K2Params& w, const tp_inst* inst, int32_t n_inst, const tp_req* req,
                            int32_t n_req, const double* t_dead, int32_t H, int32_t* B, int32_t* KV, int bkv_rows,
@@ -375,7 +536,6 @@ int launch_project_compact(const K2Params& w, const tp_inst* inst, int32_t n_ins
                            const int32_t* force_adm, const uint32_t* lost_mask) {
     if (n_inst == 0) return TP_OK;
     if (!w.cell_tab || !w.end_n) return TP_EINVAL;
-    const SegGeom g = seg_geom(H);
     K1cParams p;
     p.inst = inst;
     p.req = reinterpret_cast<const int4*>(req);
@@ -392,9 +552,6 @@ int launch_project_compact(const K2Params& w, const tp_inst* inst, int32_t n_ins
     p.force_adm = force_adm;
     p.lost_mask = lost_mask;
     p.skip = skip;
-    p.S_log2 = g.S_log2;
-    p.P = g.P;
-    p.arr = g.arr;
     p.cuts = w.cuts;
     for (int k = 0; k < 5; ++k) p.cut_off[k] = w.cut_off[k];
     p.rtab = w.rtab;
@@ -414,22 +571,19 @@ int launch_project_compact(const K2Params& w, const tp_inst* inst, int32_t n_ins
     p.end_d = w.end_d;
     // cell_count (count - 1) and cell_tab are contiguous: one reset; claimers zero their clamp masks
     if (cudaMemsetAsync(w.cell_count, 0xFF, 4 + (size_t)w.n_cells * 4, s) != cudaSuccess) return TP_ECUDA;
-    // warps per CTA: up to kWarpsPerCta, fewer for long horizons (per-warp histograms)
-    const size_t per_warp = (size_t)2 * g.arr * sizeof(int);
-    if (per_warp > 200 * 1024) return TP_EINVAL;
-    const int wpb = (int)std::max<size_t>(1, std::min<size_t>(kWarpsPerCta, (100 * 1024) / per_warp));
-    const size_t smem = (size_t)wpb * per_warp;
-    int dev = 0;
-    if (cudaGetDevice(&dev) != cudaSuccess) return TP_ECUDA;
-    static int attr_bytes[64] = {};
-    if (dev < 64 && attr_bytes[dev] < (int)smem) {
-        if (cudaFuncSetAttribute(k1_compact, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess)
-            return TP_EINVAL;   // H too large for the per-warp histograms
-        attr_bytes[dev] = (int)smem;
+    // warps per instance: small batches get several warps per instance (the per-instance chain
+    // of dependent loads and reductions is the latency; shorter per-warp loops shorten it), large
+    // batches one (the GPU is full anyway)
+    int dev = 0, sms = 148;
+    if (cudaGetDevice(&dev) == cudaSuccess) cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    static const int wpi_env = env_wpi();
+    const int64_t slots = (int64_t)sms * 32;    // C2 (1,024 instances): 4 warps each; C3: one
+    const int wpi = wpi_env ? wpi_env : ((int64_t)n_inst * 4 <= slots ? 4 : (int64_t)n_inst * 2 <= slots ? 2 : 1);
+    switch (wpi) {
+        case 4: return launch_wpi<4>(p, n_inst, H, s);
+        case 2: return launch_wpi<2>(p, n_inst, H, s);
+        default: return launch_wpi<1>(p, n_inst, H, s);
     }
-    const int grid = (n_inst + wpb - 1) / wpb;
-    k1_compact<<<grid, wpb * 32, smem, s>>>(p);
-    return cudaPeekAtLastError() == cudaSuccess ? TP_OK : TP_ECUDA;
 }
 
 }  // namespace tp
