@@ -453,7 +453,8 @@ def main():
     roof = {"bound": "smem", "kernel": {"direct": "k2_gbdt", "runs": "k2_gbdt<runs> (+ k2_runs pre-pass)",
                                         "cells": "k2_gbdt<cells> (+ k2_runs pre-pass, k2_expand)",
                                         "fused": "k2_gbdt<cells> (+ k2_runs pre-pass)",
-                                        "compact": "k2_gbdt<cells> (runs built by K1c)"}[args.k2],
+                                        "compact": f"k2_cells_phase<{info.depth},2> x {k2_phases(info)} "
+                                                   "tree-resident phases (runs built by K1c)"}[args.k2],
             "achieved": achieved, "peak": peak, "unit": "GB/s",
             "frac": achieved / peak, "traffic": traffic,
             "peak_basis": f"{sms} SMs x 128 B/clk (LDS) x sm_max_mhz {smax:.0f} (MEASURED_PEAKS.json clock)",
@@ -484,7 +485,8 @@ def main():
         "cpu_baseline": cpu,
         "e2e": e2e,
         # our kernels per step: k1_project / k1_compact, [k2_runs], k2_gbdt, [k2_expand], k3_select* / k3_compact
-        "gpu_launches": {"direct": 3, "runs": 4, "cells": 5, "fused": 4, "compact": 3}[args.k2] * args.steps,
+        "gpu_launches": {"direct": 3, "runs": 4, "cells": 5, "fused": 4,
+                         "compact": 2 + k2_phases(info)}[args.k2] * args.steps,
         "clocks": clk,
         "paper_context": "paper controller on host CPU (A100 box): projection <2 ms, model ~3 ms per call, "
                          "scheduler+throttle 35 ms per decision (P:466, P:495, P:557)",
@@ -492,6 +494,13 @@ def main():
     print(json.dumps(line), flush=True)
     if world > 1:
         dist.destroy_process_group()
+
+
+def k2_phases(info):
+    """Launches of k2_cells_phase per step (k2_gbdt.cu launch_phases: <= 200 KB of trees each)."""
+    tw = max(4, 2 << info.depth) * 4
+    per = max(1, min((200 * 1024) // tw, 512))
+    return max(1, -(-info.n_trees // per))
 
 
 def dataclasses_replace(cfg, n_inst):

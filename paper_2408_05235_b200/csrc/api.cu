@@ -402,25 +402,55 @@ int tp_decide_admit(tp_ctx* c, const tp_gbdt* m, const tp_inst* inst, int32_t n_
     int rc = tp::launch_project(inst, n_inst, req, n_req, H, c->B, c->KV, c->n, c->n_adm, status, s);
     // 2. every prefix as a virtual instance, its candidates forced in
     if (!rc) rc = tp::launch_admit_expand(inst, n_inst, c->qc, c->n_adm, status, c->vinst, c->vforce, s);
-    if (!rc) rc = tp::launch_project(c->vinst, V, req, n_req, H, c->vB, c->vKV, c->vn, c->vnadm, c->vstatus, s,
-                                     c->vforce, nullptr);
     // 3. M at the maximum frequency on every prefix state (cell mode, LUT only)
     // (a lost running request does not exempt the prefix from the checks: only BAD / EMPTY are skipped)
-    if (!rc) rc = predict_runs(m, c->vinst, V, c->vB, c->vKV, c->vn, H, freq_mhz + (F - 1), 1, nullptr, c->vstatus,
-                               c->vwork, c->vwork_bytes, stream, TP_ST_BAD_INPUT | TP_ST_EMPTY);
-    // 4. checks 2-3 per prefix, 5. FIFO resolution with lost marks
+    const bool compact = c->k2_mode == TP_K2_COMPACT;
     tp::K2Params w;
     std::memset(&w, 0, sizeof(w));
+    fill_model(m, w);
     tp::runs_workspace_carve(c->vwork, tp::model_cells(m->m), V, H, 1, w);
+    if (compact) {
+        // K1c builds the prefix states' runs and cells directly; K2 evaluates the cells at f_max
+        if (!rc) rc = tp::launch_project_compact(w, c->vinst, V, req, n_req, t_dead, H, nullptr, nullptr, 0, c->vn,
+                                                 c->vnadm, c->vstatus, TP_ST_BAD_INPUT | TP_ST_EMPTY, s, c->vforce,
+                                                 nullptr);
+        tp::K2Params k = w;
+        k.n_inst = V;
+        k.H = H;
+        k.F = 1;
+        k.freq[0] = freq_mhz[F - 1];
+        k.skip = TP_ST_BAD_INPUT | TP_ST_EMPTY;
+        k.runs_ready = 1;
+        if (!rc) rc = tp::launch_gbdt(k, true, s);
+    } else {
+        if (!rc) rc = tp::launch_project(c->vinst, V, req, n_req, H, c->vB, c->vKV, c->vn, c->vnadm, c->vstatus, s,
+                                         c->vforce, nullptr);
+        if (!rc) rc = predict_runs(m, c->vinst, V, c->vB, c->vKV, c->vn, H, freq_mhz + (F - 1), 1, nullptr,
+                                   c->vstatus, c->vwork, c->vwork_bytes, stream, TP_ST_BAD_INPUT | TP_ST_EMPTY);
+    }
+    // 4. checks 2-3 per prefix, 5. FIFO resolution with lost marks
     if (!rc) rc = tp::launch_admit_checks(c->vinst, V, req, t_dead, c->vn, c->vstatus, w, H, tbt_ticks, c->vres, s);
     if (!rc) rc = tp::launch_admit_resolve(n_inst, c->qc, inst, status, c->n_adm, c->vres, c->adm_final, c->lost, s);
     // 6. the throttle on the admitted state (lost marks applied -> bypass)
-    if (!rc) rc = tp::launch_project(inst, n_inst, req, n_req, H, c->B, c->KV, c->n, c->n_adm, status, s,
-                                     c->adm_final, c->lost);
-    if (!rc) rc = tp_predict_ips_runs(m, inst, n_inst, c->B, c->KV, c->n, H, freq_mhz, F, nullptr, status, c->work,
-                                      c->work_bytes, stream);
-    if (!rc) rc = select_ws(m, c->work, inst, n_inst, req, n_req, t_dead, c->n, c->n_adm, H, F, tbt_slo, level,
-                            status, nullptr, c->search, stream);
+    if (compact) {
+        tp::K2Params w2;
+        std::memset(&w2, 0, sizeof(w2));
+        fill_model(m, w2);
+        tp::runs_workspace_carve(c->work, tp::model_cells(m->m), n_inst, H, 1, w2);
+        if (!rc) rc = tp::launch_project_compact(w2, inst, n_inst, req, n_req, t_dead, H, c->B, c->KV, 0, c->n,
+                                                 c->n_adm, status, TP_ST_BAD_INPUT | TP_ST_EMPTY | TP_ST_BYPASS_LOST,
+                                                 s, c->adm_final, c->lost);
+        if (!rc) rc = tp_predict_cells(m, c->work, c->work_bytes, n_inst, H, freq_mhz, F, stream);
+        if (!rc) rc = tp_select_freq_compact(m, c->work, c->work_bytes, n_inst, c->n, H, F, tbt_slo, c->search, level,
+                                             status, stream);
+    } else {
+        if (!rc) rc = tp::launch_project(inst, n_inst, req, n_req, H, c->B, c->KV, c->n, c->n_adm, status, s,
+                                         c->adm_final, c->lost);
+        if (!rc) rc = tp_predict_ips_runs(m, inst, n_inst, c->B, c->KV, c->n, H, freq_mhz, F, nullptr, status,
+                                          c->work, c->work_bytes, stream);
+        if (!rc) rc = select_ws(m, c->work, inst, n_inst, req, n_req, t_dead, c->n, c->n_adm, H, F, tbt_slo, level,
+                                status, nullptr, c->search, stream);
+    }
     if (!rc && n_adm_out && cudaMemcpyAsync(n_adm_out, c->n_adm, (size_t)n_inst * 4, cudaMemcpyDeviceToDevice, s))
         rc = TP_ECUDA;
     if (!rc && adm_lost_out &&

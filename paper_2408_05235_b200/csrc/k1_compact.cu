@@ -10,11 +10,13 @@
 //     carry one, ascending.
 // The B/KV curves never leave the SM unless the caller asks for them (bkv_rows).
 //
-// One WARP per instance (the CTA-per-instance K1 spends most of its issue slots on block-wide
-// phases and barriers at large batches): the events go to a per-warp shared histogram, the scans
-// and the gate use warp shuffles only (no __syncthreads anywhere).  Lane t owns the contiguous
-// segment m in [1 + t*S, 1 + (t+1)*S) (S a power of two >= 4); segments are padded by P = 4 words
-// when S/4 is even so that 8 consecutive lanes' 128-bit accesses fall in distinct bank quads.
+// One to four WARPS per instance (the CTA-per-instance K1 spends most of its issue slots on
+// block-wide phases and barriers at large batches; at small batches a few warps per instance
+// shorten its chain of dependent loads): the events go to a per-instance shared histogram, the
+// scans and the gate use warp shuffles plus, across the instance's warps, a named barrier and
+// shared exchange slots.  Group lane t owns the contiguous segment m in [1 + t*S, 1 + (t+1)*S)
+// (S a power of two >= 4); segments are padded by P = 4 words when S/4 is even so that 8
+// consecutive lanes' 128-bit accesses fall in distinct bank quads.
 #include <algorithm>
 #include <cstdlib>
 

@@ -329,3 +329,27 @@ def test_compact_geometry(gpu, oracle_mod, n_inst, H):
     inputs = W.config_inputs(cfg)
     assert_parity(run_gpu(gpu, blob, inputs, want_tr=False, mode="compact"),
                   run_oracle(oracle_mod, blob, inputs, want_tr=False))
+
+
+def test_ctx_ips_grid_on_demand(gpu, oracle_mod):
+    """A context created for a cell-mode model runs the compact path and owns no ips grid until a
+    mode that writes it is selected (C5-sized contexts would otherwise hold a 34 GB grid)."""
+    tp, runner = gpu
+    cfg = W.CONFIGS["P1"]
+    blob = W.write_blob(W.config_ensemble(cfg))
+    inputs = W.config_inputs(cfg)
+    model = tp.Gbdt(blob, 0)
+    I, R = len(inputs["inst"]), len(inputs["req"])
+    ctx = tp.Ctx(0, I, R, inputs["H"], len(inputs["freq"]), model)
+    assert not ctx.buffers()[4]
+    ref = run_oracle(oracle_mod, blob, inputs, want_grid=False, want_tr=False)
+    for mode in (tp.K2_COMPACT, tp.K2_RUNS, tp.K2_DIRECT, tp.K2_COMPACT):
+        ctx.set_k2_mode(mode)
+        if mode != tp.K2_COMPACT:
+            assert ctx.buffers()[4]
+        r = runner.Round(inputs, "cuda:0", k2_mode="direct")
+        ctx.decide(model, r.inst, I, r.req, R, r.t_dead, inputs["freq"], inputs["tbt_slo"], r.level, r.status)
+        torch.cuda.synchronize()
+        assert np.array_equal(r.level.cpu().numpy(), ref["level"])
+        assert np.array_equal(r.status.cpu().numpy().view(np.uint32), ref["status"])
+    assert ctx.buffers()[4]          # allocated by the first non-compact mode, kept
