@@ -126,7 +126,7 @@ struct Group {
 };
 
 template <int WPI>
-__global__ void __launch_bounds__(kWarpsPerCta * 32)
+__global__ void __launch_bounds__(kWarpsPerCta * 32, WPI == 1 ? 6 : 8)
 k1_compact(const __grid_constant__ K1cParams p) {
     extern __shared__ __align__(16) int smem[];
     constexpr int GL = 32 * WPI;                       // group lanes
