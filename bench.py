@@ -315,17 +315,19 @@ def main():
     stream = torch.cuda.current_stream(dev)
     flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)     # > 126 MB L2
 
-    def step(evs=None):
+    def step(evs=None, split=True):
+        # split=False: events only around the whole step (an event between two kernels stops the
+        # second from launching early -- programmatic dependent launch -- and costs ~4 us each)
         if evs:
             evs[0].record(stream)
         rnd.project(stream)
-        if evs:
+        if evs and split:
             evs[1].record(stream)
         rnd.predict(model, stream)
-        if evs:
+        if evs and split:
             evs[2].record(stream)
         rnd.select(stream)
-        if evs:
+        if evs and split:
             evs[3].record(stream)
         if world > 1:
             if dist_test:
@@ -361,13 +363,20 @@ def main():
     time.sleep(0.3)
     for k in range(args.steps):
         flush.zero_()                      # untimed L2 flush between timed steps
-        step(evs[k])
+        step(evs[k], split=False)
     torch.cuda.synchronize(dev)
     clk = clocks.stop()
     if world > 1:
         dist.barrier()
-    per = np.array([[e[j].elapsed_time(e[j + 1]) for j in range(4)] for e in evs])   # ms
-    t_total = float(per.sum())
+    t_total = float(sum(e[0].elapsed_time(e[4]) for e in evs))          # ms, the K timed steps
+    # per-kernel breakdown (and the K2 time of the roofline): a second pass of K steps with events
+    # between the kernels, same inputs, same L2 flushes
+    evk = [[torch.cuda.Event(enable_timing=True) for _ in range(5)] for _ in range(args.steps)]
+    for k in range(args.steps):
+        flush.zero_()
+        step(evk[k])
+    torch.cuda.synchronize(dev)
+    per = np.array([[e[j].elapsed_time(e[j + 1]) for j in range(4)] for e in evk])   # ms
     k_ms = per.mean(axis=0)
     # the north_star's direct K2 (one descent per grid point), timed on the same inputs for reference
     d_ms = None
@@ -480,7 +489,10 @@ def main():
                    "search": args.search},
         "grid_evals_per_sec": grid_per_s,
         "per_kernel_ms": {"k1_project": k_ms[0], "k2_gbdt": k_ms[1], "k3_select": k_ms[2],
-                          "gather": k_ms[3]},
+                          "gather": k_ms[3],
+                          "note": "from a second pass of the same steps with events between the kernels "
+                                  "(those events stop programmatic dependent launch; the timed steps carry "
+                                  "events only at their ends)"},
         "roofline": roof,
         "cpu_baseline": cpu,
         "e2e": e2e,
