@@ -283,7 +283,8 @@ k1_compact(const __grid_constant__ K1cParams p) {
                                    max(m + 2 <= H ? v.z : 0, m + 3 <= H ? v.w : 0)));
         }
     }
-    uint32_t st = grp.max(kvmax) > in.kv_cap ? TP_ST_KV_OVER : 0u;   // (its barrier also publishes the scan)
+    int kvb = grp.max(kvmax);          // (its barrier also publishes the scan)
+    uint32_t st = kvb > in.kv_cap ? TP_ST_KV_OVER : 0u;
 
     // ---- FIFO gate: queued c admitted iff B[1]+1 <= max_batch and max_m KV + KV_c <= kv_cap ----
     // One candidate at a time, lane-strided over its window m = 1..l_c.  Only the window
@@ -301,19 +302,28 @@ k1_compact(const __grid_constant__ K1cParams p) {
         for (int c = 0; c < ncand; ++c) {
             const int4 r = __ldg(&p.req[rb + nr + c]);  // a = 0 (validated)
             const int q = r.y, lc = r.z;
+            // kvb: an upper bound of max_m KV[m] (exact after the scan).  KV_c[m] <= KV_c[l_c] on
+            // the window, so kvb + KV_c[l_c] <= kv_cap admits without scanning the window
+            const int kvc_top = (int)fdN.div((uint32_t)(lc + q - 2)) + 1;
             if (forced < 0) {
                 bool admit = B1 + 1 <= in.max_batch;
-                if (admit) {
+                if (admit && kvb + kvc_top > in.kv_cap) {
                     int mx = 0;
 #pragma unroll 4
                     for (int m = 1 + gl; m <= lc; m += GL)   // Eq. 1: KV_c[m] = ceil((m - 1 + q) / N)
                         mx = max(mx, sKV[ph(m)] + (int)fdN.div((uint32_t)(m + q - 2)) + 1);
-                    admit = grp.max(mx) <= in.kv_cap;
+                    mx = grp.max(mx);
+                    admit = mx <= in.kv_cap;
+                    kvb = max(kvb, mx);              // past the window KV is unchanged (<= kvb)
+                } else {
+                    kvb += kvc_top;
                 }
                 if (!admit) {
                     st |= TP_ST_QUEUE_BLOCKED;
                     break;
                 }
+            } else {
+                kvb += kvc_top;
             }
 #pragma unroll 4
             for (int m = 1 + gl; m <= lc; m += GL) {
