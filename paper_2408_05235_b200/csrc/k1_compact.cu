@@ -171,6 +171,8 @@ k1_compact(const __grid_constant__ K1cParams p) {
             bad |= eb;
             if (eb) continue;
             const int a = r.x, q = r.y, l = (int)l64, aq = a + q;
+            if (p.end_n)   // the deadline list reads t_dead at the end: start its trip to L2 now
+                asm volatile("prefetch.global.L2 [%0];" ::"l"(p.t_dead + rb + e));
             foot += (int64_t)fdN.div((uint32_t)(aq + l - 2)) + 1;            // ceil((a+l-1+q)/N)
             if (e < nr) {
                 nloc = max(nloc, l);
