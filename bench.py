@@ -368,7 +368,8 @@ def main():
     clk = clocks.stop()
     if world > 1:
         dist.barrier()
-    t_total = float(sum(e[0].elapsed_time(e[4]) for e in evs))          # ms, the K timed steps
+    step_ms = np.array([e[0].elapsed_time(e[4]) for e in evs])            # ms, the K timed steps
+    t_total = float(step_ms.sum())
     # per-kernel breakdown (and the K2 time of the roofline): a second pass of K steps with events
     # between the kernels, same inputs, same L2 flushes
     evk = [[torch.cuda.Event(enable_timing=True) for _ in range(5)] for _ in range(args.steps)]
@@ -488,6 +489,8 @@ def main():
                    "l2": "flushed between timed steps (256 MiB device write, untimed)", "k2": args.k2,
                    "search": args.search},
         "grid_evals_per_sec": grid_per_s,
+        "step_ms_pctl": {"p10": float(np.percentile(step_ms, 10)), "p50": float(np.percentile(step_ms, 50)),
+                         "p90": float(np.percentile(step_ms, 90)), "rank": "0"},
         "per_kernel_ms": {"k1_project": k_ms[0], "k2_gbdt": k_ms[1], "k3_select": k_ms[2],
                           "gather": k_ms[3],
                           "note": "from a second pass of the same steps with events between the kernels "
