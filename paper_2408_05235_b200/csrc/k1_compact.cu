@@ -26,6 +26,7 @@ namespace tp {
 namespace {
 
 constexpr int kWarpsPerCta = 4;
+template <int WPI> __host__ __device__ constexpr int cta_warps() { return WPI > kWarpsPerCta ? WPI : kWarpsPerCta; }
 constexpr unsigned kFull = 0xffffffffu;
 
 struct SegGeom {
@@ -126,11 +127,11 @@ struct Group {
 };
 
 template <int WPI>
-__global__ void __launch_bounds__(kWarpsPerCta * 32, WPI == 1 ? 6 : 8)
+__global__ void __launch_bounds__(cta_warps<WPI>() * 32, WPI == 1 ? 6 : 32 / cta_warps<WPI>())
 k1_compact(const __grid_constant__ K1cParams p) {
     extern __shared__ __align__(16) int smem[];
     constexpr int GL = 32 * WPI;                       // group lanes
-    constexpr int NG = kWarpsPerCta / WPI;             // groups (instances) per full CTA
+    constexpr int NG = cta_warps<WPI>() / WPI;         // groups (instances) per full CTA
     __shared__ long long s_x[WPI > 1 ? NG : 1][2 * WPI * 4];
     const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
     const int g = w / WPI;
@@ -514,7 +515,7 @@ namespace {
 int env_wpi() {
     const char* v = std::getenv("TP_K1C_WARPS");
     const int x = v ? std::atoi(v) : 0;
-    return (x == 1 || x == 2 || x == 4) ? x : 0;
+    return (x == 1 || x == 2 || x == 4 || x == 8) ? x : 0;
 }
 
 template <int WPI>
@@ -527,7 +528,7 @@ int launch_wpi(const K1cParams& p0, int32_t n_inst, int32_t H, cudaStream_t s) {
     // instances per CTA: up to kWarpsPerCta / WPI, fewer for long horizons (per-group histograms)
     const size_t per_group = (size_t)2 * g.arr * sizeof(int);
     if (per_group > 200 * 1024) return TP_EINVAL;
-    const int gpb = (int)std::max<size_t>(1, std::min<size_t>(kWarpsPerCta / WPI, (100 * 1024) / per_group));
+    const int gpb = (int)std::max<size_t>(1, std::min<size_t>(cta_warps<WPI>() / WPI, (100 * 1024) / per_group));
     const size_t smem = (size_t)gpb * per_group;
     int dev = 0;
     if (cudaGetDevice(&dev) != cudaSuccess) return TP_ECUDA;
@@ -594,6 +595,7 @@ int launch_project_compact(const K2Params& w, const tp_inst* inst, int32_t n_ins
     const int64_t slots = (int64_t)sms * 32;    // C2 (1,024 instances): 4 warps each; C3: one
     const int wpi = wpi_env ? wpi_env : ((int64_t)n_inst * 4 <= slots ? 4 : (int64_t)n_inst * 2 <= slots ? 2 : 1);
     switch (wpi) {
+        case 8: return launch_wpi<8>(p, n_inst, H, s);
         case 4: return launch_wpi<4>(p, n_inst, H, s);
         case 2: return launch_wpi<2>(p, n_inst, H, s);
         default: return launch_wpi<1>(p, n_inst, H, s);
