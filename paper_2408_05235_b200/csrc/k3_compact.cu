@@ -22,10 +22,11 @@ namespace {
 
 constexpr int kWarpsPerCta = 8;
 constexpr unsigned kFull = 0xffffffffu;
-// W = 1 (large batches, throughput): 8 CTAs per SM and 4 LUT rows prefetched; W > 1 (small
-// batches, latency): 4 CTAs per SM and 8 rows prefetched (measured on C3 / C2)
+// W = 1 (large batches, throughput): 8 CTAs per SM and 2 LUT rows prefetched; W > 1 (small
+// batches, latency): 4 CTAs per SM, 8 rows prefetched and the next run chunk loaded ahead
+// (measured on C3 / C2)
 #ifndef TP_K3C_PREFETCH
-#define TP_K3C_PREFETCH 4
+#define TP_K3C_PREFETCH 2
 #endif
 #ifndef TP_K3C_MINB
 #define TP_K3C_MINB 8
@@ -143,12 +144,17 @@ k3_compact(const __grid_constant__ K3cParams p) {
                 nx_key = __ldg(p.run_key + row + k);
             }
         };
-        load_chunk(ka);
+        // W = 1 (large batches, 8 CTAs/SM at 32 registers): no look-ahead load -- the registers it
+        // needs cost more in spills than it saves in latency (C3: 535 -> 505 us with 2-row prefetch)
+        constexpr bool kNext = W > 1;
+        if constexpr (kNext) load_chunk(ka);
         for (int kb = ka; kb < kz; kb += 32) {
+            if constexpr (!kNext) load_chunk(kb);
             const int s_k = nx_s, len_k = nx_len;
             const int rr = (kb + lane < kz) ? __ldcg(p.cell_tab + nx_key) : 0;
             const int roff = rr * F;                  // the run's LUT row offset (< 2^27)
-            if (kb + 32 < kz) load_chunk(kb + 32);
+            if constexpr (kNext)
+                if (kb + 32 < kz) load_chunk(kb + 32);
             if (kb + lane < kz) cm |= __ldcg(p.cell_clamp + rr);
             const int cnt = min(32, kz - kb);
             constexpr int kPrefetch = W == 1 ? TP_K3C_PREFETCH : 8;
