@@ -88,3 +88,22 @@ def test_binding_has_no_cpu_path():
             if fn.endswith((".py", ".cu", ".cuh", ".h", ".cpp")):
                 txt = open(os.path.join(dirpath, fn)).read()
                 assert not re.search(r"^\s*(from|import)\s+oracle|liboracle|oracle\.", txt, re.M), fn
+
+
+def test_compact_entry_validation(tp):
+    """The compact path's entries reject bad arguments on the host (no CUDA call is made)."""
+    L = tp._L
+    vp = ctypes.c_void_p(1)
+    f = np.array([1000.0, 1200.0], np.float32)
+    fd = f.ctypes.data
+    # no model, bad H, bad bkv_rows, B without KV
+    assert L.tp_project_compact(None, vp, 1 << 20, vp, 1, vp, 1, vp, 8, None, None, 0, vp, vp, vp, None) == tp.TP_EINVAL
+    assert L.tp_project_compact(None, vp, 1 << 20, vp, 1, vp, 1, vp, 0, None, None, 0, vp, vp, vp, None) == tp.TP_EINVAL
+    assert L.tp_project_compact(None, vp, 1 << 20, vp, 1, vp, 1, vp, 8, vp, None, 0, vp, vp, vp, None) == tp.TP_EINVAL
+    assert L.tp_project_compact(None, vp, 1 << 20, vp, 1, vp, 1, vp, 8, vp, vp, 2, vp, vp, vp, None) == tp.TP_EINVAL
+    assert L.tp_predict_cells(None, vp, 1 << 20, 1, 8, fd, 2, None) == tp.TP_EINVAL
+    # F out of [1, 32], bad search order, tbt_slo out of range
+    assert L.tp_select_freq_compact(None, vp, 1 << 20, 1, vp, 8, 0, 0.2, 0, vp, vp, None) == tp.TP_EINVAL
+    assert L.tp_select_freq_compact(None, vp, 1 << 20, 1, vp, 8, 33, 0.2, 0, vp, vp, None) == tp.TP_EINVAL
+    assert L.tp_select_freq_compact(None, vp, 1 << 20, 1, vp, 8, 2, 0.2, 2, vp, vp, None) == tp.TP_EINVAL
+    assert L.tp_select_freq_compact(None, vp, 1 << 20, 1, vp, 8, 2, 100.0, 0, vp, vp, None) == tp.TP_EINVAL
