@@ -17,6 +17,7 @@
 //  * Persistent-style grid (#SMs x occupancy CTAs); tiles are split evenly over CTAs by a
 //    per-CTA scan of the per-instance tile counts.
 #include <algorithm>
+#include <type_traits>
 #include <cstdlib>
 
 #include "tp_internal.cuh"
@@ -549,18 +550,17 @@ k2_cells_phase(const __grid_constant__ K2Params p, int t_begin, int t_count, int
     const int64_t t0 = U * blockIdx.x / gridDim.x, t1 = U * (blockIdx.x + 1) / gridDim.x;
     const int nB = p.cut_off[2] - p.cut_off[1], nKV = p.cut_off[3] - p.cut_off[2];
     const uint32_t nk1 = (uint32_t)nKV + 1, nb1 = (uint32_t)nB + 1;
-    for (int64_t task = t0 + tid; task < t1; task += blockDim.x) {   // (no task: the CTA still drains its TMA)
-        const int ug = (int)(task / ncell);
-        const int cidx = (int)(task - (int64_t)ug * ncell);
-        const int u0 = ug * RU;
+    // One work item = RR rows of one cell (levels u0 .. u0 + RR - 1), all trees of the phase.
+    auto item = [&](auto rr_tag, int cidx, int u0) {
+        constexpr int RR = decltype(rr_tag)::value;
         const uint32_t c = p.cell_list[cidx];
         const uint32_t rkv = c % nk1;
         const uint32_t rb = (c / nk1) % nb1, rtp = c / (nk1 * nb1);
         const uint32_t xlo = rtp | (rb << 16);
-        uint32_t xhi[RU];
-        float acc[RU];
+        uint32_t xhi[RR];
+        float acc[RR];
 #pragma unroll
-        for (int r = 0; r < RU; ++r) {
+        for (int r = 0; r < RR; ++r) {
             const int u = min(u0 + r, p.F - 1);
             xhi[r] = rkv | (s_rf[u] << 16);
             acc[r] = first ? p.base : p.lut[(size_t)cidx * p.F + u];
@@ -571,26 +571,26 @@ k2_cells_phase(const __grid_constant__ K2Params p, int t_begin, int t_count, int
             const int nt = min(kPhaseChunkTrees, t_count - ch * kPhaseChunkTrees);
             auto tree = [&](int tt) {
                 const uint32_t* tw = cw + tt * TW;
-                uint32_t idx[RU];
+                uint32_t idx[RR];
                 if constexpr (D >= 2) {
                     const uint32_t w1 = tw[1];
                     const uint2 w23 = *reinterpret_cast<const uint2*>(tw + 2);
 #pragma unroll
-                    for (int r = 0; r < RU; ++r) {
+                    for (int r = 0; r < RR; ++r) {
                         const bool c0 = prmt(xlo, xhi[r], w1) > ~w1;
                         idx[r] = step_from(c0 ? 6u : 4u, c0 ? w23.y : w23.x, xlo, xhi[r]);
                     }
                 } else {
 #pragma unroll
-                    for (int r = 0; r < RU; ++r) idx[r] = 1u;
+                    for (int r = 0; r < RR; ++r) idx[r] = 1u;
                 }
 #pragma unroll
                 for (int d = (D >= 2 ? 2 : 0); d < D; ++d) {
 #pragma unroll
-                    for (int r = 0; r < RU; ++r) idx[r] = descend(idx[r], tw[idx[r]], xlo, xhi[r]);
+                    for (int r = 0; r < RR; ++r) idx[r] = descend(idx[r], tw[idx[r]], xlo, xhi[r]);
                 }
 #pragma unroll
-                for (int r = 0; r < RU; ++r) acc[r] = __fadd_rn(acc[r], __uint_as_float(tw[idx[r]]));
+                for (int r = 0; r < RR; ++r) acc[r] = __fadd_rn(acc[r], __uint_as_float(tw[idx[r]]));
             };
             if (nt == kPhaseChunkTrees) {
 #pragma unroll
@@ -602,7 +602,7 @@ k2_cells_phase(const __grid_constant__ K2Params p, int t_begin, int t_count, int
         if (last) {
             uint32_t cmask = 0;
 #pragma unroll
-            for (int r = 0; r < RU; ++r) {
+            for (int r = 0; r < RR; ++r) {
                 const float v = acc[r];
                 const float cl = isnan(v) ? 0x1p-4f : fminf(fmaxf(v, 0x1p-4f), 0x1p17f);
                 if (u0 + r < p.F) {
@@ -614,11 +614,32 @@ k2_cells_phase(const __grid_constant__ K2Params p, int t_begin, int t_count, int
             if (cmask) atomicOr(p.cell_clamp + cidx, cmask);
         } else {
 #pragma unroll
-            for (int r = 0; r < RU; ++r)
+            for (int r = 0; r < RR; ++r)
                 if (u0 + r < p.F) p.lut[(size_t)cidx * p.F + u0 + r] = acc[r];
         }
+    };
+    // The CTA's RU-row tasks [t0, t1): the first P (a multiple of 4 SMSPs x 32 lanes) run as
+    // RU-row items, so every SMSP gets the same number of warp-items; with RU = 2 the remaining
+    // tasks run as single-row items (two per task), so the ragged end costs half-size warp-items
+    // instead of one more full round on some SMSPs.
+    const int64_t ntask = t1 - t0;
+    const int64_t P = (RU == 2) ? (ntask / 128) * 128 : ntask;
+    const int64_t nitems = P + (ntask - P) * (RU == 2 ? 2 : 0);
+    for (int64_t it = tid; it < nitems; it += blockDim.x) {   // (no item: the CTA still drains its TMA)
+        if (it < P) {                                         // warp-uniform: P is a multiple of 32
+            const int64_t task = t0 + it;
+            const int ug = (int)(task / ncell);
+            const int cidx = (int)(task - (int64_t)ug * ncell);
+            item(std::integral_constant<int, RU>{}, cidx, ug * RU);
+        } else if constexpr (RU == 2) {
+            const int64_t s1 = it - P;
+            const int64_t task = t0 + P + (s1 >> 1);
+            const int ug = (int)(task / ncell);
+            const int cidx = (int)(task - (int64_t)ug * ncell);
+            item(std::integral_constant<int, 1>{}, cidx, ug * 2 + (int)(s1 & 1));
+        }
     }
-    if (tid == 0 && t0 + tid >= t1)            // no task: wait for the bulk copies before exiting
+    if (tid == 0 && nitems == 0)               // no task: wait for the bulk copies before exiting
         for (int ch = 0; ch < nchunks; ++ch) mbar_wait(&bar[ch], 0u);
 }
 
