@@ -412,11 +412,16 @@ def main():
         ctx = tp.Ctx(local, I, R, rnd.H, rnd.F, model if args.k2 in ("cells", "fused", "compact") else None)
         ctx.set_k2_mode({"direct": tp.K2_DIRECT, "compact": tp.K2_COMPACT}.get(args.k2, tp.K2_RUNS))
         ctx.set_search(args.search)
-        h_inst = torch.from_numpy(inputs["inst"].view(np.uint8)).pin_memory()
-        h_req = torch.from_numpy(inputs["req"].view(np.uint8)).pin_memory()
-        h_td = torch.from_numpy(inputs["t_dead"]).pin_memory()
-        h_level = torch.empty(max(I, 1), dtype=torch.int32).pin_memory()
-        h_status = torch.empty(max(I, 1), dtype=torch.int32).pin_memory()
+        # one pinned host buffer [inst | req | t_dead] (tp_decide_host then copies it in one go) and
+        # one [level | status] buffer for the results
+        bi, br, bd = inputs["inst"].nbytes, inputs["req"].nbytes, inputs["t_dead"].nbytes
+        h_in = torch.empty(bi + br + bd, dtype=torch.uint8).pin_memory()
+        h_in[:bi].copy_(torch.from_numpy(inputs["inst"].view(np.uint8)))
+        h_in[bi:bi + br].copy_(torch.from_numpy(inputs["req"].view(np.uint8)))
+        h_in[bi + br:].copy_(torch.from_numpy(np.ascontiguousarray(inputs["t_dead"]).view(np.uint8)))
+        h_inst, h_req, h_td = h_in[:bi], h_in[bi:bi + br], h_in[bi + br:].view(torch.float64)
+        h_out = torch.empty((2, max(I, 1)), dtype=torch.int32).pin_memory()
+        h_level, h_status = h_out[0], h_out[1]
         ke = args.e2e_steps or args.steps
         for _ in range(3):
             ctx.decide_host(model, h_inst, I, h_req, R, h_td, rnd.freq, rnd.tbt, h_level, h_status, stream)

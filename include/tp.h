@@ -297,7 +297,10 @@ int tp_decide(tp_ctx* c, const tp_gbdt* m, const tp_inst* inst, int32_t n_inst, 
 
 /* Same with HOST inputs/outputs: enqueues host->device copies of inst/req/t_dead, the three
  * kernels and device->host copies of level/status, all on `stream`.  Outputs are valid after
- * the stream is synchronised.  Use pinned host memory for asynchronous copies. */
+ * the stream is synchronised.  Use pinned host memory for asynchronous copies.  When the host
+ * inputs are packed back to back (h_req == (char*)h_inst + n_inst * sizeof(tp_inst) and h_t_dead ==
+ * (char*)h_req + n_req * sizeof(tp_req)) they travel in ONE copy, and when h_status == h_level +
+ * n_inst the outputs come back in one copy. */
 int tp_decide_host(tp_ctx* c, const tp_gbdt* m, const tp_inst* h_inst, int32_t n_inst,
                    const tp_req* h_req, int32_t n_req, const double* h_t_dead,
                    const float* freq_mhz, int32_t F, float tbt_slo, int32_t* h_level,

@@ -28,7 +28,6 @@ struct tp_ctx {
     int device;
     int32_t n_inst_max, n_req_max, H, F_max;
     int32_t *B, *KV, *n, *n_adm, *level;
-    uint32_t* status;
     float* ips;
     void* work;
     size_t work_bytes;
@@ -43,9 +42,7 @@ struct tp_ctx {
     uint2* vres;
     void* vwork;
     size_t vwork_bytes;
-    tp_inst* inst;
-    tp_req* req;
-    double* t_dead;
+    void* stage;     // tp_decide_host's device copy of the inputs: [inst | req | t_dead]
 };
 
 extern "C" {
@@ -334,14 +331,13 @@ int tp_ctx_create(int device, const tp_gbdt* model, int32_t n_inst_max, int32_t 
     const size_t I = (size_t)(n_inst_max > 0 ? n_inst_max : 1), R = (size_t)(n_req_max > 0 ? n_req_max : 1);
     bool ok = cudaMalloc(&c->B, I * H * 4) == cudaSuccess && cudaMalloc(&c->KV, I * H * 4) == cudaSuccess &&
               cudaMalloc(&c->n, I * 4) == cudaSuccess && cudaMalloc(&c->n_adm, I * 4) == cudaSuccess &&
-              cudaMalloc(&c->level, I * 4) == cudaSuccess && cudaMalloc(&c->status, I * 4) == cudaSuccess &&
+              cudaMalloc(&c->level, I * 8) == cudaSuccess &&   // [level | status] of the last call, contiguous
               // the ips grid only for the paths that write it (allocated on demand by set_k2_mode)
               (c->cells_model || cudaMalloc(&c->ips, I * F_max * H * 4) == cudaSuccess) &&
               cudaMalloc(&c->work, c->work_bytes = tp::runs_workspace_bytes(model ? tp::model_cells(model->m) : 0,
                                                                             (int32_t)I, H, F_max)) == cudaSuccess &&
-              cudaMalloc(&c->inst, I * sizeof(tp_inst)) == cudaSuccess &&
-              cudaMalloc(&c->req, R * sizeof(tp_req)) == cudaSuccess &&
-              cudaMalloc(&c->t_dead, R * sizeof(double)) == cudaSuccess;
+              // host-input staging [inst | req | t_dead], carved per call (tp_decide_host)
+              cudaMalloc(&c->stage, I * sizeof(tp_inst) + R * (sizeof(tp_req) + sizeof(double))) == cudaSuccess;
     cudaSetDevice(prev);
     if (!ok) {
         tp_ctx_free(c);
@@ -356,8 +352,8 @@ int tp_ctx_free(tp_ctx* c) {
     int prev = 0;
     cudaGetDevice(&prev);
     cudaSetDevice(c->device);
-    void* ptrs[] = {c->B,     c->KV,    c->n,      c->n_adm,     c->level, c->status, c->ips,   c->work,
-                    c->inst,  c->req,   c->t_dead, c->vinst,     c->vforce, c->vB,   c->vKV,   c->vn,
+    void* ptrs[] = {c->B,     c->KV,    c->n,      c->n_adm,     c->level, c->ips,   c->work,
+                    c->stage, c->vinst,     c->vforce, c->vB,   c->vKV,   c->vn,
                     c->vnadm, c->adm_final, c->vstatus, c->lost, c->vres,  c->vwork};
     for (void* p : ptrs)
         if (p) cudaFree(p);
@@ -536,16 +532,34 @@ int tp_decide_host(tp_ctx* c, const tp_gbdt* m, const tp_inst* h_inst, int32_t n
     if (n_inst > 0 && (!h_inst || !h_level || !h_status || (n_req > 0 && (!h_req || !h_t_dead)))) return TP_EINVAL;
     if (!freq_ok(freq_mhz, F) || F > c->F_max || !tbt_ok(tbt_slo)) return TP_EINVAL;
     cudaStream_t s = S(stream);
-    if (cudaMemcpyAsync(c->inst, h_inst, (size_t)n_inst * sizeof(tp_inst), cudaMemcpyHostToDevice, s) ||
-        cudaMemcpyAsync(c->req, h_req, (size_t)n_req * sizeof(tp_req), cudaMemcpyHostToDevice, s) ||
-        cudaMemcpyAsync(c->t_dead, h_t_dead, (size_t)n_req * sizeof(double), cudaMemcpyHostToDevice, s))
+    // device staging laid out like a packed host buffer [inst | req | t_dead] (offsets 16-byte /
+    // 8-byte aligned for any counts); when the caller's buffers are packed that way, one copy
+    char* base = static_cast<char*>(c->stage);
+    const size_t bi = (size_t)n_inst * sizeof(tp_inst), br = (size_t)n_req * sizeof(tp_req),
+                 bd = (size_t)n_req * sizeof(double);
+    tp_inst* d_inst = reinterpret_cast<tp_inst*>(base);
+    tp_req* d_req = reinterpret_cast<tp_req*>(base + bi);
+    double* d_dead = reinterpret_cast<double*>(base + bi + br);
+    const char* hi = reinterpret_cast<const char*>(h_inst);
+    const bool packed = n_inst > 0 && n_req > 0 && reinterpret_cast<const char*>(h_req) == hi + bi &&
+                        reinterpret_cast<const char*>(h_t_dead) == hi + bi + br;
+    if (packed) {
+        if (cudaMemcpyAsync(base, h_inst, bi + br + bd, cudaMemcpyHostToDevice, s)) return TP_ECUDA;
+    } else if (cudaMemcpyAsync(d_inst, h_inst, bi, cudaMemcpyHostToDevice, s) ||
+               (br && cudaMemcpyAsync(d_req, h_req, br, cudaMemcpyHostToDevice, s)) ||
+               (bd && cudaMemcpyAsync(d_dead, h_t_dead, bd, cudaMemcpyHostToDevice, s))) {
         return TP_ECUDA;
-    int rc = tp_decide(c, m, c->inst, n_inst, c->req, n_req, c->t_dead, freq_mhz, F, tbt_slo, c->level, c->status,
-                       stream);
+    }
+    int32_t* d_level = c->level;
+    uint32_t* d_status = reinterpret_cast<uint32_t*>(c->level + n_inst);
+    int rc = tp_decide(c, m, d_inst, n_inst, d_req, n_req, d_dead, freq_mhz, F, tbt_slo, d_level, d_status, stream);
     if (rc) return rc;
-    if (cudaMemcpyAsync(h_level, c->level, (size_t)n_inst * 4, cudaMemcpyDeviceToHost, s) ||
-        cudaMemcpyAsync(h_status, c->status, (size_t)n_inst * 4, cudaMemcpyDeviceToHost, s))
+    if (reinterpret_cast<const char*>(h_status) == reinterpret_cast<const char*>(h_level) + (size_t)n_inst * 4) {
+        if (cudaMemcpyAsync(h_level, d_level, (size_t)n_inst * 8, cudaMemcpyDeviceToHost, s)) return TP_ECUDA;
+    } else if (cudaMemcpyAsync(h_level, d_level, (size_t)n_inst * 4, cudaMemcpyDeviceToHost, s) ||
+               cudaMemcpyAsync(h_status, d_status, (size_t)n_inst * 4, cudaMemcpyDeviceToHost, s)) {
         return TP_ECUDA;
+    }
     return TP_OK;
 }
 

@@ -257,6 +257,18 @@ def test_decide_entry_points_agree(gpu, oracle_mod, k2, cells):
     torch.cuda.synchronize()
     assert np.array_equal(h_level.numpy(), ref["level"])
     assert np.array_equal(h_status.numpy().view(np.uint32), ref["status"])
+    # packed host buffers: [inst | req | t_dead] in, [level | status] out (one copy each way)
+    bi, br = inputs["inst"].nbytes, inputs["req"].nbytes
+    h_in = torch.empty(bi + br + inputs["t_dead"].nbytes, dtype=torch.uint8).pin_memory()
+    h_in[:bi].copy_(torch.from_numpy(inputs["inst"].view(np.uint8)))
+    h_in[bi:bi + br].copy_(torch.from_numpy(inputs["req"].view(np.uint8)))
+    h_in[bi + br:].copy_(torch.from_numpy(np.ascontiguousarray(inputs["t_dead"]).view(np.uint8)))
+    h_out = torch.full((2, I), -7, dtype=torch.int32).pin_memory()
+    ctx.decide_host(model, h_in[:bi], I, h_in[bi:bi + br], R, h_in[bi + br:].view(torch.float64), inputs["freq"],
+                    inputs["tbt_slo"], h_out[0], h_out[1])
+    torch.cuda.synchronize()
+    assert np.array_equal(h_out[0].numpy(), ref["level"])
+    assert np.array_equal(h_out[1].numpy().view(np.uint32), ref["status"])
 
 
 def test_runs_are_fewer_than_grid_rows(gpu, oracle_mod):
