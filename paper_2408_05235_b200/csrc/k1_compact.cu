@@ -428,7 +428,6 @@ k1_compact(const __grid_constant__ K1cParams p) {
                     tot += (int)x[v * 4 + 2] + (m0 + 32 * v <= nn && (uint32_t)x[v * 4] != pl);
                 }
                 carry = prevlast;
-                if (WPI == 1) __syncwarp();
                 const unsigned mask = mrest | (head0 ? 1u : 0u);
                 if (lane == 0 ? head0 : head_rest) {
                     const int pos = h + before + __popc(mask & ltm);
