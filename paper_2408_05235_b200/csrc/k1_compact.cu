@@ -75,6 +75,8 @@ struct K1cParams {
     int32_t* end_n;
     int32_t* end_l;
     long long* end_d;
+    int32_t* flag_count;     // k1_packed -> wide fallback hand-over (count - 1)
+    int32_t* flag_list;
 };
 
 __device__ __forceinline__ uint32_t rank_of(const float* __restrict__ c, int cnt, float x) {
@@ -126,24 +128,11 @@ struct Group {
     }
 };
 
+// One instance, by the WPI warps of group grp (histograms sB / sKV in the group's shared memory).
 template <int WPI>
-__global__ void __launch_bounds__(cta_warps<WPI>() * 32, WPI == 1 ? 6 : 32 / cta_warps<WPI>())
-k1_compact(const __grid_constant__ K1cParams p) {
-    extern __shared__ __align__(16) int smem[];
+__device__ __forceinline__ void k1_body(const K1cParams& p, const int i, Group<WPI>& grp, int* sB, int* sKV,
+                                        const int gl, const int lane) {
     constexpr int GL = 32 * WPI;                       // group lanes
-    constexpr int NG = cta_warps<WPI>() / WPI;         // groups (instances) per full CTA
-    __shared__ long long s_x[WPI > 1 ? NG : 1][2 * WPI * 4];
-    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-    const int g = w / WPI;
-    Group<WPI> grp;
-    grp.gw = w % WPI;
-    grp.bar = 1 + g;
-    grp.xs = s_x[WPI > 1 ? g : 0];
-    const int gl = grp.gw * 32 + lane;                 // lane within the group
-    const int i = blockIdx.x * (int)((blockDim.x >> 5) / WPI) + g;
-    if (i >= p.n_inst) return;                         // group-uniform
-    int* sB = smem + (size_t)g * 2 * p.arr;
-    int* sKV = sB + p.arr;
     const int SL = p.S_log2, S = 1 << SL, P = p.P, H = p.H;
     auto ph = [&](int m) { return (m - 1) + P * ((m - 1) >> SL); };   // physical index of m >= 1
 
@@ -505,11 +494,308 @@ k1_compact(const __grid_constant__ K1cParams p) {
     }
 }
 
+
+// ---------------------------------------------------------------------------------------------
+// K1c, packed (large batches, one warp per instance): the two histograms in ONE int32 array,
+// value = B[m] * 2^16 + KV[m] -- exact whenever B < 2^15 and KV < 2^16, which the footprint check
+// certifies per instance (B <= R + Q, KV <= the sum of the requests' final block counts); the
+// difference-array events and the scan then work on the packed words unchanged (two's-complement
+// sums), and one atomic carries both end-of-request events.  Half the shared memory of k1_compact<1>
+// (more resident warps: this kernel is latency-bound) and half the scan work.  Run records are
+// written straight from the ballot compaction (consecutive positions per step: coalesced); the
+// Eq. 4 table is built in windows of the histogram space.  Instances the check rejects are handed
+// to k1_compact<1, true> through the flag list.
+#ifndef TP_K1P_MINB
+#define TP_K1P_MINB 8
+#endif
+__global__ void __launch_bounds__(kWarpsPerCta * 32, TP_K1P_MINB)
+k1_packed(const __grid_constant__ K1cParams p) {
+    extern __shared__ __align__(16) int smem[];
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    const int i = blockIdx.x * (int)(blockDim.x >> 5) + w;
+    if (i >= p.n_inst) return;                        // warp-uniform
+    int* sv = smem + (size_t)w * p.arr;
+    const int SL = p.S_log2, S = 1 << SL, P = p.P, H = p.H;
+    auto ph = [&](int m) { return (m - 1) + P * ((m - 1) >> SL); };   // physical index of m >= 1
+
+    const tp_inst in = p.inst[i];
+    const int64_t rb = in.req_begin;
+    const int nr = in.n_run, nq = in.n_queue, N = in.N;
+    const FastDiv fdN((uint32_t)(N > 0 ? N : 1));
+    for (int k = lane * 4; k + 3 < p.arr; k += 128) *reinterpret_cast<int4*>(sv + k) = make_int4(0, 0, 0, 0);
+    __syncwarp();
+
+    bool bad = N < 1 || in.tp < 1 || (int64_t)in.tp >= kFeatLimit || nr < 0 || nq < 0 || in.kv_cap < 0 ||
+               in.max_batch < 0 || rb < 0 || rb + (int64_t)nr + nq > (int64_t)p.n_req;
+    int64_t foot = 0;
+    int nloc = 0, b1 = 0, kv1 = 0;
+    bool lost = false;
+    if (!bad) {
+        for (int e = lane; e < nr + nq; e += 32) {
+            const int4 r = __ldg(&p.req[rb + e]);
+            const int64_t l64 = (int64_t)r.z - r.x;
+            const bool eb = r.x < 0 || r.y < 1 || r.z < 1 || r.x >= kFeatLimit || r.y >= kFeatLimit || l64 < 1 ||
+                            l64 > H || (e >= nr && r.x != 0);
+            bad |= eb;
+            if (eb) continue;
+            const int a = r.x, q = r.y, l = (int)l64, aq = a + q;
+            asm volatile("prefetch.global.L2 [%0];" ::"l"(p.t_dead + rb + e));
+            const int kv_end = (int)fdN.div((uint32_t)(aq + l - 2)) + 1;           // ceil((a+l-1+q)/N)
+            foot += kv_end;
+            if (e < nr) {
+                nloc = max(nloc, l);
+                lost |= (r.w & TP_REQ_LOST) != 0;
+                const int c1 = (int)fdN.div((uint32_t)(aq - 1));                    // ceil(aq / N) - 1
+                kv1 += c1 + 1;
+                ++b1;
+                for (int m = 2 + (c1 + 1) * N - aq; m <= l; m += N) atomicAdd(&sv[ph(m)], 1);
+                atomicAdd(&sv[ph(l + 1)], -(65536 + kv_end));                       // B -1 and KV -kv_end
+            }
+        }
+    }
+    bad = __any_sync(kFull, bad);
+    for (int o = 16; o; o >>= 1) foot += __shfl_xor_sync(kFull, foot, o);
+    b1 = __reduce_add_sync(kFull, b1);
+    kv1 = __reduce_add_sync(kFull, kv1);
+    nloc = warp_max(nloc);
+    lost = __any_sync(kFull, lost);
+    bad = bad || foot >= kFeatLimit;
+    if (!bad && (nr + nq >= 32768 || foot >= 65536)) {       // does not fit the packed words
+        if (lane == 0) p.flag_list[atomicAdd(p.flag_count, 1) + 1] = i;   // flag_count holds count - 1
+        return;
+    }
+    if (bad) {
+        if (p.B) {
+            const int lim = p.bkv_rows ? H : 1;
+            for (int m = lane; m < lim; m += 32) {
+                p.B[(int64_t)i * H + m] = 0;
+                p.KV[(int64_t)i * H + m] = 0;
+            }
+        }
+        if (lane == 0) {
+            p.n[i] = 0;
+            p.n_adm[i] = 0;
+            p.status[i] = TP_ST_BAD_INPUT;
+            if (p.run_h) p.run_h[i] = 0;
+            if (p.end_n) p.end_n[i] = 0;
+        }
+        return;
+    }
+    __syncwarp();
+    if (lane == 0) sv[0] += b1 * 65536 + kv1;     // the m = 1 terms (index 0 gets no other event)
+    __syncwarp();
+
+    // ---- inclusive scan of the packed words over the lane segments ----
+    int* seg = sv + lane * (S + P);
+    const int lo = 1 + lane * S;
+    int kvmax = 0;
+    {
+        int sum = 0;
+        for (int k = 0; k < S; k += 4) {
+            const int4 v = *reinterpret_cast<const int4*>(seg + k);
+            sum += v.x + v.y + v.z + v.w;
+        }
+        int x = sum;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const int y = __shfl_up_sync(kFull, x, o);
+            if (lane >= o) x += y;
+        }
+        int pre = x - sum;
+        for (int k = 0; k < S; k += 4) {
+            int4 v = *reinterpret_cast<const int4*>(seg + k);
+            v.x += pre; v.y += v.x; v.z += v.y; v.w += v.z;
+            pre = v.w;
+            *reinterpret_cast<int4*>(seg + k) = v;
+            const int m = lo + k;
+            kvmax = max(kvmax, max(max(m <= H ? (v.x & 0xFFFF) : 0, m + 1 <= H ? (v.y & 0xFFFF) : 0),
+                                   max(m + 2 <= H ? (v.z & 0xFFFF) : 0, m + 3 <= H ? (v.w & 0xFFFF) : 0)));
+        }
+    }
+    __syncwarp();
+    int kvb = warp_max(kvmax);
+    uint32_t st = kvb > in.kv_cap ? TP_ST_KV_OVER : 0u;
+
+    // ---- FIFO gate (as k1_compact: one candidate at a time over its window, exact bound shortcut) ----
+    int n_adm = 0;
+    const int forced = p.force_adm ? min(max(p.force_adm[i], 0), nq) : -1;
+    const uint32_t lmask = p.lost_mask ? p.lost_mask[i] : 0u;
+    const int ncand = forced >= 0 ? forced : nq;
+    if (forced < 0 && ncand > 0 && (st & TP_ST_KV_OVER)) {
+        st |= TP_ST_QUEUE_BLOCKED;
+    } else {
+        int B1 = sv[0] >> 16;
+        for (int c = 0; c < ncand; ++c) {
+            const int4 r = __ldg(&p.req[rb + nr + c]);
+            const int q = r.y, lc = r.z;
+            const int kvc_top = (int)fdN.div((uint32_t)(lc + q - 2)) + 1;
+            if (forced < 0) {
+                bool admit = B1 + 1 <= in.max_batch;
+                if (admit && kvb + kvc_top > in.kv_cap) {
+                    int mx = 0;
+#pragma unroll 4
+                    for (int m = 1 + lane; m <= lc; m += 32)
+                        mx = max(mx, (sv[ph(m)] & 0xFFFF) + (int)fdN.div((uint32_t)(m + q - 2)) + 1);
+                    mx = warp_max(mx);
+                    admit = mx <= in.kv_cap;
+                    kvb = max(kvb, mx);
+                } else {
+                    kvb += kvc_top;
+                }
+                if (!admit) {
+                    st |= TP_ST_QUEUE_BLOCKED;
+                    break;
+                }
+            } else {
+                kvb += kvc_top;
+            }
+#pragma unroll 4
+            for (int m = 1 + lane; m <= lc; m += 32) sv[ph(m)] += 65536 + (int)fdN.div((uint32_t)(m + q - 2)) + 1;
+            __syncwarp();
+            ++B1;
+            ++n_adm;
+            nloc = max(nloc, lc);
+            lost |= (r.w & TP_REQ_LOST) || (c < 32 && ((lmask >> c) & 1u));
+        }
+    }
+    if (forced >= 0 && forced < nq) st |= TP_ST_QUEUE_BLOCKED;
+    const int n = nloc;
+    if (n == 0) st |= TP_ST_EMPTY;
+    else if (lost) st |= TP_ST_BYPASS_LOST;
+    __syncwarp();
+
+    if (p.B) {
+        int* Bo = p.B + (int64_t)i * H;
+        int* Ko = p.KV + (int64_t)i * H;
+        const int lim = p.bkv_rows ? H : 1;
+        for (int m = 1 + lane; m <= lim; m += 32) {
+            const int v = sv[ph(m)];
+            Bo[m - 1] = v >> 16;
+            Ko[m - 1] = v & 0xFFFF;
+        }
+    }
+    if (lane == 0) {
+        p.n[i] = n;
+        p.n_adm[i] = n_adm;
+        p.status[i] = st;
+    }
+    const int nn = (st & p.skip) ? 0 : n;
+    const unsigned ltm = (1u << lane) - 1u;
+    const size_t row = (size_t)i * H;
+
+    // ---- runs of equal cells (records straight from the ballot compaction), claims ----
+    if (p.run_h) {
+        const int nB = p.cut_off[2] - p.cut_off[1], nKV = p.cut_off[3] - p.cut_off[2];
+        const int lB = p.rtab_len[0], lKV = p.rtab_len[1];
+        const uint16_t* tB = p.rtab + p.rtab_off[0];
+        const uint16_t* tKV = p.rtab + p.rtab_off[1];
+        const uint32_t rtp = rank_of(p.cuts + p.cut_off[0], p.cut_off[1] - p.cut_off[0], (float)in.tp);
+        const uint32_t nk1 = (uint32_t)nKV + 1;
+        const uint32_t cell_base = rtp * (uint32_t)(nB + 1) * nk1;
+        int h = 0;
+        uint32_t carry = 0xffffffffu;
+        for (int m0 = 1; m0 <= nn; m0 += 32) {
+            const int m = m0 + lane;
+            uint32_t k = 0;
+            if (m <= nn) {
+                const int v = sv[ph(m)];
+                const int b = v >> 16, kv = v & 0xFFFF;
+                const uint32_t rbk = b < lB ? __ldg(tB + b) : rank_of(p.cuts + p.cut_off[1], nB, (float)b);
+                const uint32_t rkv = kv < lKV ? __ldg(tKV + kv) : rank_of(p.cuts + p.cut_off[2], nKV, (float)kv);
+                k = cell_base + rbk * nk1 + rkv;
+            }
+            uint32_t pk = __shfl_up_sync(kFull, k, 1);
+            if (lane == 0) pk = carry;
+            carry = __shfl_sync(kFull, k, 31);
+            const bool head = m <= nn && k != pk;
+            const unsigned mask = __ballot_sync(kFull, head);
+            if (head) {
+                const int pos = h + __popc(mask & ltm);
+                p.run_m[row + pos] = m;
+                p.run_key[row + pos] = k;
+                if (__ldcg(p.cell_tab + k) == -1 && atomicCAS(p.cell_tab + k, -1, -2) == -1) {
+                    const int idx = atomicAdd(p.cell_count, 1) + 1;   // cell_count holds count - 1
+                    p.cell_list[idx] = k;
+                    p.cell_clamp[idx] = 0u;
+                    p.cell_tab[k] = idx;
+                }
+            }
+            h += __popc(mask);
+        }
+        if (lane == 0) p.run_h[i] = h;
+    }
+
+    // ---- Eq. 4 deadline list, in windows of the histogram space (arr / 2 int64 entries) ----
+    if (p.end_n) {
+        long long* dmin = reinterpret_cast<long long*>(sv);
+        const int wm = p.arr / 2;
+        int ne = 0;
+        for (int wb = 1; wb <= nn; wb += wm) {
+            const int we = min(nn, wb + wm - 1);
+            __syncwarp();
+            for (int m = wb + lane; m <= we; m += 32) dmin[m - wb] = kNoDeadline;
+            __syncwarp();
+            for (int e = lane; e < nr + n_adm; e += 32) {
+                const int64_t j = rb + e;
+                const int4 r = __ldg(&p.req[j]);
+                const int l = r.z - r.x;
+                if (l >= wb && l <= we) atomicMin(&dmin[l - wb], slack_ticks(__ldg(&p.t_dead[j]) - in.t_cur));
+            }
+            __syncwarp();
+            for (int m0 = wb; m0 <= we; m0 += 32) {
+                const int m = m0 + lane;
+                const long long d = m <= we ? dmin[m - wb] : kNoDeadline;
+                const unsigned mask = __ballot_sync(kFull, d != kNoDeadline);
+                if (d != kNoDeadline) {
+                    const int pos = ne + __popc(mask & ltm);
+                    p.end_l[row + pos] = m;
+                    p.end_d[row + pos] = d;
+                }
+                ne += __popc(mask);
+            }
+        }
+        if (lane == 0) p.end_n[i] = ne;
+    }
+}
+
+template <int WPI, bool FLAGGED = false>   // FLAGGED: the instances k1_packed handed over
+__global__ void __launch_bounds__(cta_warps<WPI>() * 32, WPI == 1 ? 6 : 32 / cta_warps<WPI>())
+k1_compact(const __grid_constant__ K1cParams p) {
+    extern __shared__ __align__(16) int smem[];
+    constexpr int NG = cta_warps<WPI>() / WPI;         // groups (instances) per full CTA
+    __shared__ long long s_x[WPI > 1 ? NG : 1][2 * WPI * 4];
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    const int g = w / WPI, gpb = (int)(blockDim.x >> 5) / WPI;
+    Group<WPI> grp;
+    grp.gw = w % WPI;
+    grp.bar = 1 + g;
+    grp.xs = s_x[WPI > 1 ? g : 0];
+    const int gl = grp.gw * 32 + lane;                 // lane within the group
+    int* sB = smem + (size_t)g * 2 * p.arr;
+    int* sKV = sB + p.arr;
+    if constexpr (FLAGGED) {  // persistent over the hand-over list
+        const int nflag = *p.flag_count + 1;
+        for (int j = blockIdx.x * gpb + g; j < nflag; j += gridDim.x * gpb) {
+            grp.sync();
+            k1_body<WPI>(p, p.flag_list[j], grp, sB, sKV, gl, lane);
+        }
+        return;
+    }
+    const int i = blockIdx.x * gpb + g;
+    if (i >= p.n_inst) return;                         // group-uniform
+    k1_body<WPI>(p, i, grp, sB, sKV, gl, lane);
+}
+
 }  // namespace
 
 int project_compact_smem_per_warp(int32_t H) { return 2 * seg_geom(H, 32).arr * (int)sizeof(int); }
 
 namespace {
+int env_int_k1(const char* name, int dflt) {
+    const char* v = std::getenv(name);
+    return v ? std::atoi(v) : dflt;
+}
+
 // TP_K1C_WARPS (1/2/4): warps per instance override (tuning)
 int env_wpi() {
     const char* v = std::getenv("TP_K1C_WARPS");
@@ -517,7 +803,7 @@ int env_wpi() {
     return (x == 1 || x == 2 || x == 4 || x == 8) ? x : 0;
 }
 
-template <int WPI>
+template <int WPI, bool FLAGGED = false>
 int launch_wpi(const K1cParams& p0, int32_t n_inst, int32_t H, cudaStream_t s) {
     K1cParams p = p0;
     const SegGeom g = seg_geom(H, 32 * WPI);
@@ -533,14 +819,41 @@ int launch_wpi(const K1cParams& p0, int32_t n_inst, int32_t H, cudaStream_t s) {
     if (cudaGetDevice(&dev) != cudaSuccess) return TP_ECUDA;
     static int attr_bytes[64] = {};
     if (dev < 64 && attr_bytes[dev] < (int)smem) {
-        if (cudaFuncSetAttribute(k1_compact<WPI>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) !=
-            cudaSuccess)
+        if (cudaFuncSetAttribute(k1_compact<WPI, FLAGGED>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 (int)smem) != cudaSuccess)
             return TP_EINVAL;   // H too large for the per-group histograms
         attr_bytes[dev] = (int)smem;
     }
-    const int grid = (n_inst + gpb - 1) / gpb;
-    k1_compact<WPI><<<grid, gpb * WPI * 32, smem, s>>>(p);
+    int sms = 148;
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    // FLAGGED: a persistent grid over the (normally empty) hand-over list
+    const int grid = FLAGGED ? std::min(sms, (n_inst + gpb - 1) / gpb) : (n_inst + gpb - 1) / gpb;
+    k1_compact<WPI, FLAGGED><<<grid, gpb * WPI * 32, smem, s>>>(p);
     return cudaPeekAtLastError() == cudaSuccess ? TP_OK : TP_ECUDA;
+}
+
+// k1_packed (one warp per instance), then the wide kernel over the instances it handed over
+int launch_packed(const K1cParams& p0, int32_t n_inst, int32_t H, cudaStream_t s) {
+    K1cParams p = p0;
+    const SegGeom g = seg_geom(H, 32);
+    p.S_log2 = g.S_log2;
+    p.P = g.P;
+    p.arr = g.arr;
+    const size_t per_warp = (size_t)g.arr * sizeof(int);
+    if (per_warp > 200 * 1024) return TP_EINVAL;
+    const int wpb = (int)std::max<size_t>(1, std::min<size_t>(kWarpsPerCta, (100 * 1024) / per_warp));
+    const size_t smem = (size_t)wpb * per_warp;
+    int dev = 0;
+    if (cudaGetDevice(&dev) != cudaSuccess) return TP_ECUDA;
+    static int attr_bytes[64] = {};
+    if (dev < 64 && attr_bytes[dev] < (int)smem) {
+        if (cudaFuncSetAttribute(k1_packed, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess)
+            return TP_EINVAL;
+        attr_bytes[dev] = (int)smem;
+    }
+    k1_packed<<<(n_inst + wpb - 1) / wpb, wpb * 32, smem, s>>>(p);
+    if (cudaPeekAtLastError() != cudaSuccess) return TP_ECUDA;
+    return launch_wpi<1, true>(p0, n_inst, H, s);
 }
 }  // namespace
 
@@ -583,8 +896,11 @@ int launch_project_compact(const K2Params& w, const tp_inst* inst, int32_t n_ins
     p.end_n = w.end_n;
     p.end_l = w.end_l;
     p.end_d = w.end_d;
-    // cell_count (count - 1) and cell_tab are contiguous: one reset; claimers zero their clamp masks
-    if (cudaMemsetAsync(w.cell_count, 0xFF, 4 + (size_t)w.n_cells * 4, s) != cudaSuccess) return TP_ECUDA;
+    p.flag_count = w.flag_count;
+    p.flag_list = w.flag_list;
+    // flag_count, cell_count (both count - 1) and cell_tab are contiguous: one reset; claimers zero
+    // their cells' clamp masks
+    if (cudaMemsetAsync(w.flag_count, 0xFF, 8 + (size_t)w.n_cells * 4, s) != cudaSuccess) return TP_ECUDA;
     // warps per instance: small batches get several warps per instance (the per-instance chain
     // of dependent loads and reductions is the latency; shorter per-warp loops shorten it), large
     // batches one (the GPU is full anyway)
@@ -593,11 +909,12 @@ int launch_project_compact(const K2Params& w, const tp_inst* inst, int32_t n_ins
     static const int wpi_env = env_wpi();
     const int64_t slots = (int64_t)sms * 32;    // C2 (1,024 instances): 4 warps each; C3: one
     const int wpi = wpi_env ? wpi_env : ((int64_t)n_inst * 4 <= slots ? 4 : (int64_t)n_inst * 2 <= slots ? 2 : 1);
+    static const bool packed = env_int_k1("TP_K1C_PACKED", 1) != 0;
     switch (wpi) {
         case 8: return launch_wpi<8>(p, n_inst, H, s);
         case 4: return launch_wpi<4>(p, n_inst, H, s);
         case 2: return launch_wpi<2>(p, n_inst, H, s);
-        default: return launch_wpi<1>(p, n_inst, H, s);
+        default: return packed ? launch_packed(p, n_inst, H, s) : launch_wpi<1>(p, n_inst, H, s);
     }
 }
 

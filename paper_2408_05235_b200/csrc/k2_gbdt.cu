@@ -803,6 +803,9 @@ static size_t carve(void* ws, int64_t n_cells, int32_t n_inst, int32_t H, int32_
     a = align256(a + I * (size_t)H * 4);
     p.end_d = reinterpret_cast<long long*>(a);
     a = align256(a + I * (size_t)H * 8);
+    p.flag_list = reinterpret_cast<int32_t*>(a);
+    a = align256(a + I * 4);
+    p.flag_count = nullptr;
     p.cell_tab = nullptr;
     p.cell_list = nullptr;
     p.cell_count = nullptr;
@@ -816,9 +819,10 @@ static size_t carve(void* ws, int64_t n_cells, int32_t n_inst, int32_t H, int32_
         p.n_cells = (int32_t)n_cells;
         p.cell_cap = (int32_t)cap;
         // cell_count (stored as count - 1) directly before cell_tab: one 0xFF memset resets both
-        p.cell_count = reinterpret_cast<int32_t*>(a);
-        p.cell_tab = reinterpret_cast<int32_t*>(a + 4);
-        a = align256(a + 4 + (size_t)n_cells * 4);
+        p.flag_count = reinterpret_cast<int32_t*>(a);
+        p.cell_count = reinterpret_cast<int32_t*>(a + 4);
+        p.cell_tab = reinterpret_cast<int32_t*>(a + 8);
+        a = align256(a + 8 + (size_t)n_cells * 4);
         p.cell_list = reinterpret_cast<uint32_t*>(a);
         a = align256(a + (size_t)cap * 4);
         p.cell_clamp = reinterpret_cast<uint32_t*>(a);

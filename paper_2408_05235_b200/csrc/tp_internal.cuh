@@ -108,6 +108,10 @@ struct K2Params {
     int32_t* end_n;          // [n_inst]
     int32_t* end_l;          // [n_inst][H]
     long long* end_d;        // [n_inst][H]
+    // compact path, K1c's packed histograms: instances that do not fit them (count - 1, directly
+    // before cell_count: reset by the same memset) and their list, handled by the wide kernel
+    int32_t* flag_count;
+    int32_t* flag_list;      // [n_inst]
 };
 
 // workspace for tp_predict_ips_runs; cell mode is used when the model's dense cell space

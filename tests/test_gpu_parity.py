@@ -365,3 +365,23 @@ def test_ctx_ips_grid_on_demand(gpu, oracle_mod):
         assert np.array_equal(r.level.cpu().numpy(), ref["level"])
         assert np.array_equal(r.status.cpu().numpy().view(np.uint32), ref["status"])
     assert ctx.buffers()[4]          # allocated by the first non-compact mode, kept
+
+
+def test_compact_packed_fallback(gpu, oracle_mod):
+    """Large batches run K1c with packed B * 2^16 + KV histograms; instances whose footprint does not
+    fit (KV >= 2^16 blocks, or >= 2^15 requests) go through the wide kernel -- both bit-exact."""
+    cfg = dataclasses.replace(W.CONFIGS["C1"], n_inst=3000, seed=4321)     # > 2,368: one warp each
+    blob = W.write_blob(W.config_ensemble(cfg))
+    inputs = W.config_inputs(cfg)
+    inst, req = inputs["inst"].copy(), inputs["req"].copy()
+    for i in (5, 1234, 2999):                  # N = 1 and 9,000-token prompts: > 65,536 blocks
+        b, nr = int(inst[i]["req_begin"]), int(inst[i]["n_run"])
+        inst[i]["N"] = 1
+        inst[i]["kv_cap"] = 1 << 22
+        req["q"][b:b + nr + int(inst[i]["n_queue"])] = 9000
+    assert int(req["q"][int(inst[5]["req_begin"]):][:8].sum()) >= 65536
+    inputs = dict(inputs, inst=inst, req=req)
+    got = run_gpu(gpu, blob, inputs, want_tr=False, mode="compact")
+    ref = run_oracle(oracle_mod, blob, inputs, want_tr=False)
+    assert_parity(got, ref)
+    assert int(got["KV"][5].max()) >= 65536
