@@ -506,7 +506,7 @@ __device__ __forceinline__ void k1_body(const K1cParams& p, const int i, Group<W
 // Eq. 4 table is built in windows of the histogram space.  Instances the check rejects are handed
 // to k1_compact<1, true> through the flag list.
 #ifndef TP_K1P_MINB
-#define TP_K1P_MINB 8
+#define TP_K1P_MINB 12
 #endif
 __global__ void __launch_bounds__(kWarpsPerCta * 32, TP_K1P_MINB)
 k1_packed(const __grid_constant__ K1cParams p) {
