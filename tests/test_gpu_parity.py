@@ -331,11 +331,12 @@ def test_imported_sklearn_model(gpu, oracle_mod, mode):
 
 # ------------------------------------------------------------------ compact-path geometry
 
-@pytest.mark.parametrize("n_inst,H", [(2000, 512), (300, 2000), (40, 8192), (7, 16384)])
+@pytest.mark.parametrize("n_inst,H", [(2000, 512), (300, 2000), (40, 8192), (7, 16384), (2500, 200), (2500, 2000)])
 def test_compact_geometry(gpu, oracle_mod, n_inst, H):
     """The compact path's launch geometry against the oracle: K3c with W = 2 warps per instance
     (2,000 instances), K1c segments longer than 32 iterations (H = 2,000: S = 64; H = 8,192 / 16,384:
-    one warp per CTA, 66 / 132 KB of per-warp histograms)."""
+    one warp per CTA, 66 / 132 KB of per-warp histograms), and the packed K1c of large batches
+    (2,500 instances) with 8- and 64-iteration segments."""
     cfg = dataclasses.replace(W.CONFIGS["P2"], n_inst=n_inst, H=H, seed=8100 + H)
     blob = W.write_blob(W.config_ensemble(cfg))
     inputs = W.config_inputs(cfg)
