@@ -130,7 +130,7 @@ k3_compact(const __grid_constant__ K3cParams p) {
         long long cur_d = __shfl_sync(kFull, ed, 0);
         // this level's column of the tick LUT (W = 1: lanes >= F read column F-1 -- in the row,
         // ignored -- instead of a predicated load; fewer live registers)
-        const long long* lt = p.lut_ticks + (W == 1 ? min(lane, F - 1) : lane);
+        const int lc = W == 1 ? min(lane, F - 1) : lane;
         // run chunk kb: start, length and LUT row per lane; the next chunk's records are loaded
         // while the current one is walked
         int nx_s = n + 1, nx_len = 0;
@@ -165,7 +165,7 @@ k3_compact(const __grid_constant__ K3cParams p) {
 #pragma unroll
                 for (int q = 0; q < kPrefetch; ++q) {
                     const int o_ = __shfl_sync(kFull, roff, (j0 + q) & 31);
-                    tv[q] = (W == 1 || act) ? __ldcg(lt + o_) : 0;   // rows past cnt: row 0, unused
+                    tv[q] = (W == 1 || act) ? __ldcg(p.lut_ticks + (unsigned)(o_ + lc)) : 0;   // rows past cnt: row 0
                 }
 #pragma unroll
                 for (int q = 0; q < kPrefetch; ++q) {
