@@ -254,6 +254,10 @@ def main():
     ap.add_argument("--search", default="exhaustive", choices=["exhaustive", "binary"],
                     help="K3 order: lowest passing level over all levels (reading A-13, default) or the "
                          "paper's binary search (P:555, reading A-24; needs --k2 fused)")
+    ap.add_argument("--graph", dest="graph", action="store_true", default=True,
+                    help="time the step as a replayed CUDA graph of its kernels (default; SURVEY §8d)")
+    ap.add_argument("--no-graph", dest="graph", action="store_false",
+                    help="launch the kernels one by one in the timed steps")
     ap.add_argument("--k2", default="compact", choices=["compact", "fused", "cells", "runs", "direct"],
                     help="path: compact (K1c runs + deadline list -> K2 on the cells -> K3c, default), "
                          "cell-memoised fused with K3, cell-memoised with the ips grid, run-compressed, or "
@@ -315,20 +319,39 @@ def main():
     stream = torch.cuda.current_stream(dev)
     flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)     # > 126 MB L2
 
+    def kernels(strm):
+        rnd.project(strm)
+        rnd.predict(model, strm)
+        rnd.select(strm)
+
+    graph = None
+    if args.graph:           # the K1 -> K2 -> K3 sequence captured once, replayed every step
+        gs = torch.cuda.Stream(dev)
+        with torch.cuda.stream(gs):
+            kernels(gs)      # warm-up on the capture stream (attributes, lazy module loading)
+        torch.cuda.synchronize(dev)
+        graph = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(graph, stream=gs):
+            kernels(gs)
+        torch.cuda.synchronize(dev)
+
     def step(evs=None, split=True):
         # split=False: events only around the whole step (an event between two kernels stops the
         # second from launching early -- programmatic dependent launch -- and costs ~4 us each)
         if evs:
             evs[0].record(stream)
-        rnd.project(stream)
-        if evs and split:
-            evs[1].record(stream)
-        rnd.predict(model, stream)
-        if evs and split:
-            evs[2].record(stream)
-        rnd.select(stream)
-        if evs and split:
-            evs[3].record(stream)
+        if graph is not None and not split:
+            graph.replay()
+        else:
+            rnd.project(stream)
+            if evs and split:
+                evs[1].record(stream)
+            rnd.predict(model, stream)
+            if evs and split:
+                evs[2].record(stream)
+            rnd.select(stream)
+            if evs and split:
+                evs[3].record(stream)
         if world > 1:
             if dist_test:
                 g = torch.empty(gathered.shape, dtype=gathered.dtype)
@@ -492,6 +515,7 @@ def main():
                    "global_instances": int(inst_all), "H": cfg.H, "F": cfg.F, "trees": info.n_trees,
                    "depth": info.depth, "parallelism": f"instance-sharded x{world}" + (" + NCCL all-gather" if world > 1 else ""),
                    "l2": "flushed between timed steps (256 MiB device write, untimed)", "k2": args.k2,
+                   "cuda_graph": bool(args.graph),
                    "search": args.search},
         "grid_evals_per_sec": grid_per_s,
         "step_ms_pctl": {"p10": float(np.percentile(step_ms, 10)), "p50": float(np.percentile(step_ms, 50)),
