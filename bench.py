@@ -529,8 +529,10 @@ def main():
         "cpu_baseline": cpu,
         "e2e": e2e,
         # our kernels per step: k1_project / k1_compact, [k2_runs], k2_gbdt, [k2_expand], k3_select* / k3_compact
+        # compact: K1c (+ the hand-over kernel after k1_packed at one warp per instance, i.e. when
+        # the batch exceeds 16 warps per SM), the K2 phases, K3c
         "gpu_launches": {"direct": 3, "runs": 4, "cells": 5, "fused": 4,
-                         "compact": 2 + k2_phases(info)}[args.k2] * args.steps,
+                         "compact": 2 + k2_phases(info) + int(I * 2 > sms * 32)}[args.k2] * args.steps,
         "clocks": clk,
         "paper_context": "paper controller on host CPU (A100 box): projection <2 ms, model ~3 ms per call, "
                          "scheduler+throttle 35 ms per decision (P:466, P:495, P:557)",
