@@ -192,6 +192,7 @@ def bench_replay(args, cfg, rank, world, local, dist, dist_test):
     model = tp.Gbdt(W.write_blob(W.config_ensemble(cfg)), local)
     rp = replay.Replay(data, model, dev, admission=args.admission, search=args.search)
     stream = torch.cuda.current_stream(dev)
+    sms = torch.cuda.get_device_properties(dev).multi_processor_count
     for _ in range(max(args.warmup, 3)):
         rp.round(stream)
     torch.cuda.synchronize(dev)
@@ -235,7 +236,11 @@ def bench_replay(args, cfg, rank, world, local, dist, dist_test):
         "decisions_per_sec_decide_only": I * args.steps / (float(tot[1]) / 1e3),
         "per_round_ms": {"decide": dec_ms / args.steps, "advance": adv_ms / args.steps},
         "replay_stats_after_warmup_and_steps": st,
-        "gpu_launches": None, "clocks": clk,
+        # per round without admission: K1c (+ hand-over kernel at one warp per instance), the K2
+        # phases, K3c, the replay advance; with admission control the prefix pass adds its own
+        "gpu_launches": (None if args.admission else
+                         (3 + k2_phases(model.info()) + int((i1 - i0) * 2 > sms * 32)) * args.steps),
+        "clocks": clk,
     }
     print(json.dumps(line), flush=True)
 
