@@ -1,22 +1,25 @@
 #!/usr/bin/env python
 """Benchmark of the throttLL'eM frequency-selection hot path (BASELINE.json metric: frequency
-decisions/s and GBDT grid evals/s vs roofline).
+decisions/s and GBDT grid evals/s at 1/2/4/8 B200, vs roofline).
 
-One step = one decision round over the workload: K1 projection -> K2 GBDT grid -> K3 SLO scan
-(+ one NCCL all-gather of the decisions when N > 1).  Inputs are synthetic and seeded
-(paper_2408_05235_b200/workload.py), already resident in HBM when the timed region starts.
+One step = one decision round over the workload: K1c projection (+ pieces, cell claims, Eq. 4
+minima) -> K2 GBDT on the distinct cells -> K3c SLO scan + frequency choice (+ one NCCL all-gather
+of the decisions when N > 1).  Inputs are synthetic and seeded (paper_2408_05235_b200/workload.py),
+already resident in HBM when the timed region starts.
 
-  python bench.py [--gpus N] [--steps K] [--warmup W] [--workload C2] [--impl ours|reference]
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--workload C5] [--impl ours|reference]
 
-N > 1 runs under torchrun (one process per GPU, NCCL).  Default workload C2 = BASELINE.json
-configs[1]; per-GPU work is fixed (weak scaling: rank r decides instances [r*I, (r+1)*I) of the
-same generator).  --workload C5 is the strong-scaling sweep (262,144 instances split over N).
+Default workload C5 = BASELINE.json configs[4], the configuration the metric is quoted on: 262,144
+instances sharded over the N GPUs (strong scaling: rank r decides its contiguous 262,144/N).  N > 1
+runs under torchrun, one process per GPU, NCCL.  --workload C2/C3 time the other configs (C2: weak
+scaling, 1,024 instances per GPU); --workload C4 is the trace replay.
 """
 from __future__ import annotations
 
 import argparse
 import json
 import os
+import platform
 import statistics
 import subprocess
 import sys
@@ -34,9 +37,10 @@ DESCR = {
     "C2": "BASELINE configs[1]: 1,024 instances, batch<=64, 16 freq levels, 512-iter horizon, 200-tree depth-8 GBDT",
     "C3": "BASELINE configs[2]: 65,536 instances, synthetic Azure-like trace, batch<=256, 32 freq levels, 1,024-iter horizon (200-tree depth-8 assumed)",
     "C4": "BASELINE configs[3]: trace replay, 1M requests across 4,096 TP instance states re-decided every iteration, 500-tree depth-8 GBDT",
-    "C5": "BASELINE configs[4]: 262,144 instances sharded over N GPUs (strong scaling), 200-tree depth-8",
+    "C5": "BASELINE configs[4]: scaling sweep, 262,144 instances sharded over N B200 with NCCL gather of decisions (C3 generator, 200-tree depth-8)",
 }
 SKIP = 64 | 1 | 2
+METRIC = "frequency decisions/sec"
 
 
 def env_int(k, d):
@@ -47,11 +51,11 @@ def env_int(k, d):
 
 
 def shard_of(cfg, rank, world):
-    """Instance range of this rank and the global instance count (paper_2408_05235_b200/shard.py)."""
+    """Instance range [i0, i1) of this rank and the global instance count (shard.py)."""
     from paper_2408_05235_b200 import shard
-    if cfg.name == "C5":            # strong scaling: fixed total
-        return (*shard.shard_range(cfg.n_inst, rank, world), cfg.n_inst)
-    return (*shard.weak_range(cfg.n_inst, rank), cfg.n_inst * world)   # weak: fixed per GPU
+    if cfg.name == "C2":            # weak scaling: 1,024 new instances per GPU
+        return (*shard.weak_range(cfg.n_inst, rank), cfg.n_inst * world)
+    return (*shard.shard_range(cfg.n_inst, rank, world), cfg.n_inst)   # strong: fixed total
 
 
 class Clocks:
@@ -104,65 +108,89 @@ def measured_peaks():
         return {}
 
 
-def cpu_baseline(cfg, blob, inputs, budget_s=15.0, search="exhaustive"):
-    """The oracle, as it stands, on this host's cores, on a bounded prefix of the workload."""
+def cpu_model():
+    try:
+        out = subprocess.run(["lscpu"], capture_output=True, text=True, timeout=10).stdout
+        for line in out.splitlines():
+            if line.lower().startswith("model name"):
+                return line.split(":", 1)[1].strip()
+    except (OSError, subprocess.SubprocessError):
+        pass
+    return platform.processor() or "unknown"
+
+
+def stratified(n_total, k, offset=0):
+    """k instances spread evenly over [0, n_total) (the oracle's bounded sample of a workload)."""
+    k = max(1, min(k, n_total))
+    return np.unique((np.arange(k, dtype=np.int64) * n_total) // k + offset % max(1, n_total // k))
+
+
+def sample_inputs(inputs, idx):
+    """A self-contained round of the instances idx (request rows copied, req_begin rebased)."""
+    inst = inputs["inst"][idx].copy()
+    b = inputs["inst"]["req_begin"][idx].astype(np.int64)
+    c = (inputs["inst"]["n_run"][idx] + inputs["inst"]["n_queue"][idx]).astype(np.int64)
+    rows = np.concatenate([np.arange(x, x + y) for x, y in zip(b, c)]) if len(idx) else np.zeros(0, np.int64)
+    inst["req_begin"] = np.concatenate([[0], np.cumsum(c)[:-1]]).astype(np.int32)
+    return dict(inputs, inst=inst, req=inputs["req"][rows], t_dead=inputs["t_dead"][rows])
+
+
+def oracle_time(blob, sub, threads, search):
     from oracle import oracle
     m = oracle.Model(blob)
+    t = time.perf_counter()
+    oracle.decide(m, sub["inst"], sub["req"], sub["t_dead"], sub["H"], sub["freq"], sub["tbt_slo"],
+                  want_grid=False, want_curves=False, threads=threads, search=search)
+    return time.perf_counter() - t
+
+
+def cpu_baseline(cfg, blob, inputs, search="exhaustive", budget_s=15.0):
+    """The oracle, as it stands, on this host's cores, on a bounded stratified sample of the same
+    workload (all threads, plus a 1-thread figure on a smaller sample)."""
     threads = os.cpu_count() or 1
-    inst = inputs["inst"]
-
-    def run(k):
-        sub = inst[:k]
-        last = int(sub[-1]["req_begin"] + sub[-1]["n_run"] + sub[-1]["n_queue"])
-        t = time.perf_counter()
-        oracle.decide(m, sub, inputs["req"][:last], inputs["t_dead"][:last], inputs["H"], inputs["freq"],
-                      inputs["tbt_slo"], want_grid=False, want_curves=False, threads=threads, search=search)
-        return time.perf_counter() - t
-
-    k = min(len(inst), max(threads, 8))
-    dt = run(k)
-    while k < len(inst) and dt < 1.0:
-        k = min(len(inst), k * 4)
-        dt = run(k)
-    if k < len(inst) and dt < budget_s:
-        k = min(len(inst), max(k, int(k * budget_s / max(dt, 1e-3))))
-        dt = run(k)
+    I = len(inputs["inst"])
+    k = min(I, max(threads * 4, 32))
+    dt = oracle_time(blob, sample_inputs(inputs, stratified(I, k)), threads, search)
+    if k < I and dt < budget_s:
+        k = min(I, max(k, int(k * budget_s / max(dt, 1e-3))))
+        dt = oracle_time(blob, sample_inputs(inputs, stratified(I, k)), threads, search)
+    k1 = max(1, min(I, int(k * 2.0 / max(dt * threads, 1e-3))))        # ~2 s single-threaded
+    dt1 = oracle_time(blob, sample_inputs(inputs, stratified(I, k1, 1)), 1, search)
     return {"value": k / dt, "unit": "decisions/s", "cores": threads, "kind": "oracle",
-            "sample": f"first {k} of {len(inst)} instances of {cfg.name} ("
-                      + ("all F levels evaluated" if search == "exhaustive" else "the paper's binary search")
-                      + f", {threads} threads), {dt:.1f} s"}
+            "cpu_model": cpu_model(),
+            "sample": f"{k} of {len(inputs['inst'])} instances of {cfg.name} (stratified, every "
+                      f"{max(1, I // k)}th) on {threads} threads, {dt:.1f} s; "
+                      + ("all F levels evaluated" if search == "exhaustive" else "the paper's binary search"),
+            "one_thread": {"value": k1 / dt1, "unit": "decisions/s", "cores": 1,
+                           "sample": f"{k1} instances (stratified), {dt1:.1f} s"}}
 
 
 def bench_reference(args, cfg):
-    """--impl reference: the CPU oracle is this tier's reference arm (rank 0 only)."""
-    rank = env_int("RANK", 0)
-    if rank != 0:
+    """--impl reference: the CPU oracle is this tier's reference arm (rank 0 only), on the same
+    workload as our arm: each step decides a bounded stratified sample of it."""
+    if env_int("RANK", 0) != 0:
         return
     blob = W.write_blob(W.config_ensemble(cfg))
-    per_step = {"C1": 1, "C2": 64, "C3": 16, "C4": 8, "C5": 16}[cfg.name]
-    inputs = W.config_inputs(cfg, 0, max(per_step, 1))
-    from oracle import oracle
-    m = oracle.Model(blob)
+    world = max(args.gpus, env_int("WORLD_SIZE", 1))
+    _, _, I_glob = shard_of(cfg, 0, world)
+    inputs = W.config_inputs(dataclasses_replace(cfg, I_glob))
+    per_step = args.ref_per_step or {"C1": 1, "C2": 256, "C3": 256, "C4": 128, "C5": 256}[cfg.name]
     threads = os.cpu_count() or 1
-
-    def step():
-        oracle.decide(m, inputs["inst"], inputs["req"], inputs["t_dead"], inputs["H"], inputs["freq"],
-                      inputs["tbt_slo"], want_grid=False, want_curves=False, threads=threads, search=args.search)
-    for _ in range(args.warmup):
-        step()
-    t = time.perf_counter()
-    for _ in range(args.steps):
-        step()
-    dt = time.perf_counter() - t
+    subs = [sample_inputs(inputs, stratified(I_glob, per_step, s)) for s in range(args.warmup + args.steps)]
+    for s in range(args.warmup):
+        oracle_time(blob, subs[s], threads, args.search)
+    dt = sum(oracle_time(blob, subs[args.warmup + s], threads, args.search) for s in range(args.steps))
     v = per_step * args.steps / dt
-    line = {"impl": "reference", "metric": "frequency decisions/sec", "value": v, "unit": "decisions/s",
-            "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup, "ms_per_step": dt / args.steps * 1e3,
-            "higher_is_better": True, "scaling": "weak" if cfg.name != "C5" else "strong", "vs_baseline": None,
+    line = {"impl": "reference", "metric": METRIC, "value": v, "unit": "decisions/s",
+            "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": dt / args.steps * 1e3,
+            "higher_is_better": True, "scaling": "weak" if cfg.name == "C2" else "strong", "vs_baseline": None,
             "dtype": "f32", "data": "synthetic",
-            "config": {"workload": DESCR[cfg.name], "name": cfg.name, "instances_per_step": per_step,
-                       "search": args.search},
+            "config": {"workload": DESCR[cfg.name], "name": cfg.name, "global_instances": I_glob,
+                       "instances_per_step": per_step, "search": args.search,
+                       "sample": "each step decides a different stratified sample of the same workload"},
             "cpu_baseline": {"value": v, "unit": "decisions/s", "cores": threads, "kind": "oracle",
-                             "sample": f"first {per_step} instances of {cfg.name} per step"},
+                             "cpu_model": cpu_model(),
+                             "sample": f"{per_step} of {I_glob} instances of {cfg.name} per step (stratified)"},
             "e2e": {"value": v, "unit": "decisions/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
 
@@ -222,7 +250,7 @@ def bench_replay(args, cfg, rank, world, local, dist, dist_test):
     I = rc.n_inst
     st = rp.stats_dict()
     line = {
-        "metric": "frequency decisions/sec", "value": I * args.steps / (float(tot[0]) / 1e3), "unit": "decisions/s",
+        "metric": METRIC, "value": I * args.steps / (float(tot[0]) / 1e3), "unit": "decisions/s",
         "n_gpus": world, "steps": args.steps, "warmup": max(args.warmup, 3),
         "ms_per_step": float(tot[0]) / args.steps, "higher_is_better": True, "scaling": "strong",
         "vs_baseline": None, "dtype": "f32", "data": "synthetic",
@@ -236,8 +264,6 @@ def bench_replay(args, cfg, rank, world, local, dist, dist_test):
         "decisions_per_sec_decide_only": I * args.steps / (float(tot[1]) / 1e3),
         "per_round_ms": {"decide": dec_ms / args.steps, "advance": adv_ms / args.steps},
         "replay_stats_after_warmup_and_steps": st,
-        # per round without admission: K1c (+ hand-over kernel at one warp per instance), the K2
-        # phases, K3c, the replay advance; with admission control the prefix pass adds its own
         "gpu_launches": (None if args.admission else
                          (3 + k2_phases(model.info()) + int((i1 - i0) * 2 > sms * 32)) * args.steps),
         "clocks": clk,
@@ -248,33 +274,37 @@ def bench_replay(args, cfg, rank, world, local, dist, dist_test):
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=100)
+    ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=5)
-    ap.add_argument("--workload", default="C2", choices=sorted(DESCR))
+    ap.add_argument("--workload", default="C5", choices=sorted(DESCR))
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--e2e-steps", type=int, default=None)
+    ap.add_argument("--ref-per-step", type=int, default=None,
+                    help="reference arm: instances the oracle decides per step (default per workload)")
+    ap.add_argument("--instances", type=int, default=None,
+                    help="override the workload's global instance count (tests; the line says so)")
+    ap.add_argument("--dump-decisions", default=None,
+                    help="rank 0 writes the gathered [2, I] (level, status) rows of the last step (.npy)")
     ap.add_argument("--admission", type=int, default=0,
                     help="C4 replay: run the paper's full admission control on up to N queued requests per instance")
     ap.add_argument("--search", default="exhaustive", choices=["exhaustive", "binary"],
                     help="K3 order: lowest passing level over all levels (reading A-13, default) or the "
-                         "paper's binary search (P:555, reading A-24; needs --k2 fused)")
+                         "paper's binary search (P:555, reading A-24)")
     ap.add_argument("--graph", dest="graph", action="store_true", default=True,
                     help="time the step as a replayed CUDA graph of its kernels (default; SURVEY §8d)")
     ap.add_argument("--no-graph", dest="graph", action="store_false",
                     help="launch the kernels one by one in the timed steps")
-    ap.add_argument("--k2", default="compact", choices=["compact", "fused", "cells", "runs", "direct"],
-                    help="path: compact (K1c runs + deadline list -> K2 on the cells -> K3c, default), "
-                         "cell-memoised fused with K3, cell-memoised with the ips grid, run-compressed, or "
-                         "one evaluation per grid point")
     args = ap.parse_args()
     cfg = W.CONFIGS[args.workload]
+    if args.instances:
+        cfg = dataclasses_replace(cfg, args.instances)
     if args.impl == "reference":
         return bench_reference(args, cfg)
 
     import torch
     import torch.distributed as dist
-    from paper_2408_05235_b200 import runner, tp
+    from paper_2408_05235_b200 import runner, shard, tp
 
     world = env_int("WORLD_SIZE", 1)
     rank = env_int("RANK", 0)
@@ -294,15 +324,13 @@ def main():
         else:
             dist.init_process_group("nccl", device_id=dev)
 
-    def _coll(t, fn):
-        if not dist_test:
-            return fn(t)
-        c = t.cpu()
-        fn(c)
-        t.copy_(c)
-
     def all_reduce(t, op):
-        _coll(t, lambda x: dist.all_reduce(x, op=op))
+        if not dist_test:
+            dist.all_reduce(t, op=op)
+            return
+        c = t.cpu()
+        dist.all_reduce(c, op=op)
+        t.copy_(c)
 
     if cfg.name == "C4":
         bench_replay(args, cfg, rank, world, local, dist, dist_test)
@@ -315,74 +343,50 @@ def main():
     I, R = len(inputs["inst"]), len(inputs["req"])
     model = tp.Gbdt(blob, local)
     info = model.info()
-    rnd = runner.Round(inputs, dev, k2_mode=args.k2, model=model, search=args.search)
-    rnd.bkv = False          # compact path: the B/KV curves stay on chip
-    dec = torch.empty((2, max(I, 1)), dtype=torch.int32, device=dev)   # level, status rows
-    rnd.level, rnd.status = dec[0], dec[1]
-    # equal shards (C2 weak, C5 = 262144 / {1,2,4,8}): one preallocated all-gather of [2, I] rows
-    gathered = torch.empty((world * 2, max(I, 1)), dtype=torch.int32, device=dev) if world > 1 else None
+    counts = [shard_of(cfg, r, world)[1] - shard_of(cfg, r, world)[0] for r in range(world)]
+    gather = shard.DecisionGather(counts, dev, host_staging=dist_test) if world > 1 else None
+    rows = gather.rows() if gather else torch.empty((2, max(I, 1)), dtype=torch.int32, device=dev)
+    # the exact step (runner.BenchStep): K1c -> K2 cell phases -> K3c, B/KV on chip, PDL, one graph;
+    # level / status written straight into the gather's send rows
+    step = runner.BenchStep(inputs, dev, model, search=args.search, graph=args.graph, level=rows[0],
+                            status=rows[1])
+    rnd = step.rnd
     stream = torch.cuda.current_stream(dev)
     flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)     # > 126 MB L2
 
-    def kernels(strm):
-        rnd.project(strm)
-        rnd.predict(model, strm)
-        rnd.select(strm)
-
-    graph = None
-    if args.graph:           # the K1 -> K2 -> K3 sequence captured once, replayed every step
-        gs = torch.cuda.Stream(dev)
-        with torch.cuda.stream(gs):
-            kernels(gs)      # warm-up on the capture stream (attributes, lazy module loading)
-        torch.cuda.synchronize(dev)
-        graph = torch.cuda.CUDAGraph()
-        with torch.cuda.graph(graph, stream=gs):
-            kernels(gs)
-        torch.cuda.synchronize(dev)
-
-    def step(evs=None, split=True):
-        # split=False: events only around the whole step (an event between two kernels stops the
-        # second from launching early -- programmatic dependent launch -- and costs ~4 us each)
+    def one_step(evs=None):
         if evs:
             evs[0].record(stream)
-        if graph is not None and not split:
-            graph.replay()
-        else:
+        if evs and len(evs) == 5:     # instrumented: kernel by kernel, events between kernels
             rnd.project(stream)
-            if evs and split:
-                evs[1].record(stream)
+            evs[1].record(stream)
             rnd.predict(model, stream)
-            if evs and split:
-                evs[2].record(stream)
+            evs[2].record(stream)
             rnd.select(stream)
-            if evs and split:
-                evs[3].record(stream)
-        if world > 1:
-            if dist_test:
-                g = torch.empty(gathered.shape, dtype=gathered.dtype)
-                dist.all_gather_into_tensor(g, dec.cpu())
-                gathered.copy_(g)
-            else:
-                dist.all_gather_into_tensor(gathered, dec)
+            evs[3].record(stream)
+        else:
+            step.run(stream)
+        if gather is not None:
+            gather.gather()
         if evs:
-            evs[4].record(stream)
+            evs[-1].record(stream)
 
     for _ in range(max(args.warmup, 3)):
-        step()
+        one_step()
     torch.cuda.synchronize(dev)
 
-    # algorithmic grid size of this rank (from K1's outputs; not timed)
+    # algorithmic sizes of this rank's step (from K1c's outputs; read once, untimed)
     n_h = rnd.n[:I].cpu().numpy().astype(np.int64)
     st_h = rnd.status[:I].cpu().numpy().view(np.uint32)
-    grid = int((n_h * ((st_h & SKIP) == 0)).sum()) * rnd.F
-    padded = int((((n_h + 31) // 32) * 32 * ((st_h & SKIP) == 0)).sum()) * rnd.F
-    evaluated = {"runs": lambda: tp.runs_total(rnd.work, I, rnd.H) * rnd.F,
-                 "cells": lambda: tp.cells_total(rnd.work, model, I, rnd.H, rnd.F) * rnd.F,
-                 "fused": lambda: tp.cells_total(rnd.work, model, I, rnd.H, rnd.F) * rnd.F,
-                 "compact": lambda: tp.cells_total(rnd.work, model, I, rnd.H, rnd.F) * rnd.F,
-                 "direct": lambda: grid}[args.k2]()
+    nadm_h = rnd.n_adm[:I].cpu().numpy().astype(np.int64)
+    live = (st_h & SKIP) == 0
+    grid = int((n_h * live).sum()) * rnd.F
+    cs = tp.compact_stats(model, rnd.work, I, rnd.H, rnd.F)
+    evaluated = cs["cells"] * rnd.F          # K2's model evaluations (LUT rows x levels)
+    n_req_all = int((inputs["inst"]["n_run"].astype(np.int64) + inputs["inst"]["n_queue"]).sum())
+    n_sched = int(inputs["inst"]["n_run"].astype(np.int64).sum() + nadm_h.sum())
 
-    evs = [[torch.cuda.Event(enable_timing=True) for _ in range(5)] for _ in range(args.steps)]
+    evs = [[torch.cuda.Event(enable_timing=True) for _ in range(2)] for _ in range(args.steps)]
     clocks = Clocks(local)
     if world > 1:
         dist.barrier()
@@ -391,25 +395,30 @@ def main():
     time.sleep(0.3)
     for k in range(args.steps):
         flush.zero_()                      # untimed L2 flush between timed steps
-        step(evs[k], split=False)
+        one_step(evs[k])
     torch.cuda.synchronize(dev)
     clk = clocks.stop()
     if world > 1:
         dist.barrier()
-    step_ms = np.array([e[0].elapsed_time(e[4]) for e in evs])            # ms, the K timed steps
+    step_ms = np.array([a.elapsed_time(b) for a, b in evs])            # ms, the K timed steps
     t_total = float(step_ms.sum())
-    # per-kernel breakdown (and the K2 time of the roofline): a second pass of K steps with events
-    # between the kernels, same inputs, same L2 flushes
+    if args.dump_decisions:
+        res = gather.result() if gather is not None else rows[:, :I]
+        if rank == 0:
+            np.save(args.dump_decisions, res.cpu().numpy())
+    # per-kernel breakdown (the kernel times of the rooflines): a second pass of K steps kernel by
+    # kernel with events between the kernels, same inputs, same L2 flushes
     evk = [[torch.cuda.Event(enable_timing=True) for _ in range(5)] for _ in range(args.steps)]
     for k in range(args.steps):
         flush.zero_()
-        step(evk[k])
+        one_step(evk[k])
     torch.cuda.synchronize(dev)
     per = np.array([[e[j].elapsed_time(e[j + 1]) for j in range(4)] for e in evk])   # ms
     k_ms = per.mean(axis=0)
-    # the north_star's direct K2 (one descent per grid point), timed on the same inputs for reference
+    # the north_star's direct K2 (one descent per grid point) on the same inputs, where its ips
+    # grid fits (I x F x H fp32)
     d_ms = None
-    if args.k2 != "direct":
+    if I * rnd.F * rnd.H * 4 <= (16 << 30):
         rd = runner.Round(inputs, dev, k2_mode="direct")
         rd.project(stream)
         rd.predict(model, stream)
@@ -422,53 +431,47 @@ def main():
         torch.cuda.synchronize(dev)
         d_ms = float(np.median([a.elapsed_time(b) for a, b in de]))
         del rd
-    tot = torch.tensor([t_total, grid, I], dtype=torch.float64, device=dev)
+    tot = torch.tensor([t_total, grid, I, evaluated], dtype=torch.float64, device=dev)
     if world > 1:
         mx = tot[:1].clone()
         sm = tot[1:].clone()
         all_reduce(mx, dist.ReduceOp.MAX)
         all_reduce(sm, dist.ReduceOp.SUM)
         tot = torch.cat([mx, sm])
-    t_max_ms, grid_all, inst_all = float(tot[0]), float(tot[1]), float(tot[2])
+    t_max_ms, grid_all, inst_all, eval_all = (float(x) for x in tot)
     sec = t_max_ms / 1e3
     decisions_per_s = inst_all * args.steps / sec
-    grid_per_s = grid_all * args.steps / sec
 
     # end to end through the C ABI with host buffers (pinned), copies inside the timed region
-    e2e = None
-    if True:
-        ctx = tp.Ctx(local, I, R, rnd.H, rnd.F, model if args.k2 in ("cells", "fused", "compact") else None)
-        ctx.set_k2_mode({"direct": tp.K2_DIRECT, "compact": tp.K2_COMPACT}.get(args.k2, tp.K2_RUNS))
-        ctx.set_search(args.search)
-        # one pinned host buffer [inst | req | t_dead] (tp_decide_host then copies it in one go) and
-        # one [level | status] buffer for the results
-        bi, br, bd = inputs["inst"].nbytes, inputs["req"].nbytes, inputs["t_dead"].nbytes
-        h_in = torch.empty(bi + br + bd, dtype=torch.uint8).pin_memory()
-        h_in[:bi].copy_(torch.from_numpy(inputs["inst"].view(np.uint8)))
-        h_in[bi:bi + br].copy_(torch.from_numpy(inputs["req"].view(np.uint8)))
-        h_in[bi + br:].copy_(torch.from_numpy(np.ascontiguousarray(inputs["t_dead"]).view(np.uint8)))
-        h_inst, h_req, h_td = h_in[:bi], h_in[bi:bi + br], h_in[bi + br:].view(torch.float64)
-        h_out = torch.empty((2, max(I, 1)), dtype=torch.int32).pin_memory()
-        h_level, h_status = h_out[0], h_out[1]
-        ke = args.e2e_steps or args.steps
-        for _ in range(3):
-            ctx.decide_host(model, h_inst, I, h_req, R, h_td, rnd.freq, rnd.tbt, h_level, h_status, stream)
-        torch.cuda.synchronize(dev)
-        ee = [[torch.cuda.Event(enable_timing=True) for _ in range(2)] for _ in range(ke)]
-        for k in range(ke):
-            flush.zero_()
-            ee[k][0].record(stream)
-            ctx.decide_host(model, h_inst, I, h_req, R, h_td, rnd.freq, rnd.tbt, h_level, h_status, stream)
-            ee[k][1].record(stream)
-        torch.cuda.synchronize(dev)
-        te = torch.tensor([sum(a.elapsed_time(b) for a, b in ee)], dtype=torch.float64, device=dev)
-        if world > 1:
-            all_reduce(te, dist.ReduceOp.MAX)
-        ok = np.array_equal(h_level[:I].numpy(), dec[0, :I].cpu().numpy())
-        e2e = {"value": inst_all * ke / (float(te[0]) / 1e3), "unit": "decisions/s",
-               "h2d_bytes_per_step": int(I * 48 + R * 16 + R * 8), "d2h_bytes_per_step": int(I * 8),
-               "matches_device_path": bool(ok)}
-        ctx.free()
+    ctx = tp.Ctx(local, I, R, rnd.H, rnd.F, model)
+    ctx.set_search(args.search)
+    bi, br, bd = inputs["inst"].nbytes, inputs["req"].nbytes, inputs["t_dead"].nbytes
+    h_in = torch.empty(bi + br + bd, dtype=torch.uint8).pin_memory()     # [inst | req | t_dead]: one copy
+    h_in[:bi].copy_(torch.from_numpy(inputs["inst"].view(np.uint8)))
+    h_in[bi:bi + br].copy_(torch.from_numpy(inputs["req"].view(np.uint8)))
+    h_in[bi + br:].copy_(torch.from_numpy(np.ascontiguousarray(inputs["t_dead"]).view(np.uint8)))
+    h_inst, h_req, h_td = h_in[:bi], h_in[bi:bi + br], h_in[bi + br:].view(torch.float64)
+    h_out = torch.empty((2, max(I, 1)), dtype=torch.int32).pin_memory()   # [level | status]: one copy
+    ke = args.e2e_steps or min(args.steps, 10)
+    for _ in range(3):
+        ctx.decide_host(model, h_inst, I, h_req, R, h_td, rnd.freq, rnd.tbt, h_out[0], h_out[1], stream)
+    torch.cuda.synchronize(dev)
+    ee = [[torch.cuda.Event(enable_timing=True) for _ in range(2)] for _ in range(ke)]
+    for k in range(ke):
+        flush.zero_()
+        ee[k][0].record(stream)
+        ctx.decide_host(model, h_inst, I, h_req, R, h_td, rnd.freq, rnd.tbt, h_out[0], h_out[1], stream)
+        ee[k][1].record(stream)
+    torch.cuda.synchronize(dev)
+    te = torch.tensor([sum(a.elapsed_time(b) for a, b in ee)], dtype=torch.float64, device=dev)
+    if world > 1:
+        all_reduce(te, dist.ReduceOp.MAX)
+    ok = np.array_equal(h_out[0, :I].numpy(), rows[0, :I].cpu().numpy())
+    e2e = {"value": inst_all * ke / (float(te[0]) / 1e3), "unit": "decisions/s",
+           "h2d_bytes_per_step": int(bi + br + bd), "d2h_bytes_per_step": int(I * 8),
+           "api": "tp_decide_host (pinned host buffers, one H2D + one D2H copy per step)",
+           "matches_device_path": bool(ok)}
+    ctx.free()
 
     if rank != 0:
         if world > 1:
@@ -477,74 +480,106 @@ def main():
 
     peaks = measured_peaks()
     smax = float(peaks.get("sm_max_mhz", 1965.0))
-    # K2 roofline: shared-memory load bandwidth, 128 B/clk/SM (B200_PROFILING / B300_MICROARCH
-    # LDS crossbar) x 148 SMs x max SM clock.  Algorithmic bytes per grid point: T*(D+1) 4-byte
-    # node/leaf words.
+    hbm = float(peaks.get("hbm_gbs", 6553.6))
     sms = torch.cuda.get_device_properties(dev).multi_processor_count
-    per_pt = info.n_trees * (info.depth + 1) * 4
-    k2_s = k_ms[1] / 1e3
-    achieved = evaluated * per_pt / k2_s / 1e9     # this rank's K2 (incl. the run pre-pass), GB/s
-    peak = sms * 128 * smax * 1e6 / 1e9
-    traffic = None
-    try:
-        with open(os.path.join(ROOT, "profiles", "k2_traffic.json")) as f:
-            tj = json.load(f)
-        if tj.get("workload") == cfg.name:
-            traffic = tj.get("dram_bytes_per_launch")
-    except (OSError, ValueError):
-        pass
-    roof = {"bound": "smem", "kernel": {"direct": "k2_gbdt", "runs": "k2_gbdt<runs> (+ k2_runs pre-pass)",
-                                        "cells": "k2_gbdt<cells> (+ k2_runs pre-pass, k2_expand)",
-                                        "fused": "k2_gbdt<cells> (+ k2_runs pre-pass)",
-                                        "compact": f"k2_cells_phase<{info.depth},2> x {k2_phases(info)} "
-                                                   "tree-resident phases (runs built by K1c)"}[args.k2],
-            "achieved": achieved, "peak": peak, "unit": "GB/s",
-            "frac": achieved / peak, "traffic": traffic,
-            "peak_basis": f"{sms} SMs x 128 B/clk (LDS) x sm_max_mhz {smax:.0f} (MEASURED_PEAKS.json clock)",
-            "frac_at_observed_clock": (achieved / (sms * 128 * clk["sm_mhz"] * 1e6 / 1e9)) if clk["sm_mhz"] else None,
-            "bytes_per_evaluated_row": per_pt, "evaluated_rows_per_launch": evaluated,
-            "grid_points_per_launch": grid, "padded_grid_points": padded}
+    traffic = load_traffic(cfg.name)
+    # K1c (HBM): header 48 B + 16 B per request record + 8 B t_dead per scheduled request read;
+    # n / n_adm / status 12 B + 16 B per piece record (start, cell id, Dmin) written
+    k1_bytes = 48 * I + 16 * n_req_all + 8 * n_sched + 12 * I + 16 * cs["pieces"]
+    # K2 (shared-memory loads): T * (D + 1) 4-byte node / leaf words per evaluated row
+    per_row = info.n_trees * (info.depth + 1) * 4
+    # K3c (HBM): n + status 8 B in, 16 B per piece record in, level 4 B out; the T' LUT reads
+    # (F * 8 B per piece) stay on chip / in L2
+    k3_bytes = 12 * I + 16 * cs["pieces"]
+    lds_peak = sms * 128 * smax * 1e6 / 1e9
+    kern = {
+        "k1": roof("hbm", "k1_packed / k1_compact (K1c: projection, gate, pieces, cell claims, Eq. 4 minima)",
+                   k1_bytes, k_ms[0], hbm, traffic.get("k1"),
+                   basis="48 + 16 (R+Q) + 8 (R+Q_adm) + 12 + 16 pieces bytes per instance"),
+        "k2": roof("smem", f"k2_cells_phase<{info.depth},2> x {k2_phases(info)} tree-resident phases",
+                   evaluated * per_row, k_ms[1], lds_peak, traffic.get("k2"),
+                   basis=f"{per_row} B of node/leaf words per evaluated row (cells x levels); peak {sms} SMs x "
+                         f"128 B/clk x {smax:.0f} MHz"),
+        "k3": roof("hbm", "k3_compact<W> (K3c: exact T_R per piece, Eq. 4, TBT, ballot argmin)",
+                   k3_bytes, k_ms[2], hbm, traffic.get("k3"),
+                   basis="12 + 16 pieces bytes per instance (LUT reads are L2 traffic)",
+                   extra={"lut_bytes_l2": 8 * rnd.F * cs["pieces"],
+                          "tick_updates_per_s": rnd.F * cs["pieces"] / (k_ms[2] / 1e3)}),
+    }
+    dom = max(kern, key=lambda k: kern[k]["ms"])
+    roofline = dict(kern[dom], dominant=dom, per_kernel=kern)
     if d_ms is not None:
-        da = grid * per_pt / (d_ms / 1e3) / 1e9
-        roof["direct_k2"] = {"ms": d_ms, "achieved": da, "frac": da / peak,
-                             "note": "tp_predict_ips (one descent per grid point) on the same inputs"}
+        da = grid * per_row / (d_ms / 1e3) / 1e9
+        roofline["direct_k2"] = {"ms": d_ms, "achieved": da, "frac": da / lds_peak,
+                                 "note": "tp_predict_ips (one descent per grid point) on the same inputs"}
     cpu = None
     if world == 1 and not args.no_cpu_baseline:
         cpu = cpu_baseline(cfg, blob, inputs, search=args.search)
+    dist_info = None
+    if world > 1:
+        dist_info = {"backend": dist.get_backend(), "world_size": world,
+                     "nccl": ".".join(map(str, torch.cuda.nccl.version())) if not dist_test else None}
     line = {
-        "metric": "frequency decisions/sec", "value": decisions_per_s, "unit": "decisions/s",
+        "metric": METRIC, "value": decisions_per_s, "unit": "decisions/s",
         "n_gpus": world, "steps": args.steps, "warmup": max(args.warmup, 3), "ms_per_step": t_max_ms / args.steps,
-        "higher_is_better": True, "scaling": "strong" if cfg.name == "C5" else "weak", "vs_baseline": None,
+        "higher_is_better": True, "scaling": "weak" if cfg.name == "C2" else "strong", "vs_baseline": None,
         "dtype": "f32", "data": "synthetic",
         "config": {"workload": DESCR[cfg.name], "name": cfg.name, "instances_per_gpu": I,
                    "global_instances": int(inst_all), "H": cfg.H, "F": cfg.F, "trees": info.n_trees,
-                   "depth": info.depth, "parallelism": f"instance-sharded x{world}" + (" + NCCL all-gather" if world > 1 else ""),
-                   "l2": "flushed between timed steps (256 MiB device write, untimed)", "k2": args.k2,
-                   "cuda_graph": bool(args.graph),
-                   "search": args.search},
-        "grid_evals_per_sec": grid_per_s,
+                   "depth": info.depth,
+                   "parallelism": f"instance-sharded x{world}" + (" + NCCL all-gather" if world > 1 else ""),
+                   "l2": "flushed between timed steps (256 MiB device write, untimed)",
+                   "path": "compact: K1c -> K2 cell phases -> K3c (B/KV on chip), PDL, "
+                           + ("one CUDA graph per step" if args.graph else "kernel by kernel"),
+                   "search": args.search,
+                   "instances_override": bool(args.instances)},
+        "grid_evals_per_sec": grid_all * args.steps / sec,
+        "grid_evals_note": "(instance, level, m <= n) grid points whose IPS each step determines (sum F*n_i); "
+                           "the model is evaluated once per distinct cell and level (model_evals_per_sec)",
+        "model_evals_per_sec": eval_all * args.steps / sec,
+        "model_evals_per_sec_k2_only": evaluated / (k_ms[1] / 1e3),
+        "counts_per_step_rank0": {"instances": I, "requests": n_req_all, "scheduled": n_sched,
+                                  "pieces": cs["pieces"], "end_positions": cs["ends"], "cells": cs["cells"],
+                                  "grid_points": grid},
         "step_ms_pctl": {"p10": float(np.percentile(step_ms, 10)), "p50": float(np.percentile(step_ms, 50)),
                          "p90": float(np.percentile(step_ms, 90)), "rank": "0"},
-        "per_kernel_ms": {"k1_project": k_ms[0], "k2_gbdt": k_ms[1], "k3_select": k_ms[2],
-                          "gather": k_ms[3],
-                          "note": "from a second pass of the same steps with events between the kernels "
-                                  "(those events stop programmatic dependent launch; the timed steps carry "
-                                  "events only at their ends)"},
-        "roofline": roof,
+        "per_kernel_ms": {"k1_project": k_ms[0], "k2_gbdt": k_ms[1], "k3_select": k_ms[2], "gather": k_ms[3],
+                          "note": "second pass of the same steps, kernel by kernel with events between the kernels "
+                                  "(the timed steps replay one graph with events only at their ends)"},
+        "roofline": roofline,
         "cpu_baseline": cpu,
         "e2e": e2e,
-        # our kernels per step: k1_project / k1_compact, [k2_runs], k2_gbdt, [k2_expand], k3_select* / k3_compact
-        # compact: K1c (+ the hand-over kernel after k1_packed at one warp per instance, i.e. when
-        # the batch exceeds 16 warps per SM), the K2 phases, K3c
-        "gpu_launches": {"direct": 3, "runs": 4, "cells": 5, "fused": 4,
-                         "compact": 2 + k2_phases(info) + int(I * 2 > sms * 32)}[args.k2] * args.steps,
+        # our kernels per step: K1c (k1_packed + the hand-over k1_compact<1,1> at one warp per
+        # instance, i.e. when the batch exceeds 16 warps per SM), the K2 phases, K3c
+        "gpu_launches": (2 + k2_phases(info) + int(I * 2 > sms * 32)) * args.steps,
         "clocks": clk,
+        "dist": dist_info,
         "paper_context": "paper controller on host CPU (A100 box): projection <2 ms, model ~3 ms per call, "
                          "scheduler+throttle 35 ms per decision (P:466, P:495, P:557)",
     }
     print(json.dumps(line), flush=True)
     if world > 1:
         dist.destroy_process_group()
+
+
+def roof(bound, kernel, algo_bytes, ms, peak_gbs, traffic, basis, extra=None):
+    achieved = algo_bytes / (ms / 1e3) / 1e9
+    r = {"bound": bound, "kernel": kernel, "achieved": achieved, "peak": peak_gbs, "unit": "GB/s",
+         "frac": achieved / peak_gbs, "traffic": traffic, "ms": ms, "algorithmic_bytes": int(algo_bytes),
+         "basis": basis}
+    if extra:
+        r.update(extra)
+    return r
+
+
+def load_traffic(name):
+    """ncu dram__bytes (read + write) per launch of each kernel, from the committed capture of
+    this workload (profiles/traffic_<name>.json), or {}."""
+    try:
+        with open(os.path.join(ROOT, "profiles", f"traffic_{name}.json")) as f:
+            return json.load(f).get("dram_bytes_per_launch", {})
+    except (OSError, ValueError):
+        return {}
 
 
 def k2_phases(info):

@@ -253,8 +253,8 @@ int tp_select_freq_binary(const tp_gbdt* m, const void* workspace, const tp_inst
  *   (running or admitted) request, Dmin[l] = min ceil(fl64(t_dead - t_cur) * 2^40) (reading A-12).
  *   B / KV [dev] optional (both NULL or both set): full [n_inst][H] rows as tp_project if
  *   bkv_rows = 1, only the m = 1 column (B[i*H], KV[i*H]) if bkv_rows = 0.
- *   t_dead [dev] fp64 seconds per request entry (as tp_select_freq).  H <= ~12000 (per-warp shared
- *   histograms; larger H -> TP_EINVAL).
+ *   t_dead [dev] fp64 seconds per request entry (as tp_select_freq).  H <= 16384 (the per-warp
+ *   shared histograms fit up to H = 16384; larger H fails the general H check with TP_EINVAL).
  * tp_predict_cells -- K2 on the claimed cells: LUT[cell][u] = clamp(M(cell, freq_mhz[u])) (as
  *   tp_predict_ips_runs in cell mode; no pre-pass: the runs come from tp_project_compact).
  * tp_select_freq_compact -- K3c, one warp per instance, lane u = level u: T_R formed run by run
@@ -274,6 +274,13 @@ int tp_select_freq_compact(const tp_gbdt* m, const void* workspace, size_t works
                            const int32_t* n, int32_t H, int32_t F, float tbt_slo, int32_t search,
                            int32_t* level, uint32_t* status, void* stream);
 
+/* Statistics of the last tp_project_compact on `workspace` (host copies; synchronises the device):
+ * out[0] = pieces over all instances (the records K1c wrote and K3c walks), out[1] = end positions
+ * (iterations where a scheduled request finishes), out[2] = distinct cells claimed (LUT rows K2
+ * evaluates).  For measurement (bench.py's algorithmic byte counts), not on the decision path. */
+int tp_compact_stats(const tp_gbdt* m, const void* workspace, size_t workspace_bytes, int32_t n_inst,
+                     int32_t H, int32_t F, int64_t* out);
+
 /*
  * Convenience: one decision round with library-owned scratch.
  * tp_ctx_create allocates, on `device`, B/KV/n/n_adm (n_inst_max x H), the ips grid
@@ -285,7 +292,8 @@ int tp_ctx_create(int device, const tp_gbdt* model, int32_t n_inst_max, int32_t 
                   int32_t F_max, tp_ctx** out);
 int tp_ctx_free(tp_ctx* c);
 
-/* K1 -> K2 -> K3 on device-resident inputs; level/status [dev] out.  With TP_K2_COMPACT (the default
+/* K1 -> K2 -> K3 on device-resident inputs; level/status [dev] out.  tp_decide, tp_decide_host
+ * and tp_decide_admit make the context's device current for the call and restore the caller's.  With TP_K2_COMPACT (the default
  * for a context created for `m`) the compact path runs: tp_project_compact (B/KV: m = 1 column only)
  * -> tp_predict_cells -> tp_select_freq_compact.  With TP_K2_RUNS (the default otherwise) and a
  * context created for `m`, K2 runs in cell mode without materialising the ips grid
@@ -333,9 +341,10 @@ enum { TP_K2_DIRECT = 0, TP_K2_RUNS = 1, TP_K2_COMPACT = 2 };
 int tp_ctx_set_k2_mode(tp_ctx* c, int mode);   /* may allocate the ips grid: TP_ENOMEM */
 
 /* K3 search order for tp_decide / tp_decide_host / tp_decide_admit (default exhaustive, reading
- * A-13).  TP_SEARCH_BINARY (reading A-24, tp_select_freq_binary) needs the fused cell path: a
- * context created for the model, TP_K2_RUNS and H <= 8192; otherwise those calls return
- * TP_ENOTIMPL. */
+ * A-13).  TP_SEARCH_BINARY (reading A-24) is supported by the compact path (TP_K2_COMPACT, the
+ * default: K3c replays the search on its per-level pass bits) and by the fused cell path
+ * (TP_K2_RUNS with a context created for the model and H <= 8192, tp_select_freq_binary); with
+ * TP_K2_DIRECT, or TP_K2_RUNS without a cell-mode model, those calls return TP_ENOTIMPL. */
 enum { TP_SEARCH_EXHAUSTIVE = 0, TP_SEARCH_BINARY = 1 };
 int tp_ctx_set_search(tp_ctx* c, int search);
 

@@ -22,6 +22,21 @@ bool H_ok(int32_t H) { return H >= 1 && H <= tp::kMaxH; }
 
 cudaStream_t S(void* s) { return reinterpret_cast<cudaStream_t>(s); }
 
+// Makes the context's device current for one call (the launch helpers read per-device attributes
+// of the current device) and restores the caller's on return.
+struct DeviceGuard {
+    int prev = -1;
+    bool ok = true;
+    explicit DeviceGuard(int dev) {
+        if (cudaGetDevice(&prev) != cudaSuccess) prev = -1;
+        if (prev != dev) ok = cudaSetDevice(dev) == cudaSuccess;
+    }
+    ~DeviceGuard() {
+        int cur = -1;
+        if (prev >= 0 && cudaGetDevice(&cur) == cudaSuccess && cur != prev) cudaSetDevice(prev);
+    }
+};
+
 }  // namespace
 
 struct tp_ctx {
@@ -179,6 +194,32 @@ int tp_cells_total(const tp_gbdt* m, const void* workspace, int32_t n_inst, int3
     if (cudaMemcpy(&c, p.cell_count, 4, cudaMemcpyDeviceToHost) != cudaSuccess) return TP_ECUDA;
     *total = (int64_t)c + 1;   // stored as count - 1
     return TP_OK;
+}
+
+int tp_compact_stats(const tp_gbdt* m, const void* workspace, size_t workspace_bytes, int32_t n_inst, int32_t H,
+                     int32_t F, int64_t* out) {
+    if (!m || !out || n_inst < 0 || !H_ok(H) || F < 1 || F > tp::kMaxF) return TP_EINVAL;
+    out[0] = out[1] = out[2] = 0;
+    if (n_inst == 0) return TP_OK;
+    const int64_t cells = tp::model_cells(m->m);
+    if (!workspace || cells > tp::kMaxCells || workspace_bytes < tp::runs_workspace_bytes(cells, n_inst, H, F))
+        return TP_EINVAL;
+    tp::K2Params p;
+    std::memset(&p, 0, sizeof(p));
+    tp::runs_workspace_carve(const_cast<void*>(workspace), cells, n_inst, H, F, p);
+    int32_t* h = new (std::nothrow) int32_t[2 * (size_t)n_inst];
+    if (!h) return TP_ENOMEM;
+    int32_t c = -1;
+    const bool ok = cudaMemcpy(h, p.run_h, (size_t)n_inst * 4, cudaMemcpyDeviceToHost) == cudaSuccess &&
+                    cudaMemcpy(h + n_inst, p.end_n, (size_t)n_inst * 4, cudaMemcpyDeviceToHost) == cudaSuccess &&
+                    cudaMemcpy(&c, p.cell_count, 4, cudaMemcpyDeviceToHost) == cudaSuccess;
+    for (int32_t i = 0; ok && i < n_inst; ++i) {
+        out[0] += h[i];
+        out[1] += h[n_inst + i];
+    }
+    out[2] = (int64_t)c + 1;
+    delete[] h;
+    return ok ? TP_OK : TP_ECUDA;
 }
 
 int tp_select_freq(const tp_inst* inst, int32_t n_inst, const tp_req* req, int32_t n_req, const double* t_dead,
@@ -386,6 +427,9 @@ int tp_ctx_enable_admission(tp_ctx* c, int32_t q_max) {
 int tp_decide_admit(tp_ctx* c, const tp_gbdt* m, const tp_inst* inst, int32_t n_inst, const tp_req* req,
                     int32_t n_req, const double* t_dead, const float* freq_mhz, int32_t F, float tbt_slo,
                     int32_t* level, uint32_t* status, int32_t* n_adm_out, uint32_t* adm_lost_out, void* stream) {
+    if (!c) return TP_EINVAL;
+    DeviceGuard dg(c->device);
+    if (!dg.ok) return TP_ECUDA;
     if (!c || !m || !c->qc || m != c->cells_model || n_inst < 0 || n_inst > c->n_inst_max || F > c->F_max ||
         !freq_ok(freq_mhz, F) || !tbt_ok(tbt_slo))
         return TP_EINVAL;
@@ -492,6 +536,9 @@ int tp_ctx_buffers(tp_ctx* c, int32_t** B, int32_t** KV, int32_t** n, int32_t** 
 int tp_decide(tp_ctx* c, const tp_gbdt* m, const tp_inst* inst, int32_t n_inst, const tp_req* req, int32_t n_req,
               const double* t_dead, const float* freq_mhz, int32_t F, float tbt_slo, int32_t* level,
               uint32_t* status, void* stream) {
+    if (!c) return TP_EINVAL;
+    DeviceGuard dg(c->device);
+    if (!dg.ok) return TP_ECUDA;
     if (!c || !m || n_inst < 0 || n_inst > c->n_inst_max || F > c->F_max || !freq_ok(freq_mhz, F) ||
         !tbt_ok(tbt_slo))
         return TP_EINVAL;
@@ -528,6 +575,9 @@ int tp_decide(tp_ctx* c, const tp_gbdt* m, const tp_inst* inst, int32_t n_inst, 
 int tp_decide_host(tp_ctx* c, const tp_gbdt* m, const tp_inst* h_inst, int32_t n_inst, const tp_req* h_req,
                    int32_t n_req, const double* h_t_dead, const float* freq_mhz, int32_t F, float tbt_slo,
                    int32_t* h_level, uint32_t* h_status, void* stream) {
+    if (!c) return TP_EINVAL;
+    DeviceGuard dg(c->device);
+    if (!dg.ok) return TP_ECUDA;
     if (!c || !m || n_inst < 0 || n_inst > c->n_inst_max || n_req < 0 || n_req > c->n_req_max) return TP_EINVAL;
     if (n_inst > 0 && (!h_inst || !h_level || !h_status || (n_req > 0 && (!h_req || !h_t_dead)))) return TP_EINVAL;
     if (!freq_ok(freq_mhz, F) || F > c->F_max || !tbt_ok(tbt_slo)) return TP_EINVAL;

@@ -1,13 +1,12 @@
 // K1c -- the compact path's first kernel: KV usage & batch-size projection (PAPER §4.2, Eq. 1-2,
 // P:432-469) with the FIFO admission gate (check 1 + batch cap, §4.3.2, one request at a
 // time P:755), fused with what the two later kernels need from it:
-//   * run compression + cell claims (what k2_runs does from the B/KV rows): M depends on m only
-//     through the cell (rank_tp, rank_B[m], rank_KV[m]) of the grid row (reading A-7), so
-//     consecutive iterations in one cell form a run; first-seen cells are appended to the cell list
-//     K2 evaluates;
-//   * the deadline list of Eq. 4: Dmin[l] = min over the scheduled requests ending at
-//     l of ceil(fl64(t_dead - t_cur) * 2^40) (reading A-12), compacted to the end positions that
-//     carry one, ascending.
+//   * pieces + cell claims: M depends on m only through the cell (rank_tp, rank_B[m], rank_KV[m])
+//     of the grid row (reading A-7), so m = 1..n is cut into pieces of one cell that also
+//     end at every request's last iteration (piece_rules below); first-seen cells are appended to
+//     the cell list K2 evaluates;
+//   * Eq. 4 per piece: Dmin of the piece's tail = min over the scheduled requests ending
+//     there of ceil(fl64(t_dead - t_cur) * 2^40) (reading A-12) -- K3c checks T_R there.
 // The B/KV curves never leave the SM unless the caller asks for them (bkv_rows).
 //
 // One to four WARPS per instance (the CTA-per-instance K1 spends most of its issue slots on
@@ -127,6 +126,63 @@ struct Group {
         return r;
     }
 };
+
+// First claimant of a cell appends it to the cell list K2 evaluates (cell_count holds count - 1)
+// and zeroes its clamp mask.
+__device__ __forceinline__ void claim_cell(const K1cParams& p, uint32_t k) {
+    if (__ldcg(p.cell_tab + k) == -1 && atomicCAS(p.cell_tab + k, -1, -2) == -1) {
+        const int idx = atomicAdd(p.cell_count, 1) + 1;
+        p.cell_list[idx] = k;
+        p.cell_clamp[idx] = 0u;
+        p.cell_tab[k] = idx;
+    }
+}
+
+// piece_rules.  K3c accumulates T_R (Eq. 3) piece by piece and checks Eq. 4 at
+// piece tails, so K1c cuts m = 1..n into PIECES: maximal runs of consecutive iterations in one cell
+// (rank_tp, rank_B[m], rank_KV[m]) -- the model's value is constant on a piece (reading A-7)
+// -- that also end at every end position l (the last iteration of a scheduled request).  No
+// admissions happen past m = 1, so B only drops, at l + 1, for the requests ending at l: m - 1 is an
+// end position iff B[m] < B[m - 1], and the heads are m = 1 plus every m with key(m) != key(m - 1) or
+// B[m] < B[m - 1].  Per instance: run_h = #pieces, run_m / run_key = head m / cell id of each piece,
+// end_d = Dmin of the piece's tail (piece_deadlines), end_n = #end positions (statistics).
+
+// Eq. 4 per piece: end_d[k] = min over the scheduled requests whose last iteration l is piece k's
+// tail of ceil(fl64(t_dead - t_cur) * 2^40) (reading A-12), kNoDeadline where none ends.  The piece
+// of l comes from the chunk meta (heads before l's 32-iteration chunk + heads in it up to l, - 1).
+// The minima collect in shared memory behind the meta when they fit in `words` 32-bit words from
+// `base`, else straight in global memory.
+template <int WPI>
+__device__ __forceinline__ void piece_deadlines(const K1cParams& p, Group<WPI>& grp, int i, const tp_inst& in,
+                                                int64_t rb, int n_sched, int nn, int h, const int2* meta,
+                                                long long* base, int words, int gl) {
+    constexpr int GL = 32 * WPI;
+    if (nn == 0) return;
+    const size_t row = (size_t)i * p.H;
+    const int C = (nn + 31) >> 5;
+    long long* D = base + C;                         // behind meta[C] (8 bytes each)
+    const bool sm = 2 * (C + h) <= words;
+    grp.sync();                                      // meta written by the whole group
+    for (int k = gl; k < h; k += GL) {
+        if (sm) D[k] = kNoDeadline;
+        else p.end_d[row + k] = kNoDeadline;
+    }
+    grp.sync();
+    for (int e = gl; e < n_sched; e += GL) {
+        const int64_t j = rb + e;
+        const int4 r = __ldg(&p.req[j]);
+        const int l = r.z - r.x;                     // 1 <= l <= nn (validated; n = max l)
+        const int2 mt = meta[(l - 1) >> 5];
+        const int k = mt.y + __popc((unsigned)mt.x & (0xffffffffu >> (31 - ((l - 1) & 31)))) - 1;
+        const long long d = slack_ticks(__ldg(&p.t_dead[j]) - in.t_cur);
+        if (sm) atomicMin(&D[k], d);
+        else atomicMin(&p.end_d[row + k], d);
+    }
+    if (sm) {
+        grp.sync();
+        for (int k = gl; k < h; k += GL) p.end_d[row + k] = D[k];
+    }
+}
 
 // One instance, by the WPI warps of group grp (histograms sB / sKV in the group's shared memory).
 template <int WPI>
@@ -364,136 +420,97 @@ __device__ __forceinline__ void k1_body(const K1cParams& p, const int i, Group<W
     }
     const int nn = (st & p.skip) ? 0 : n;    // iterations K2 / K3 evaluate
     const unsigned ltm = (1u << lane) - 1u;
+    const size_t row = (size_t)i * H;
 
-    // ---- runs of equal cells over m = 1..nn, first-seen cells claimed ----
-    if (p.run_h) {
-        const int nB = p.cut_off[2] - p.cut_off[1], nKV = p.cut_off[3] - p.cut_off[2];
-        const int lB = p.rtab_len[0], lKV = p.rtab_len[1];
-        const uint16_t* tB = p.rtab + p.rtab_off[0];
-        const uint16_t* tKV = p.rtab + p.rtab_off[1];
-        const uint32_t rtp = rank_of(p.cuts + p.cut_off[0], p.cut_off[1] - p.cut_off[0], (float)in.tp);
-        const uint32_t nk1 = (uint32_t)nKV + 1;
-        const uint32_t cell_base = rtp * (uint32_t)(nB + 1) * nk1;
-        auto key_at = [&](int pidx) {
-            const int b = sB[pidx], kv = sKV[pidx];
+    // ---- pieces over m = 1..nn (see piece_rules below), first-seen cells claimed ----
+    // Group-strided over m (warp gw takes the 32 iterations m0 + 32 gw + lane, i.e. 32-chunk
+    // c = (m0 - 1) / 32 + gw): key, B, head flag, ballot; records written straight from the
+    // compaction; across warps the first / last (key, B) and head counts go through the exchange,
+    // whose barrier also orders every histogram read of the step before the meta writes.
+    const int nB = p.cut_off[2] - p.cut_off[1], nKV = p.cut_off[3] - p.cut_off[2];
+    const int lB = p.rtab_len[0], lKV = p.rtab_len[1];
+    const uint16_t* tB = p.rtab + p.rtab_off[0];
+    const uint16_t* tKV = p.rtab + p.rtab_off[1];
+    const uint32_t rtp = rank_of(p.cuts + p.cut_off[0], p.cut_off[1] - p.cut_off[0], (float)in.tp);
+    const uint32_t nk1 = (uint32_t)nKV + 1;
+    const uint32_t cell_base = rtp * (uint32_t)(nB + 1) * nk1;
+    int2* meta = reinterpret_cast<int2*>(sB);        // [chunk] (head mask, heads before the chunk)
+    int h = 0, ends = 0;
+    uint32_t kcarry = 0xffffffffu;                   // key / B of m0 - 1 (m = 1 always starts a piece)
+    int bcarry = 0;
+    for (int m0 = 1; m0 <= nn; m0 += GL) {
+        const int m = m0 + gl;
+        uint32_t k = 0;
+        int b = 0;
+        if (m <= nn) {
+            const int pi = ph(m);
+            b = sB[pi];
+            const int kv = sKV[pi];
             const uint32_t rbk = b < lB ? __ldg(tB + b) : rank_of(p.cuts + p.cut_off[1], nB, (float)b);
             const uint32_t rkv = kv < lKV ? __ldg(tKV + kv) : rank_of(p.cuts + p.cut_off[2], nKV, (float)kv);
-            return cell_base + rbk * nk1 + rkv;
-        };
-        // Group-strided over m (warp gw takes the 32 iterations m0 + 32 gw + lane): key, head flag
-        // (key != key of m - 1), ballot compaction; the heads (m, key) are staged in place at plain
-        // indices j < #heads so far, which never reach a position a later step still reads
-        // (ph(m) >= m - 1).  Across warps: first / last keys and head counts through the exchange
-        // (whose barrier also orders every read of this step before the staging writes).
-        int h = 0;
-        uint32_t carry = 0xffffffffu;      // key of m0 - 1 (m = 1 always starts a run)
-        for (int m0 = 1; m0 <= nn; m0 += GL) {
-            const int m = m0 + gl;
-            const uint32_t k = m <= nn ? key_at(ph(m)) : 0u;
-            uint32_t pk = __shfl_up_sync(kFull, k, 1);
-            const uint32_t kfirst = __shfl_sync(kFull, k, 0), klast = __shfl_sync(kFull, k, 31);
-            const bool head_rest = lane > 0 && m <= nn && k != pk;       // lanes 1..31
-            const unsigned mrest = __ballot_sync(kFull, head_rest);
-            int before = 0;                 // heads of this step in earlier warps
-            bool head0;                     // this warp's lane-0 head flag
-            if (WPI == 1) {
-                head0 = m0 <= nn && kfirst != carry;
-                carry = klast;
-            } else {
-                const long long* x = grp.exchange(kfirst, klast, __popc(mrest), 0);
-                uint32_t prevlast = carry;
-                head0 = false;
-#pragma unroll
-                for (int v = 0; v < WPI; ++v) {
-                    const bool hv = m0 + 32 * v <= nn && (uint32_t)x[v * 4] != prevlast;
-                    if (v < grp.gw) before += (int)x[v * 4 + 2] + hv;
-                    if (v == grp.gw) head0 = hv;
-                    prevlast = (uint32_t)x[v * 4 + 1];
-                }
-                int tot = 0;
-#pragma unroll
-                for (int v = 0; v < WPI; ++v) {
-                    const uint32_t pl = v == 0 ? carry : (uint32_t)x[(v - 1) * 4 + 1];
-                    tot += (int)x[v * 4 + 2] + (m0 + 32 * v <= nn && (uint32_t)x[v * 4] != pl);
-                }
-                carry = prevlast;
-                const unsigned mask = mrest | (head0 ? 1u : 0u);
-                if (lane == 0 ? head0 : head_rest) {
-                    const int pos = h + before + __popc(mask & ltm);
-                    sKV[pos] = m;
-                    sB[pos] = (int)k;
-                }
-                h += tot;
-                continue;
-            }
-            __syncwarp();                  // every lane has read its B / KV before the staging writes
-            const unsigned mask = mrest | (head0 ? 1u : 0u);
-            if (lane == 0 ? head0 : head_rest) {
-                const int pos = h + __popc(mask & ltm);
-                sKV[pos] = m;
-                sB[pos] = (int)k;
-            }
-            h += __popc(mask);
+            k = cell_base + rbk * nk1 + rkv;
         }
-        grp.sync();
-        // coalesced run records; claims lane-parallel (first claimant appends the cell)
-        const size_t row = (size_t)i * H;
-        for (int k = gl; k < h; k += GL) {
-            const int m = sKV[k];
-            const uint32_t key = (uint32_t)sB[k];
-            p.run_m[row + k] = m;
-            p.run_key[row + k] = key;
-            if (__ldcg(p.cell_tab + key) == -1 && atomicCAS(p.cell_tab + key, -1, -2) == -1) {
-                const int idx = atomicAdd(p.cell_count, 1) + 1;   // cell_count holds count - 1
-                p.cell_list[idx] = key;
-                p.cell_clamp[idx] = 0u;
-                p.cell_tab[key] = idx;
+        const uint32_t pk = __shfl_up_sync(kFull, k, 1);
+        const int pb = __shfl_up_sync(kFull, b, 1);
+        const uint32_t kfirst = __shfl_sync(kFull, k, 0), klast = __shfl_sync(kFull, k, 31);
+        const int bfirst = __shfl_sync(kFull, b, 0), blast = __shfl_sync(kFull, b, 31);
+        const bool live = m <= nn;
+        const bool head_rest = lane > 0 && live && (k != pk || b < pb);     // lanes 1..31
+        const unsigned mrest = __ballot_sync(kFull, head_rest);
+        const unsigned erest = __ballot_sync(kFull, lane > 0 && live && b < pb);   // m - 1 is an end
+        int before = 0, tot = 0, etot = 0;           // heads / ends of this step in earlier warps, all
+        bool head0, end0;                            // this warp's lane-0 flags (vs the previous chunk)
+        if (WPI == 1) {
+            head0 = m0 <= nn && (kfirst != kcarry || bfirst < bcarry);
+            end0 = m0 <= nn && bfirst < bcarry;
+            tot = __popc(mrest) + head0;
+            etot = __popc(erest) + end0;
+            kcarry = klast;
+            bcarry = blast;
+        } else {
+            const long long* x = grp.exchange((long long)kfirst | ((long long)klast << 32),
+                                              (long long)(unsigned)bfirst | ((long long)blast << 32),
+                                              __popc(mrest), __popc(erest));
+            uint32_t pkl = kcarry;
+            int pbl = bcarry;
+            head0 = end0 = false;
+#pragma unroll
+            for (int v = 0; v < WPI; ++v) {
+                const uint32_t kf = (uint32_t)x[v * 4], kl = (uint32_t)(x[v * 4] >> 32);
+                const int bf = (int)(uint32_t)x[v * 4 + 1], bl = (int)(x[v * 4 + 1] >> 32);
+                const bool lv = m0 + 32 * v <= nn;
+                const bool ev = lv && bf < pbl, hv = lv && (kf != pkl || bf < pbl);
+                if (v < grp.gw) before += (int)x[v * 4 + 2] + hv;
+                if (v == grp.gw) {
+                    head0 = hv;
+                    end0 = ev;
+                }
+                tot += (int)x[v * 4 + 2] + hv;
+                etot += (int)x[v * 4 + 3] + ev;
+                pkl = kl;
+                pbl = bl;
             }
+            kcarry = pkl;
+            bcarry = pbl;
         }
-        if (gl == 0) p.run_h[i] = h;
+        const unsigned mask = mrest | (head0 ? 1u : 0u);
+        if (lane == 0 ? head0 : head_rest) {
+            const int pos = h + before + __popc(mask & ltm);
+            p.run_m[row + pos] = m;
+            p.run_key[row + pos] = k;
+            claim_cell(p, k);
+        }
+        if (lane == 0 && m <= nn) meta[(m - 1) >> 5] = make_int2((int)mask, h + before);
+        h += tot;
+        ends += etot;
     }
-
-    // ---- Eq. 4 deadline list: Dmin over end positions (the histogram space is reused) ----
-    if (p.end_n) {
-        grp.sync();
-        long long* dmin = reinterpret_cast<long long*>(sB);     // [0, nn], 8 (H + 1) <= 8 arr bytes
-        for (int m = gl; m <= nn; m += GL) dmin[m] = kNoDeadline;
-        grp.sync();
-        if (nn > 0) {
-            for (int e = gl; e < nr + n_adm; e += GL) {
-                const int64_t j = rb + e;
-                const int4 r = __ldg(&p.req[j]);
-                atomicMin(&dmin[r.z - r.x], slack_ticks(__ldg(&p.t_dead[j]) - in.t_cur));
-            }
-        }
-        grp.sync();
-        int ne = 0;
-        const size_t row = (size_t)i * H;
-        for (int m0 = 1; m0 <= nn; m0 += GL) {
-            const int m = m0 + gl;
-            const long long d = m <= nn ? dmin[m] : kNoDeadline;
-            const unsigned mask = __ballot_sync(kFull, d != kNoDeadline);
-            int before = 0, tot = __popc(mask);
-            if (WPI > 1) {
-                const long long* x = grp.exchange(__popc(mask), 0, 0, 0);
-                tot = 0;
-#pragma unroll
-                for (int v = 0; v < WPI; ++v) {
-                    if (v < grp.gw) before += (int)x[v * 4];
-                    tot += (int)x[v * 4];
-                }
-            }
-            if (d != kNoDeadline) {
-                const int pos = ne + before + __popc(mask & ltm);
-                p.end_l[row + pos] = m;
-                p.end_d[row + pos] = d;
-            }
-            ne += tot;
-        }
-        if (gl == 0) p.end_n[i] = ne;
+    if (gl == 0) {
+        p.run_h[i] = h;
+        p.end_n[i] = nn > 0 ? ends + 1 : 0;          // + m = nn, always an end
     }
+    piece_deadlines<WPI>(p, grp, i, in, rb, nr + n_adm, nn, h, meta, reinterpret_cast<long long*>(sB),
+                         2 * p.arr, gl);
 }
-
 
 // ---------------------------------------------------------------------------------------------
 // K1c, packed (large batches, one warp per instance): the two histograms in ONE int32 array,
@@ -683,79 +700,55 @@ k1_packed(const __grid_constant__ K1cParams p) {
     const unsigned ltm = (1u << lane) - 1u;
     const size_t row = (size_t)i * H;
 
-    // ---- runs of equal cells (records straight from the ballot compaction), claims ----
-    if (p.run_h) {
-        const int nB = p.cut_off[2] - p.cut_off[1], nKV = p.cut_off[3] - p.cut_off[2];
-        const int lB = p.rtab_len[0], lKV = p.rtab_len[1];
-        const uint16_t* tB = p.rtab + p.rtab_off[0];
-        const uint16_t* tKV = p.rtab + p.rtab_off[1];
-        const uint32_t rtp = rank_of(p.cuts + p.cut_off[0], p.cut_off[1] - p.cut_off[0], (float)in.tp);
-        const uint32_t nk1 = (uint32_t)nKV + 1;
-        const uint32_t cell_base = rtp * (uint32_t)(nB + 1) * nk1;
-        int h = 0;
-        uint32_t carry = 0xffffffffu;
-        for (int m0 = 1; m0 <= nn; m0 += 32) {
-            const int m = m0 + lane;
-            uint32_t k = 0;
-            if (m <= nn) {
-                const int v = sv[ph(m)];
-                const int b = v >> 16, kv = v & 0xFFFF;
-                const uint32_t rbk = b < lB ? __ldg(tB + b) : rank_of(p.cuts + p.cut_off[1], nB, (float)b);
-                const uint32_t rkv = kv < lKV ? __ldg(tKV + kv) : rank_of(p.cuts + p.cut_off[2], nKV, (float)kv);
-                k = cell_base + rbk * nk1 + rkv;
-            }
-            uint32_t pk = __shfl_up_sync(kFull, k, 1);
-            if (lane == 0) pk = carry;
-            carry = __shfl_sync(kFull, k, 31);
-            const bool head = m <= nn && k != pk;
-            const unsigned mask = __ballot_sync(kFull, head);
-            if (head) {
-                const int pos = h + __popc(mask & ltm);
-                p.run_m[row + pos] = m;
-                p.run_key[row + pos] = k;
-                if (__ldcg(p.cell_tab + k) == -1 && atomicCAS(p.cell_tab + k, -1, -2) == -1) {
-                    const int idx = atomicAdd(p.cell_count, 1) + 1;   // cell_count holds count - 1
-                    p.cell_list[idx] = k;
-                    p.cell_clamp[idx] = 0u;
-                    p.cell_tab[k] = idx;
-                }
-            }
-            h += __popc(mask);
+    // ---- pieces (piece_rules), records straight from the ballot compaction, claims ----
+    const int lB1 = p.rtab_len[0] - 1, lKV1 = p.rtab_len[1] - 1;   // tables end past the last cut
+    const uint16_t* tB = p.rtab + p.rtab_off[0];
+    const uint16_t* tKV = p.rtab + p.rtab_off[1];
+    const int nKV = p.cut_off[3] - p.cut_off[2];
+    const uint32_t rtp = rank_of(p.cuts + p.cut_off[0], p.cut_off[1] - p.cut_off[0], (float)in.tp);
+    const uint32_t nk1 = (uint32_t)nKV + 1;
+    const uint32_t cell_base = rtp * (uint32_t)(p.cut_off[2] - p.cut_off[1] + 1) * nk1;
+    int2* meta = reinterpret_cast<int2*>(sv);       // [chunk] (head mask, heads before the chunk)
+    int h = 0, ends = 0;
+    uint32_t kcarry = 0xffffffffu;
+    int bcarry = 0;
+    for (int m0 = 1; m0 <= nn; m0 += 32) {
+        const int m = m0 + lane;
+        uint32_t k = 0;
+        int b = 0;
+        if (m <= nn) {
+            const int v = sv[ph(m)];
+            b = v >> 16;
+            // b < 2^15, kv < 2^16 here (the packed check): the clamped table lookups are exact
+            k = cell_base + (uint32_t)__ldg(tB + min(b, lB1)) * nk1 + __ldg(tKV + min(v & 0xFFFF, lKV1));
         }
-        if (lane == 0) p.run_h[i] = h;
-    }
-
-    // ---- Eq. 4 deadline list, in windows of the histogram space (arr / 2 int64 entries) ----
-    if (p.end_n) {
-        long long* dmin = reinterpret_cast<long long*>(sv);
-        const int wm = p.arr / 2;
-        int ne = 0;
-        for (int wb = 1; wb <= nn; wb += wm) {
-            const int we = min(nn, wb + wm - 1);
-            __syncwarp();
-            for (int m = wb + lane; m <= we; m += 32) dmin[m - wb] = kNoDeadline;
-            __syncwarp();
-            for (int e = lane; e < nr + n_adm; e += 32) {
-                const int64_t j = rb + e;
-                const int4 r = __ldg(&p.req[j]);
-                const int l = r.z - r.x;
-                if (l >= wb && l <= we) atomicMin(&dmin[l - wb], slack_ticks(__ldg(&p.t_dead[j]) - in.t_cur));
-            }
-            __syncwarp();
-            for (int m0 = wb; m0 <= we; m0 += 32) {
-                const int m = m0 + lane;
-                const long long d = m <= we ? dmin[m - wb] : kNoDeadline;
-                const unsigned mask = __ballot_sync(kFull, d != kNoDeadline);
-                if (d != kNoDeadline) {
-                    const int pos = ne + __popc(mask & ltm);
-                    p.end_l[row + pos] = m;
-                    p.end_d[row + pos] = d;
-                }
-                ne += __popc(mask);
-            }
+        uint32_t pk = __shfl_up_sync(kFull, k, 1);
+        int pb = __shfl_up_sync(kFull, b, 1);
+        if (lane == 0) {
+            pk = kcarry;
+            pb = bcarry;
         }
-        if (lane == 0) p.end_n[i] = ne;
+        kcarry = __shfl_sync(kFull, k, 31);
+        bcarry = __shfl_sync(kFull, b, 31);
+        const bool live = m <= nn, endp = live && b < pb;   // m - 1 is an end position
+        const bool head = live && (k != pk || endp);
+        const unsigned mask = __ballot_sync(kFull, head);
+        ends += __popc(__ballot_sync(kFull, endp));
+        if (head) {
+            const int pos = h + __popc(mask & ltm);
+            p.run_m[row + pos] = m;
+            p.run_key[row + pos] = k;
+            claim_cell(p, k);
+        }
+        if (lane == 0) meta[(m0 - 1) >> 5] = make_int2((int)mask, h);
+        h += __popc(mask);
     }
+    if (lane == 0) {
+        p.run_h[i] = h;
+        p.end_n[i] = nn > 0 ? ends + 1 : 0;
+    }
+    Group<1> g1;
+    piece_deadlines<1>(p, g1, i, in, rb, nr + n_adm, nn, h, meta, reinterpret_cast<long long*>(sv), p.arr, lane);
 }
 
 template <int WPI, bool FLAGGED = false>   // FLAGGED: the instances k1_packed handed over

@@ -76,9 +76,8 @@ void fill(const std::vector<Node>& t, int at, uint32_t idx, int depth, int D,
 
 }  // namespace
 
-extern "C" int tp_gbdt_load(const void* host_blob, size_t nbytes, int device, tp_gbdt** out) {
-    if (!host_blob || !out) return TP_EINVAL;
-    *out = nullptr;
+namespace {
+int load_impl(const void* host_blob, size_t nbytes, int device, tp_gbdt** out) {
     const unsigned char* p = (const unsigned char*)host_blob;
     if (nbytes < 24 || std::memcmp(p, "TPGB", 4) != 0) return TP_EFORMAT;
     if (rd32(p + 4) != 1 || rd32(p + 8) != 4) return TP_EFORMAT;
@@ -118,6 +117,7 @@ extern "C" int tp_gbdt_load(const void* host_blob, size_t nbytes, int device, tp
     }
 
     const size_t words_per_tree = std::max<size_t>(4, (size_t)2 << D);   // >= 16 B: TMA size/alignment unit
+    if ((uint64_t)nt * words_per_tree > tp::kMaxModelWords) return TP_EFORMAT;  // > 1 GiB of node words
     std::vector<uint32_t> words(std::max<size_t>(1, nt * words_per_tree), 0u);
     for (uint32_t t = 0; t < nt; ++t) fill(trees[t], 0, 1u, 0, D, cuts, &words[t * words_per_tree]);
     std::vector<float> allc;
@@ -135,12 +135,15 @@ extern "C" int tp_gbdt_load(const void* host_blob, size_t nbytes, int device, tp
     }
     m.cut_off[4] = (int32_t)allc.size();
     allc.push_back(0.f);   // never empty
-    // rank tables for integer batch / KV values: rank(x) = #cuts <= x for x in [0, len)
+    // rank tables for integer batch / KV values: rank(x) = #cuts <= x for x in [0, len).  The table
+    // runs one past the largest cut (len = floor(max cut) + 2, at least 1), so its last entry is
+    // the rank of every larger x too: rank(x) = rtab[min(x, len - 1)] for every x >= 0 unless the
+    // table is capped at kRankTabMax entries (then exact for x < kRankTabMax).
     std::vector<uint16_t> rtab;
     for (int w = 0; w < 2; ++w) {
         const std::vector<float>& c = cuts[1 + w];
-        int64_t len = 0;
-        if (!c.empty() && c.back() >= 0.f) len = std::min<int64_t>((int64_t)std::floor(c.back()) + 1, tp::kRankTabMax);
+        int64_t len = 1;
+        if (!c.empty() && c.back() >= 0.f) len = std::min<int64_t>((int64_t)std::floor(c.back()) + 2, tp::kRankTabMax);
         m.rtab_off[w] = (int32_t)rtab.size();
         m.rtab_len[w] = (int32_t)len;
         for (int64_t x = 0; x < len; ++x)
@@ -171,6 +174,21 @@ extern "C" int tp_gbdt_load(const void* host_blob, size_t nbytes, int device, tp
     }
     *out = h;
     return TP_OK;
+}
+}  // namespace
+
+// The parse allocates host vectors sized from the blob: an allocation failure must not cross
+// the C ABI as an exception (it would terminate the caller), so it becomes TP_ENOMEM.
+extern "C" int tp_gbdt_load(const void* host_blob, size_t nbytes, int device, tp_gbdt** out) {
+    if (!host_blob || !out) return TP_EINVAL;
+    *out = nullptr;
+    try {
+        return load_impl(host_blob, nbytes, device, out);
+    } catch (const std::bad_alloc&) {
+        return TP_ENOMEM;
+    } catch (...) {
+        return TP_EFORMAT;
+    }
 }
 
 extern "C" int tp_gbdt_free(tp_gbdt* h) {

@@ -92,7 +92,9 @@ k_replay_advance(const __grid_constant__ AdvParams p) {
     const int64_t base = (int64_t)i * p.cap;
     const uint32_t st = p.status[i];
     const int nr = in.n_run, nq = in.n_queue;
-    const bool bad = (st & kSkip) != 0;
+    // tp_decide read this instance's requests at req_begin; the advance addresses slot i * cap:
+    // the two must agree (include/tp.h), else the state is left as is (treated as bad input)
+    const bool bad = (st & kSkip) != 0 || in.req_begin != base;
     const int n = bad ? 0 : p.n[i];
     const int nadm = bad ? 0 : p.n_adm[i];
     if (bad) {      // invalid instance data: state left as is

@@ -14,6 +14,7 @@ constexpr int kMaxF = 32;
 constexpr int kMaxH = 16384;
 constexpr int kMaxHRunsSelect = 8192;      // tp_select_freq_ws keeps ~28 B per iteration in smem
 constexpr int kMaxDepth = 12;
+constexpr uint64_t kMaxModelWords = 1ull << 28;   // node words of a loaded ensemble (1 GiB)
 constexpr int kMaxCuts = 32767;            // ranks must fit 15 bits (K2 word encoding)
 constexpr int64_t kFeatLimit = 1LL << 24;  // integer features exact in fp32
 constexpr int kRankTabMax = 1 << 16;       // rank table entries per integer feature
@@ -26,8 +27,12 @@ struct FastDiv {
     uint32_t m, s1, s2;
     FastDiv() = default;
     __host__ __device__ explicit FastDiv(uint32_t d) {
+#ifdef __CUDA_ARCH__
+        const uint32_t l = d > 1 ? 32 - __clz(d - 1) : 0;   // ceil(log2 d)
+#else
         uint32_t l = 0;
         while (l < 32 && (1ull << l) < d) ++l;
+#endif
         m = (uint32_t)((((1ull << l) - d) << 32) / d + 1);
         s1 = l < 1 ? l : 1;
         s2 = l > 1 ? l - 1 : 0;

@@ -22,7 +22,7 @@ def _dev(a, dev, dtype=None):
 class Replay:
     STATS = ("completed", "met_deadline", "dropped_arrivals", "engine_iterations", "admissions")
 
-    def __init__(self, data: dict, model: tp.Gbdt, device="cuda:0", k2_mode=tp.K2_RUNS, admission: int = 0,
+    def __init__(self, data: dict, model: tp.Gbdt, device="cuda:0", k2_mode=tp.K2_COMPACT, admission: int = 0,
                  search: str = "exhaustive"):
         """admission = q_max > 0: each round runs the paper's full admission control (tp_decide_admit)
         on at most q_max queued requests per instance before the throttle."""

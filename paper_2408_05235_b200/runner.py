@@ -119,3 +119,50 @@ class Round:
         if self.tr is not None:
             out["tr"] = get(self.tr)
         return out
+
+
+class BenchStep:
+    """The exact step bench.py times (and the at-scale parity tests and smoke() check): the
+    compact path K1c -> K2 cell phases -> K3c with B / KV kept on chip (no B / KV rows written),
+    programmatic dependent launch between the kernels, the three launches (+ the cell-table reset)
+    captured once as a CUDA graph and replayed every step.  ``level`` / ``status`` may be views
+    into a caller buffer (bench.py writes them straight into the decision gather's send rows)."""
+
+    def __init__(self, inputs: dict, device, model, search="exhaustive", graph=True, level=None, status=None):
+        self.device = torch.device(device)
+        self.rnd = Round(inputs, self.device, k2_mode="compact", model=model, search=search)
+        self.rnd.bkv = False
+        if level is not None:
+            self.rnd.level, self.rnd.status = level, status
+        self.model = model
+        self.graph = None
+        if graph:
+            gs = torch.cuda.Stream(self.device)
+            with torch.cuda.stream(gs):
+                self.kernels(gs)      # warm-up on the capture stream (attributes, lazy module loading)
+            torch.cuda.synchronize(self.device)
+            self.graph = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(self.graph, stream=gs):
+                self.kernels(gs)
+            torch.cuda.synchronize(self.device)
+
+    def kernels(self, stream):
+        self.rnd.project(stream)
+        self.rnd.predict(self.model, stream)
+        self.rnd.select(stream)
+
+    def run(self, stream=None):
+        """One step on ``stream`` (the captured graph when there is one)."""
+        if self.graph is not None:
+            self.graph.replay()
+        else:
+            self.kernels(stream)
+
+    def decisions(self, idx=None) -> dict:
+        """level / status / n / n_adm on the host (synchronises)."""
+        torch.cuda.synchronize(self.device)
+        r = self.rnd
+        sel = slice(0, r.I) if idx is None else torch.as_tensor(np.asarray(idx), device=self.device,
+                                                                  dtype=torch.long)
+        get = lambda t: t[:r.I][sel].cpu().numpy()   # noqa: E731
+        return dict(level=get(r.level), status=get(r.status).view(np.uint32), n=get(r.n), n_adm=get(r.n_adm))

@@ -25,7 +25,7 @@ EXPORTS = ["tp_gbdt_load", "tp_gbdt_free", "tp_gbdt_get_info", "tp_project", "tp
            "tp_predict_ips_workspace_size", "tp_predict_ips_runs", "tp_runs_total", "tp_cells_total", "tp_select_freq", "tp_select_freq_ws", "tp_ctx_create", "tp_ctx_free",
            "tp_decide", "tp_decide_host", "tp_replay_advance", "tp_ctx_enable_admission", "tp_decide_admit", "tp_ctx_set_k2_mode", "tp_ctx_buffers",
            "tp_select_freq_binary", "tp_ctx_set_search", "tp_project_compact", "tp_predict_cells",
-           "tp_select_freq_compact", "tp_strerror", "tp_abi_version"]
+           "tp_select_freq_compact", "tp_compact_stats", "tp_strerror", "tp_abi_version"]
 K2_DIRECT, K2_RUNS, K2_COMPACT = 0, 1, 2
 SEARCH_EXHAUSTIVE, SEARCH_BINARY = 0, 1
 
@@ -60,6 +60,7 @@ _L.tp_project_compact.argtypes = [_vp, _vp, ctypes.c_size_t, _vp, _i32, _vp, _i3
                                   _vp, _vp, _vp]
 _L.tp_predict_cells.argtypes = [_vp, _vp, ctypes.c_size_t, _i32, _i32, _vp, _i32, _vp]
 _L.tp_select_freq_compact.argtypes = [_vp, _vp, ctypes.c_size_t, _i32, _vp, _i32, _i32, _f32, _i32, _vp, _vp, _vp]
+_L.tp_compact_stats.argtypes = [_vp, _vp, ctypes.c_size_t, _i32, _i32, _i32, _vp]
 _L.tp_replay_advance.argtypes = [_vp, _vp, _i32, _vp, _vp, _vp, _vp, _i32, _i32] + [_vp] * 6 + [_vp, _i32] + [_vp] * 8
 _L.tp_ctx_enable_admission.argtypes = [_vp, _i32]
 _L.tp_decide_admit.argtypes = [_vp, _vp, _vp, _i32, _vp, _i32, _vp, _vp, _i32, _f32, _vp, _vp, _vp, _vp, _vp]
@@ -197,6 +198,14 @@ def cells_total(workspace, model, n_inst, H, F) -> int:
     _check(_L.tp_cells_total(model.handle, _dp(workspace), int(n_inst), int(H), int(F), ctypes.byref(t)),
            "tp_cells_total")
     return int(t.value)
+
+
+def compact_stats(model: Gbdt, workspace, n_inst, H, F) -> dict:
+    """Pieces, end positions and distinct cells of the last tp_project_compact (synchronous)."""
+    out = np.zeros(3, np.int64)
+    _check(_L.tp_compact_stats(model.handle, _dp(workspace), workspace.numel(), int(n_inst), int(H), int(F),
+                               out.ctypes.data), "tp_compact_stats")
+    return dict(pieces=int(out[0]), ends=int(out[1]), cells=int(out[2]))
 
 
 def tp_select_freq(inst, n_inst, req, n_req, t_dead, n, n_adm, ips, H, F, tbt_slo, level, status, tr_ticks=None,

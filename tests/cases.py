@@ -106,3 +106,20 @@ def random_tiny_case(rng, H=None, F=None, n_trees=None, depth=None, n_inst=6, al
             td[b + e] = inst[i]["t_cur"] + l * tau * rng.uniform(0.3, 3.0)
     tbt = np.float32(rng.choice([0.2, 0.05, 0.02, 0.01]))
     return ens, inst, req, td, H, freq, tbt
+
+
+def subset_inputs(inputs, idx):
+    """The instances ``idx`` of a round's inputs as a self-contained round (request rows copied,
+    req_begin rebased).  Input plumbing only."""
+    inst = inputs["inst"][idx].copy()
+    reqs, deads, off = [], [], 0
+    for k, i in enumerate(idx):
+        b = int(inputs["inst"][i]["req_begin"])
+        e = b + int(inputs["inst"][i]["n_run"]) + int(inputs["inst"][i]["n_queue"])
+        reqs.append(inputs["req"][b:e])
+        deads.append(inputs["t_dead"][b:e])
+        inst[k]["req_begin"] = off
+        off += e - b
+    req = np.concatenate(reqs) if reqs else np.zeros(0, W.REQ_DTYPE)
+    td = np.concatenate(deads) if deads else np.zeros(0)
+    return dict(inputs, inst=inst, req=req, t_dead=td)

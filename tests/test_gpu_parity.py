@@ -135,16 +135,7 @@ def test_c2_full(gpu, oracle_mod, mode):
     assert_parity(got, run_oracle(oracle_mod, blob, sub_in, want_tr=False), idx=sub, tr=False)
 
 
-def _subset(inputs, idx):
-    inst = inputs["inst"][idx].copy()
-    reqs, deads, off = [], [], 0
-    for k, i in enumerate(idx):
-        b = int(inputs["inst"][i]["req_begin"])
-        e = b + int(inputs["inst"][i]["n_run"]) + int(inputs["inst"][i]["n_queue"])
-        reqs.append(inputs["req"][b:e]); deads.append(inputs["t_dead"][b:e])
-        inst[k]["req_begin"] = off
-        off += e - b
-    return dict(inputs, inst=inst, req=np.concatenate(reqs), t_dead=np.concatenate(deads))
+_subset = cases.subset_inputs
 
 
 @pytest.mark.parametrize("name,stride", [("C3", 1024), ("C4", 256)])

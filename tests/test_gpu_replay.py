@@ -24,13 +24,14 @@ def gpu():
     return tp, replay
 
 
-def _check_rounds(gpu, oracle_mod, rc, ens_cfg, rounds, every=1, admission=0):
+def _check_rounds(gpu, oracle_mod, rc, ens_cfg, rounds, every=1, admission=0, k2_mode=None, threads=16):
     tp, replay = gpu
     data = W.gen_replay(rc)
     blob = W.write_blob(W.config_ensemble(ens_cfg))
     model = tp.Gbdt(blob, 0)
     om = oracle_mod.Model(blob)
-    rp = replay.Replay(data, model, admission=admission)
+    kw = {} if k2_mode is None else dict(k2_mode=getattr(tp, k2_mode))
+    rp = replay.Replay(data, model, admission=admission, **kw)
     stats = np.zeros(5, np.int64)
     checked = 0
     for k in range(rounds):
@@ -39,7 +40,7 @@ def _check_rounds(gpu, oracle_mod, rc, ens_cfg, rounds, every=1, admission=0):
             continue
         inst, req, td, arr_next = rp.state()
         dec = oracle_mod.decide(om, inst, req, td, data["H"], data["freq"], data["tbt_slo"], want_grid=False,
-                                admission=1 if admission else 0, adm_limit=admission or 32)
+                                admission=1 if admission else 0, adm_limit=admission or 32, threads=threads)
         rp.decide()
         torch.cuda.synchronize()
         assert np.array_equal(rp.level.cpu().numpy(), dec["level"]), k
@@ -64,10 +65,13 @@ def _check_rounds(gpu, oracle_mod, rc, ens_cfg, rounds, every=1, admission=0):
     return rp, checked
 
 
-def test_replay_matches_oracle_every_round(gpu, oracle_mod):
+@pytest.mark.parametrize("k2_mode", ["K2_COMPACT", "K2_RUNS"])
+def test_replay_matches_oracle_every_round(gpu, oracle_mod, k2_mode):
+    """Replay.decide runs tp_decide on the compact path by default (K1c writes only the m = 1
+    column of B / KV, which is what tp_replay_advance reads); the fused run/cell path as well."""
     rc = W.ReplayConfig(n_inst=24, n_requests=2400, span_s=2.0, slot_cap=300, seed=11)
     ens = dataclasses.replace(W.CONFIGS["C4"], n_trees=30, depth=6)
-    rp, checked = _check_rounds(gpu, oracle_mod, rc, ens, rounds=40)
+    rp, checked = _check_rounds(gpu, oracle_mod, rc, ens, rounds=40, k2_mode=k2_mode)
     assert checked == 40
     st = rp.stats_dict()
     assert st["completed"] > 0 and st["engine_iterations"] > 0
@@ -98,3 +102,16 @@ def test_replay_with_admission_control(gpu, oracle_mod):
     rp, checked = _check_rounds(gpu, oracle_mod, rc, ens, rounds=40, admission=8)
     assert checked == 40
     assert rp.stats_dict()["admissions"] > 0
+
+
+@pytest.mark.parametrize("admission", [0, 8])
+def test_replay_512_instances_sampled(gpu, oracle_mod, admission):
+    """BASELINE configs[3] shapes at 512 instances (1/8 of the 4,096-instance replay, the same
+    request rate per instance: 125,000 arrivals over the 25 s span) with the configs[3] ensemble
+    (500 trees, depth 8): the GPU replay runs every round; on every 5th round the oracle decides the
+    GPU's current state and an independent advance checks the state transition."""
+    rc = W.ReplayConfig(n_inst=512, n_requests=125_000, seed=1004)
+    rp, checked = _check_rounds(gpu, oracle_mod, rc, W.CONFIGS["C4"], rounds=11, every=5, admission=admission)
+    assert checked == 3
+    st = rp.stats_dict()
+    assert st["engine_iterations"] > 0
