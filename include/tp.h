@@ -102,7 +102,7 @@ typedef struct tp_gbdt_info {
     int32_t depth;        /* D: trees are stored complete to this depth */
     int32_t n_cuts[4];    /* distinct thresholds per feature [tp, batch, kv, freq] */
     float base_score;
-    int32_t _pad;
+    int32_t tick_shift;   /* 8: every output is in (1, 512) IPS, T' kept as 32-bit (tick / 2^8) */
     int64_t device_bytes; /* bytes of device memory held by the handle */
     int64_t node_bytes;   /* bytes of the node arrays (T * 2^(D+1) * 4) */
 } tp_gbdt_info;

@@ -276,6 +276,7 @@ static void fill_model(const tp_gbdt* m, tp::K2Params& p) {
     p.n_trees = m->m.n_trees;
     p.depth = m->m.depth;
     p.base = m->m.base;
+    p.tick_shift = m->m.tick_shift;
 }
 
 static bool compact_ws_ok(const tp_gbdt* m, size_t bytes, int32_t n_inst, int32_t H, int32_t F) {
@@ -329,6 +330,7 @@ int tp_select_freq_compact(const tp_gbdt* m, const void* workspace, size_t works
     tp::K2Params p;
     std::memset(&p, 0, sizeof(p));
     tp::runs_workspace_carve(const_cast<void*>(workspace), tp::model_cells(m->m), n_inst, H, F, p);
+    p.tick_shift = m->m.tick_shift;
     const int64_t tbt_ticks = (int64_t)((double)tbt_slo * 0x1p40);   // exact: tbt_slo >= 2^-17
     return tp::launch_select_compact(p, n_inst, n, H, F, tbt_ticks, search,
                                      TP_ST_BAD_INPUT | TP_ST_EMPTY | TP_ST_BYPASS_LOST, level, status, S(stream));

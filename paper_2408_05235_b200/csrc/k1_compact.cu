@@ -17,6 +17,7 @@
 // (S a power of two >= 4); segments are padded by P = 4 words when S/4 is even so that 8
 // consecutive lanes' 128-bit accesses fall in distinct bank quads.
 #include <algorithm>
+#include <cstdio>
 #include <cstdlib>
 
 #include "tp_internal.cuh"
@@ -72,8 +73,9 @@ struct K1cParams {
     int32_t* cell_count;
     uint32_t* cell_clamp;
     int32_t* end_n;
-    int32_t* end_l;
     long long* end_d;
+    int32_t tick_shift;      // Dmin in units of 2^tick_shift ticks (K2Params::tick_shift)
+    int32_t* next;           // k1_packed's persistent warps: next instance (count - 1)
     int32_t* flag_count;     // k1_packed -> wide fallback hand-over (count - 1)
     int32_t* flag_list;
 };
@@ -98,8 +100,9 @@ struct Group {
     int bar;                    // named barrier id
     long long* xs;              // [2][WPI][4]
     int par = 0;
+    // a hardware named barrier even for one warp (warp_bar, tp_internal.cuh)
     __device__ __forceinline__ void sync() const {
-        if (WPI == 1) __syncwarp();
+        if (WPI == 1) warp_bar(bar);
         else asm volatile("bar.sync %0, %1;" ::"r"(bar), "r"(WPI * 32) : "memory");
     }
     // publish 4 warp-level values (lane 0 writes), barrier, return the slot array of this round
@@ -133,7 +136,7 @@ __device__ __forceinline__ void claim_cell(const K1cParams& p, uint32_t k) {
     if (__ldcg(p.cell_tab + k) == -1 && atomicCAS(p.cell_tab + k, -1, -2) == -1) {
         const int idx = atomicAdd(p.cell_count, 1) + 1;
         p.cell_list[idx] = k;
-        p.cell_clamp[idx] = 0u;
+        p.cell_clamp[k] = 0u;
         p.cell_tab[k] = idx;
     }
 }
@@ -161,7 +164,11 @@ __device__ __forceinline__ void piece_deadlines(const K1cParams& p, Group<WPI>& 
     const size_t row = (size_t)i * p.H;
     const int C = (nn + 31) >> 5;
     long long* D = base + C;                         // behind meta[C] (8 bytes each)
+#ifdef TP_K1C_NOSMD
+    const bool sm = false;
+#else
     const bool sm = 2 * (C + h) <= words;
+#endif
     grp.sync();                                      // meta written by the whole group
     for (int k = gl; k < h; k += GL) {
         if (sm) D[k] = kNoDeadline;
@@ -174,7 +181,7 @@ __device__ __forceinline__ void piece_deadlines(const K1cParams& p, Group<WPI>& 
         const int l = r.z - r.x;                     // 1 <= l <= nn (validated; n = max l)
         const int2 mt = meta[(l - 1) >> 5];
         const int k = mt.y + __popc((unsigned)mt.x & (0xffffffffu >> (31 - ((l - 1) & 31)))) - 1;
-        const long long d = slack_ticks(__ldg(&p.t_dead[j]) - in.t_cur);
+        const long long d = slack_ticks(__ldg(&p.t_dead[j]) - in.t_cur, p.tick_shift);
         if (sm) atomicMin(&D[k], d);
         else atomicMin(&p.end_d[row + k], d);
     }
@@ -342,7 +349,7 @@ __device__ __forceinline__ void k1_body(const K1cParams& p, const int i, Group<W
     const int forced = p.force_adm ? min(max(p.force_adm[i], 0), nq) : -1;
     const uint32_t lmask = p.lost_mask ? p.lost_mask[i] : 0u;
     const int ncand = forced >= 0 ? forced : nq;
-    if (WPI == 1) __syncwarp();
+    if (WPI == 1) grp.sync();
     if (forced < 0 && ncand > 0 && (st & TP_ST_KV_OVER)) {
         st |= TP_ST_QUEUE_BLOCKED;
     } else {
@@ -525,22 +532,35 @@ __device__ __forceinline__ void k1_body(const K1cParams& p, const int i, Group<W
 #ifndef TP_K1P_MINB
 #define TP_K1P_MINB 12
 #endif
+// one warp's named barrier (see Group::sync)
+#define K1P_SYNC() warp_bar(w + 1)
 __global__ void __launch_bounds__(kWarpsPerCta * 32, TP_K1P_MINB)
 k1_packed(const __grid_constant__ K1cParams p) {
     extern __shared__ __align__(16) int smem[];
     const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-    const int i = blockIdx.x * (int)(blockDim.x >> 5) + w;
-    if (i >= p.n_inst) return;                        // warp-uniform
     int* sv = smem + (size_t)w * p.arr;
     const int SL = p.S_log2, S = 1 << SL, P = p.P, H = p.H;
     auto ph = [&](int m) { return (m - 1) + P * ((m - 1) >> SL); };   // physical index of m >= 1
+    // persistent warps: each takes the next instance from a global counter (instances differ a
+    // lot in length; a static assignment leaves warps idle behind the longest one of their CTA)
+    for (;;) {
+    int i = 0;
+#ifdef TP_K1C_STATIC
+    static __shared__ int s_once[4];
+    if (lane == 0) { i = s_once[w] == 12345 ? p.n_inst : blockIdx.x * 4 + w; s_once[w] = 12345; }
+#else
+    if (lane == 0) i = atomicAdd(p.next, 1) + 1;     // next holds count - 1 (reset by the launch's memset)
+#endif
+    i = __shfl_sync(kFull, i, 0);
+    if (i >= p.n_inst) break;                         // warp-uniform
+    K1P_SYNC();                                     // the previous instance's reads of sv are done
 
     const tp_inst in = p.inst[i];
     const int64_t rb = in.req_begin;
     const int nr = in.n_run, nq = in.n_queue, N = in.N;
     const FastDiv fdN((uint32_t)(N > 0 ? N : 1));
     for (int k = lane * 4; k + 3 < p.arr; k += 128) *reinterpret_cast<int4*>(sv + k) = make_int4(0, 0, 0, 0);
-    __syncwarp();
+    K1P_SYNC();
 
     bool bad = N < 1 || in.tp < 1 || (int64_t)in.tp >= kFeatLimit || nr < 0 || nq < 0 || in.kv_cap < 0 ||
                in.max_batch < 0 || rb < 0 || rb + (int64_t)nr + nq > (int64_t)p.n_req;
@@ -579,7 +599,7 @@ k1_packed(const __grid_constant__ K1cParams p) {
     bad = bad || foot >= kFeatLimit;
     if (!bad && (nr + nq >= 32768 || foot >= 65536)) {       // does not fit the packed words
         if (lane == 0) p.flag_list[atomicAdd(p.flag_count, 1) + 1] = i;   // flag_count holds count - 1
-        return;
+        continue;
     }
     if (bad) {
         if (p.B) {
@@ -596,11 +616,25 @@ k1_packed(const __grid_constant__ K1cParams p) {
             if (p.run_h) p.run_h[i] = 0;
             if (p.end_n) p.end_n[i] = 0;
         }
-        return;
+        continue;
     }
-    __syncwarp();
+#ifdef TP_K1C_FENCE
+    __threadfence_block();
+#endif
+    K1P_SYNC();
+#ifdef TP_K1C_DEBUG
+    {
+        int s0 = 0;
+        for (int k = lane; k < p.arr; k += 32) s0 += (k >= 1 && sv[k] != 0 && k < 2) ? 1 : 0;
+        if (lane == 0 && sv[0] != 0) printf("sv0 nonzero before m1 term: i=%d sv0=%d blk=%d w=%d\n", i, sv[0], (int)blockIdx.x, w);
+        if (lane == 0) {
+            const int old = atomicExch(&p.end_n[i], -7);
+            if (old == -7) printf("duplicate grab i=%d blk=%d w=%d\n", i, (int)blockIdx.x, w);
+        }
+    }
+#endif
     if (lane == 0) sv[0] += b1 * 65536 + kv1;     // the m = 1 terms (index 0 gets no other event)
-    __syncwarp();
+    K1P_SYNC();
 
     // ---- inclusive scan of the packed words over the lane segments ----
     int* seg = sv + lane * (S + P);
@@ -629,7 +663,12 @@ k1_packed(const __grid_constant__ K1cParams p) {
                                    max(m + 2 <= H ? (v.z & 0xFFFF) : 0, m + 3 <= H ? (v.w & 0xFFFF) : 0)));
         }
     }
-    __syncwarp();
+    K1P_SYNC();
+#ifdef TP_K1C_DEBUG
+    for (int m = 1 + lane; m <= nloc; m += 32)
+        if (sv[ph(m)] < 0) printf("after scan neg: i=%d m=%d v=%d nloc=%d blk=%d w=%d\n", i, m, sv[ph(m)], nloc, (int)blockIdx.x, w);
+    if (lane == 0 && i < 4) printf("grab i=%d blk=%d w=%d nr=%d nloc=%d\n", i, (int)blockIdx.x, w, nr, nloc);
+#endif
     int kvb = warp_max(kvmax);
     uint32_t st = kvb > in.kv_cap ? TP_ST_KV_OVER : 0u;
 
@@ -668,7 +707,7 @@ k1_packed(const __grid_constant__ K1cParams p) {
             }
 #pragma unroll 4
             for (int m = 1 + lane; m <= lc; m += 32) sv[ph(m)] += 65536 + (int)fdN.div((uint32_t)(m + q - 2)) + 1;
-            __syncwarp();
+            K1P_SYNC();
             ++B1;
             ++n_adm;
             nloc = max(nloc, lc);
@@ -679,7 +718,7 @@ k1_packed(const __grid_constant__ K1cParams p) {
     const int n = nloc;
     if (n == 0) st |= TP_ST_EMPTY;
     else if (lost) st |= TP_ST_BYPASS_LOST;
-    __syncwarp();
+    K1P_SYNC();
 
     if (p.B) {
         int* Bo = p.B + (int64_t)i * H;
@@ -719,6 +758,11 @@ k1_packed(const __grid_constant__ K1cParams p) {
         if (m <= nn) {
             const int v = sv[ph(m)];
             b = v >> 16;
+#ifdef TP_K1C_DEBUG
+            if (b < 0)
+                printf("k1_packed neg B: i=%d m=%d nn=%d n=%d v=%d nr=%d nq=%d nadm=%d blk=%d w=%d\n", i, m, nn, n, v,
+                       nr, nq, n_adm, (int)blockIdx.x, w);
+#endif
             // b < 2^15, kv < 2^16 here (the packed check): the clamped table lookups are exact
             k = cell_base + (uint32_t)__ldg(tB + min(b, lB1)) * nk1 + __ldg(tKV + min(v & 0xFFFF, lKV1));
         }
@@ -748,7 +792,11 @@ k1_packed(const __grid_constant__ K1cParams p) {
         p.end_n[i] = nn > 0 ? ends + 1 : 0;
     }
     Group<1> g1;
+    g1.bar = w + 1;
+#ifndef TP_K1C_NOPD
     piece_deadlines<1>(p, g1, i, in, rb, nr + n_adm, nn, h, meta, reinterpret_cast<long long*>(sv), p.arr, lane);
+#endif
+    }
 }
 
 template <int WPI, bool FLAGGED = false>   // FLAGGED: the instances k1_packed handed over
@@ -844,7 +892,22 @@ int launch_packed(const K1cParams& p0, int32_t n_inst, int32_t H, cudaStream_t s
             return TP_EINVAL;
         attr_bytes[dev] = (int)smem;
     }
-    k1_packed<<<(n_inst + wpb - 1) / wpb, wpb * 32, smem, s>>>(p);
+    // persistent: as many CTAs as fit at once (the warps take instances from p.next)
+    static int occ_smem[64] = {}, occ_blocks[64] = {};
+    if (dev < 64 && occ_smem[dev] != (int)smem) {
+        int b = 0;
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, k1_packed, wpb * 32, smem);
+        occ_blocks[dev] = b > 0 ? b : 1;
+        occ_smem[dev] = (int)smem;
+    }
+    int sms = 148;
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+#ifdef TP_K1C_NOPERSIST
+    const int grid = (n_inst + wpb - 1) / wpb;
+#else
+    const int grid = std::min((n_inst + wpb - 1) / wpb, sms * (dev < 64 ? occ_blocks[dev] : 1));
+#endif
+    k1_packed<<<grid, wpb * 32, smem, s>>>(p);
     if (cudaPeekAtLastError() != cudaSuccess) return TP_ECUDA;
     return launch_wpi<1, true>(p0, n_inst, H, s);
 }
@@ -855,7 +918,7 @@ int launch_project_compact(const K2Params& w, const tp_inst* inst, int32_t n_ins
                            int32_t* n, int32_t* n_adm, uint32_t* status, uint32_t skip, cudaStream_t s,
                            const int32_t* force_adm, const uint32_t* lost_mask) {
     if (n_inst == 0) return TP_OK;
-    if (!w.cell_tab || !w.end_n) return TP_EINVAL;
+    if (!w.cell_tab || !w.end_n || !w.k1_next) return TP_EINVAL;
     K1cParams p;
     p.inst = inst;
     p.req = reinterpret_cast<const int4*>(req);
@@ -887,13 +950,14 @@ int launch_project_compact(const K2Params& w, const tp_inst* inst, int32_t n_ins
     p.cell_count = w.cell_count;
     p.cell_clamp = w.cell_clamp;
     p.end_n = w.end_n;
-    p.end_l = w.end_l;
     p.end_d = w.end_d;
+    p.tick_shift = w.tick_shift;
+    p.next = w.k1_next;
     p.flag_count = w.flag_count;
     p.flag_list = w.flag_list;
-    // flag_count, cell_count (both count - 1) and cell_tab are contiguous: one reset; claimers zero
+    // K3c's counters, flag_count, cell_count (all count - 1) and cell_tab are contiguous: one reset; claimers zero
     // their cells' clamp masks
-    if (cudaMemsetAsync(w.flag_count, 0xFF, 8 + (size_t)w.n_cells * 4, s) != cudaSuccess) return TP_ECUDA;
+    if (cudaMemsetAsync(w.k1_next, 0xFF, 20 + (size_t)w.n_cells * 4, s) != cudaSuccess) return TP_ECUDA;
     // warps per instance: small batches get several warps per instance (the per-instance chain
     // of dependent loads and reductions is the latency; shorter per-warp loops shorten it), large
     // batches one (the GPU is full anyway)

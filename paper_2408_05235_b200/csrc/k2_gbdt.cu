@@ -93,6 +93,14 @@ __device__ __forceinline__ uint32_t step_from(uint32_t base2, uint32_t w, uint32
     return out;
 }
 
+// K3c's T' table entry of one (cell, level): int64 ticks of 2^-40 s, or, with the model's
+// tick_shift = 8, uint32 units of 2^8 ticks (exact: see Model::tick_shift)
+__device__ __forceinline__ void store_ticks(const K2Params& p, size_t at, float ips) {
+    const long long t = ticks_of(ips);
+    if (p.tick_shift) reinterpret_cast<uint32_t*>(p.lut_ticks)[at] = (uint32_t)(t >> p.tick_shift);
+    else p.lut_ticks[at] = t;
+}
+
 __device__ __forceinline__ uint32_t rank_of(const float* __restrict__ c, int cnt, float x) {
     int lo = 0, hi = cnt;   // upper bound: number of cuts <= x
     while (lo < hi) {
@@ -191,7 +199,7 @@ k2_runs(const __grid_constant__ K2Params p) {
             if (cells && __ldcg(p.cell_tab + key) == -1 && atomicCAS(p.cell_tab + key, -1, -2) == -1) {
                 const int idx = atomicAdd(p.cell_count, 1) + 1;   // cell_count holds count - 1
                 p.cell_list[idx] = key;
-                p.cell_clamp[idx] = 0u;
+                p.cell_clamp[key] = 0u;
                 p.cell_tab[key] = idx;
             }
         }
@@ -220,9 +228,9 @@ k2_expand(const __grid_constant__ K2Params p) {
     bool clamped = false;
     for (int k = tid; k < h; k += kExpandThreads) {
         sm[k] = p.run_m[row + k];
-        const int idx = p.cell_tab[p.run_key[row + k]];
-        sidx[k] = idx;
-        clamped |= p.cell_clamp[idx] != 0;
+        const uint32_t key = p.run_key[row + k];
+        sidx[k] = p.cell_tab[key];
+        clamped |= p.cell_clamp[key] != 0;
     }
     if (__syncthreads_or(clamped) && tid == 0) atomicOr(p.status + i, (uint32_t)TP_ST_IPS_CLAMPED);
     const int F = p.F;
@@ -344,6 +352,7 @@ k2_gbdt(const __grid_constant__ K2Params p, int TC, int nchunks) {
         const int64_t t = t0 + (int64_t)round * nwarps + warp;
         const bool active = t < t1;
         int i = 0, m = 0, u0 = 0, ni = 0, m_end = 0, cidx = -1;
+        uint32_t cell_id = 0;
         uint32_t xlo = 0, xhi[RU];
         float acc[RU];
         if (active) {
@@ -357,6 +366,7 @@ k2_gbdt(const __grid_constant__ K2Params p, int TC, int nchunks) {
                     cidx = (int)(uu - (int64_t)ug * ncell);
                     u0 = ug * RU;
                     const uint32_t c = p.cell_list[cidx];
+                    cell_id = c;
                     const uint32_t nk1 = (uint32_t)nKV + 1, nb1 = (uint32_t)nB + 1;
                     rkv = c % nk1;
                     const uint32_t rb = (c / nk1) % nb1, rtp = c / (nk1 * nb1);
@@ -481,9 +491,9 @@ k2_gbdt(const __grid_constant__ K2Params p, int TC, int nchunks) {
                     for (int r = 0; r < RU; ++r)
                         if (u0 + r < p.F) {
                             p.lut[(size_t)cidx * p.F + u0 + r] = acc[r];
-                            p.lut_ticks[(size_t)cidx * p.F + u0 + r] = ticks_of(acc[r]);
+                            store_ticks(p, (size_t)cell_id * p.F + u0 + r, acc[r]);
                         }
-                    if (cmask) atomicOr(p.cell_clamp + cidx, cmask);
+                    if (cmask) atomicOr(p.cell_clamp + cell_id, cmask);
                 }
             } else if constexpr (MODE == kRuns) {
                 // the lane writes its run [m, m_end) for its RU levels
@@ -608,10 +618,10 @@ k2_cells_phase(const __grid_constant__ K2Params p, int t_begin, int t_count, int
                 if (u0 + r < p.F) {
                     if (isnan(v) || cl != v) cmask |= 1u << (u0 + r);
                     p.lut[(size_t)cidx * p.F + u0 + r] = cl;
-                    if (p.lut_ticks) p.lut_ticks[(size_t)cidx * p.F + u0 + r] = ticks_of(cl);
+                    if (p.lut_ticks) store_ticks(p, (size_t)c * p.F + u0 + r, cl);
                 }
             }
-            if (cmask) atomicOr(p.cell_clamp + cidx, cmask);
+            if (cmask) atomicOr(p.cell_clamp + c, cmask);
         } else {
 #pragma unroll
             for (int r = 0; r < RR; ++r)
@@ -784,8 +794,8 @@ int64_t model_cells(const Model& m) {
     return (int64_t)(m.n_cuts[0] + 1) * (m.n_cuts[1] + 1) * (m.n_cuts[2] + 1);
 }
 
-// Workspace: run_h [I], run_m [I][H], run_key [I][H], end_n [I], end_l [I][H], end_d [I][H]
-// (compact path); cell mode adds cell_tab [n_cells], cell_list [cap], cell_count, cell_clamp [cap],
+// Workspace: run_h [I], run_m [I][H], run_key [I][H], end_n [I], end_d [I][H]
+// (compact path); cell mode adds cell_tab [n_cells], cell_list [cap], cell_count, cell_clamp [n_cells],
 // lut [cap][F] with cap = min(n_cells, I * H).  Returns the bytes used past `ws`.
 static size_t carve(void* ws, int64_t n_cells, int32_t n_inst, int32_t H, int32_t F, K2Params& p) {
     const size_t I = (size_t)(n_inst > 0 ? n_inst : 1);
@@ -799,13 +809,14 @@ static size_t carve(void* ws, int64_t n_cells, int32_t n_inst, int32_t H, int32_
     a = align256(a + I * (size_t)H * 4);
     p.end_n = reinterpret_cast<int32_t*>(a);
     a = align256(a + I * 4);
-    p.end_l = reinterpret_cast<int32_t*>(a);
-    a = align256(a + I * (size_t)H * 4);
     p.end_d = reinterpret_cast<long long*>(a);
     a = align256(a + I * (size_t)H * 8);
     p.flag_list = reinterpret_cast<int32_t*>(a);
     a = align256(a + I * 4);
     p.flag_count = nullptr;
+    p.k3_next = nullptr;
+    p.k1_next = nullptr;
+    p.k3_done = nullptr;
     p.cell_tab = nullptr;
     p.cell_list = nullptr;
     p.cell_count = nullptr;
@@ -818,19 +829,23 @@ static size_t carve(void* ws, int64_t n_cells, int32_t n_inst, int32_t H, int32_
         const int64_t cap = std::min<int64_t>(n_cells, (int64_t)I * H);
         p.n_cells = (int32_t)n_cells;
         p.cell_cap = (int32_t)cap;
-        // cell_count (stored as count - 1) directly before cell_tab: one 0xFF memset resets both
-        p.flag_count = reinterpret_cast<int32_t*>(a);
-        p.cell_count = reinterpret_cast<int32_t*>(a + 4);
-        p.cell_tab = reinterpret_cast<int32_t*>(a + 8);
-        a = align256(a + 8 + (size_t)n_cells * 4);
+        // K3c's counters, flag_count and cell_count (all stored as count - 1) directly before
+        // cell_tab: one 0xFF memset (K1c's launch) resets them all
+        p.k1_next = reinterpret_cast<int32_t*>(a);
+        p.k3_next = reinterpret_cast<int32_t*>(a + 4);
+        p.k3_done = reinterpret_cast<int32_t*>(a + 8);
+        p.flag_count = reinterpret_cast<int32_t*>(a + 12);
+        p.cell_count = reinterpret_cast<int32_t*>(a + 16);
+        p.cell_tab = reinterpret_cast<int32_t*>(a + 20);
+        a = align256(a + 20 + (size_t)n_cells * 4);
         p.cell_list = reinterpret_cast<uint32_t*>(a);
         a = align256(a + (size_t)cap * 4);
-        p.cell_clamp = reinterpret_cast<uint32_t*>(a);
-        a = align256(a + (size_t)cap * 4);
+        p.cell_clamp = reinterpret_cast<uint32_t*>(a);       // by cell id
+        a = align256(a + (size_t)n_cells * 4);
         p.lut = reinterpret_cast<float*>(a);
         a = align256(a + (size_t)cap * F * 4);
-        p.lut_ticks = reinterpret_cast<long long*>(a);
-        a = align256(a + (size_t)cap * F * 8);
+        p.lut_ticks = reinterpret_cast<long long*>(a);       // by cell id: K3c indexes it by the piece's key
+        a = align256(a + (size_t)n_cells * F * 8);
     }
     return (size_t)(a - a0);
 }

@@ -226,9 +226,9 @@ k3_select_runs(const tp_inst* __restrict__ inst, const int4* __restrict__ req, c
     uint32_t cl = 0;
     for (int k = tid; k < h; k += kThreads) {
         r_start[k] = __ldg(ws.run_m + row + k);
-        const int rr = __ldg(ws.cell_tab + __ldg(ws.run_key + row + k));
-        r_row[k] = rr;
-        cl |= __ldg(ws.cell_clamp + rr);
+        const uint32_t key = __ldg(ws.run_key + row + k);
+        r_row[k] = __ldg(ws.cell_tab + key);
+        cl |= __ldg(ws.cell_clamp + key);
     }
     if (tid == 0) r_start[h] = n + 1;
     for (int o = 16; o; o >>= 1) cl |= __shfl_xor_sync(0xffffffffu, cl, o);

@@ -116,6 +116,26 @@ int load_impl(const void* host_blob, size_t nbytes, int device, tp_gbdt** out) {
         if ((int)cuts[f].size() > tp::kMaxCuts) return TP_EFORMAT;
     }
 
+    // Output range of the ensemble: base + sum over trees of [min leaf, max leaf], widened by a bound
+    // on the fp32 rounding of the sequential sum (each addition errs by <= 2^-24 of a partial sum
+    // whose magnitude is <= S).  If every output is inside (1, 512) IPS, T' = fl32(1/ips) lies in
+    // (2^-9, 1) s for every cell and level: its tick count (units of 2^-40 s) is a multiple of 2^8
+    // below 2^40, so the compact path keeps T' / 2^8 ticks in 32 bits, exactly (tick_shift = 8).
+    double out_lo = base, out_hi = base, S = std::fabs((double)base);
+    for (auto& t : trees) {
+        double mn = INFINITY, mx = -INFINITY;
+        for (auto& nd : t)
+            if (nd.feature == -1) {
+                mn = std::min(mn, (double)nd.leaf);
+                mx = std::max(mx, (double)nd.leaf);
+            }
+        out_lo += mn;
+        out_hi += mx;
+        S += std::max(std::fabs(mn), std::fabs(mx));
+    }
+    const double rerr = 2.0 * ((double)nt + 1.0) * 0x1p-24 * S;
+    const int tick_shift = (out_lo - rerr > 1.0 && out_hi + rerr < 512.0) ? 8 : 0;
+
     const size_t words_per_tree = std::max<size_t>(4, (size_t)2 << D);   // >= 16 B: TMA size/alignment unit
     if ((uint64_t)nt * words_per_tree > tp::kMaxModelWords) return TP_EFORMAT;  // > 1 GiB of node words
     std::vector<uint32_t> words(std::max<size_t>(1, nt * words_per_tree), 0u);
@@ -128,6 +148,7 @@ int load_impl(const void* host_blob, size_t nbytes, int device, tp_gbdt** out) {
     m.n_trees = (int32_t)nt;
     m.depth = D;
     m.base = base;
+    m.tick_shift = tick_shift;
     for (int f = 0; f < 4; ++f) {
         m.n_cuts[f] = (int32_t)cuts[f].size();
         m.cut_off[f] = (int32_t)allc.size();
@@ -211,6 +232,7 @@ extern "C" int tp_gbdt_get_info(const tp_gbdt* h, tp_gbdt_info* out) {
     out->depth = h->m.depth;
     for (int f = 0; f < 4; ++f) out->n_cuts[f] = h->m.n_cuts[f];
     out->base_score = h->m.base;
+    out->tick_shift = h->m.tick_shift;
     out->device_bytes = h->m.device_bytes;
     out->node_bytes = (int64_t)h->m.n_trees * std::max<int64_t>(4, (int64_t)2 << h->m.depth) * 4;
     return TP_OK;

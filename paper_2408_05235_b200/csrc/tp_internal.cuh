@@ -72,6 +72,10 @@ struct Model {
     uint16_t* d_rtab = nullptr;
     int32_t rtab_off[2] = {0, 0}, rtab_len[2] = {0, 0};
     int64_t device_bytes = 0;
+    // 8 when every possible output of the ensemble lies in (1, 512) IPS (bounded at load from the
+    // leaves): then every T' = fl32(1/ips) lies in (2^-9, 1) s, so its tick count is a multiple of
+    // 2^8 below 2^40 and K2 can store T' / 2^8 ticks in 32 bits, exactly (compact path); else 0
+    int32_t tick_shift = 0;
 };
 
 struct K2Params {
@@ -102,21 +106,29 @@ struct K2Params {
     uint32_t* cell_list;     // [cap] LUT row -> cell id
     int32_t* cell_count;     // [1] distinct cells - 1 (directly before cell_tab: one reset for both)
     float* lut;              // [cap][F] clamped IPS
-    long long* lut_ticks;    // [cap][F] T' = fl32(1 / ips) in ticks of 2^-40 s (readings A-9, A-10)
-    uint32_t* cell_clamp;    // [cap] bit u set if level u's value was clamped
+    long long* lut_ticks;    // [n_cells][F] by cell id: T' = fl32(1 / ips) in ticks of 2^-40 s (A-9, A-10)
+    uint32_t* cell_clamp;    // [n_cells] by cell id: bit u set if level u's value was clamped
     int32_t n_cells, cell_cap;
     // compact path (K1c -> K2 cells -> K3c): K1c already built the runs and claimed the cells, so
     // the K2 launch skips its k2_runs pre-pass and the cell-table resets
     int32_t runs_ready;
-    // compact path: per instance, the end positions l that carry a deadline (ascending) and
-    // Dmin[l] in ticks of 2^-40 s (reading A-12), written by K1c, read by K3c
+    // compact path: the model's tick_shift; with 8, lut_ticks holds uint32 T' / 2^8 tick values
+    // and K1c's Dmin / K3c's T_R count units of 2^8 ticks (2^-32 s)
+    int32_t tick_shift;
+    // compact path: run_h / run_m / run_key hold K1c's PIECES (k1_compact.cu, piece_rules), end_d
+    // each piece's Dmin in ticks of 2^-40 s (reading A-12; INT64_MAX: no deadline), end_n the
+    // number of end positions (statistics); written by K1c, read by K3c
     int32_t* end_n;          // [n_inst]
-    int32_t* end_l;          // [n_inst][H]
     long long* end_d;        // [n_inst][H]
     // compact path, K1c's packed histograms: instances that do not fit them (count - 1, directly
     // before cell_count: reset by the same memset) and their list, handled by the wide kernel
     int32_t* flag_count;
     int32_t* flag_list;      // [n_inst]
+    // compact path, K3c's persistent warps: next instance and finished CTAs (count - 1; reset by
+    // K1c's memset and re-armed by K3c's last CTA)
+    int32_t* k3_next;
+    int32_t* k3_done;
+    int32_t* k1_next;        // K1c (packed, persistent warps): next instance (count - 1)
 };
 
 // workspace for tp_predict_ips_runs; cell mode is used when the model's dense cell space
@@ -148,11 +160,29 @@ cudaError_t launch_pdl(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t sme
     return cudaLaunchKernelEx(&cfg, kern, std::forward<Args>(args)...);
 }
 
+// One warp's own hardware barrier (named barrier `id` in [1, 8], 32 threads).  Used where a
+// warp hands data to itself through shared memory inside a persistent loop: a __syncwarp() that
+// the compiler considers redundant is emitted as nothing, and the lanes are then not reliably
+// reconverged (measured on B200: stale shared-memory reads).  The ids are immediates so that ptxas
+// reserves only the barriers actually used (a register id reserves all 16 and caps occupancy).
+__device__ __forceinline__ void warp_bar(int id) {
+    switch (id) {
+        case 1: asm volatile("bar.sync 1, 32;" ::: "memory"); break;
+        case 2: asm volatile("bar.sync 2, 32;" ::: "memory"); break;
+        case 3: asm volatile("bar.sync 3, 32;" ::: "memory"); break;
+        case 4: asm volatile("bar.sync 4, 32;" ::: "memory"); break;
+        case 5: asm volatile("bar.sync 5, 32;" ::: "memory"); break;
+        case 6: asm volatile("bar.sync 6, 32;" ::: "memory"); break;
+        case 7: asm volatile("bar.sync 7, 32;" ::: "memory"); break;
+        default: asm volatile("bar.sync 8, 32;" ::: "memory"); break;
+    }
+}
+
 constexpr long long kNoDeadline = 0x7fffffffffffffffLL;
 // ceil(s * 2^40) for the E2E compare T_R < s (T_R integer ticks of 2^-40 s, reading A-12):
 // <= 0 / NaN -> 0 (never passes), >= 2^62 -> INT64_MAX (always passes; T_R < 2^58).
-__device__ __forceinline__ long long slack_ticks(double s) {
-    const double d = s * 0x1p40;
+__device__ __forceinline__ long long slack_ticks(double s, int shift = 0) {
+    const double d = s * (shift ? 0x1p32 : 0x1p40);   // units of 2^shift ticks (shift 0 or 8)
     if (!(d > 0.0)) return 0;
     if (d >= 0x1p62) return kNoDeadline;
     return (long long)ceil(d);

@@ -38,7 +38,7 @@ _vp, _i32, _i64, _f32 = ctypes.c_void_p, ctypes.c_int32, ctypes.c_int64, ctypes.
 
 class GbdtInfo(ctypes.Structure):
     _fields_ = [("n_trees", ctypes.c_int32), ("depth", ctypes.c_int32), ("n_cuts", ctypes.c_int32 * 4),
-                ("base_score", ctypes.c_float), ("_pad", ctypes.c_int32), ("device_bytes", ctypes.c_int64),
+                ("base_score", ctypes.c_float), ("tick_shift", ctypes.c_int32), ("device_bytes", ctypes.c_int64),
                 ("node_bytes", ctypes.c_int64)]
 
 
