@@ -529,31 +529,42 @@ __device__ __forceinline__ void k1_body(const K1cParams& p, const int i, Group<W
 // written straight from the ballot compaction (consecutive positions per step: coalesced); the
 // Eq. 4 table is built in windows of the histogram space.  Instances the check rejects are handed
 // to k1_compact<1, true> through the flag list.
+#ifndef TP_K1P_WARPS
+#define TP_K1P_WARPS 4       // warps (instances in flight) per CTA
+#endif
 #ifndef TP_K1P_MINB
-#define TP_K1P_MINB 12
+#define TP_K1P_MINB (48 / TP_K1P_WARPS)
+#endif
+
+#ifndef TP_K1P_PERSIST
+#define TP_K1P_PERSIST 0     // 1: persistent warps over a global instance counter (measured slower at C3/C5)
 #endif
 // one warp's named barrier (see Group::sync)
 #define K1P_SYNC() warp_bar(w + 1)
-__global__ void __launch_bounds__(kWarpsPerCta * 32, TP_K1P_MINB)
+__global__ void __launch_bounds__(TP_K1P_WARPS * 32, TP_K1P_MINB)
 k1_packed(const __grid_constant__ K1cParams p) {
     extern __shared__ __align__(16) int smem[];
     const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
     int* sv = smem + (size_t)w * p.arr;
+    const int lB1 = p.rtab_len[0] - 1, lKV1 = p.rtab_len[1] - 1;   // tables end past the last cut
+    const uint16_t* tB = p.rtab + p.rtab_off[0];
+    const uint16_t* tKV = p.rtab + p.rtab_off[1];
     const int SL = p.S_log2, S = 1 << SL, P = p.P, H = p.H;
     auto ph = [&](int m) { return (m - 1) + P * ((m - 1) >> SL); };   // physical index of m >= 1
+#if TP_K1P_PERSIST
     // persistent warps: each takes the next instance from a global counter (instances differ a
     // lot in length; a static assignment leaves warps idle behind the longest one of their CTA)
     for (;;) {
     int i = 0;
-#ifdef TP_K1C_STATIC
-    static __shared__ int s_once[4];
-    if (lane == 0) { i = s_once[w] == 12345 ? p.n_inst : blockIdx.x * 4 + w; s_once[w] = 12345; }
-#else
     if (lane == 0) i = atomicAdd(p.next, 1) + 1;     // next holds count - 1 (reset by the launch's memset)
-#endif
     i = __shfl_sync(kFull, i, 0);
     if (i >= p.n_inst) break;                         // warp-uniform
-    K1P_SYNC();                                     // the previous instance's reads of sv are done
+    K1P_SYNC();                                       // the previous instance's reads of sv are done
+#else
+    do {                                              // one instance per warp
+    const int i = blockIdx.x * (int)(blockDim.x >> 5) + w;
+    if (i >= p.n_inst) break;
+#endif
 
     const tp_inst in = p.inst[i];
     const int64_t rb = in.req_begin;
@@ -740,14 +751,13 @@ k1_packed(const __grid_constant__ K1cParams p) {
     const size_t row = (size_t)i * H;
 
     // ---- pieces (piece_rules), records straight from the ballot compaction, claims ----
-    const int lB1 = p.rtab_len[0] - 1, lKV1 = p.rtab_len[1] - 1;   // tables end past the last cut
-    const uint16_t* tB = p.rtab + p.rtab_off[0];
-    const uint16_t* tKV = p.rtab + p.rtab_off[1];
     const int nKV = p.cut_off[3] - p.cut_off[2];
     const uint32_t rtp = rank_of(p.cuts + p.cut_off[0], p.cut_off[1] - p.cut_off[0], (float)in.tp);
     const uint32_t nk1 = (uint32_t)nKV + 1;
     const uint32_t cell_base = rtp * (uint32_t)(p.cut_off[2] - p.cut_off[1] + 1) * nk1;
     int2* meta = reinterpret_cast<int2*>(sv);       // [chunk] (head mask, heads before the chunk)
+    int32_t* const rec_m = p.run_m + row;
+    uint32_t* const rec_k = p.run_key + row;
     int h = 0, ends = 0;
     uint32_t kcarry = 0xffffffffu;
     int bcarry = 0;
@@ -764,7 +774,8 @@ k1_packed(const __grid_constant__ K1cParams p) {
                        nr, nq, n_adm, (int)blockIdx.x, w);
 #endif
             // b < 2^15, kv < 2^16 here (the packed check): the clamped table lookups are exact
-            k = cell_base + (uint32_t)__ldg(tB + min(b, lB1)) * nk1 + __ldg(tKV + min(v & 0xFFFF, lKV1));
+            k = cell_base + (uint32_t)__ldg(tB + (uint32_t)min(b, lB1)) * nk1 +
+                __ldg(tKV + (uint32_t)min(v & 0xFFFF, lKV1));
         }
         uint32_t pk = __shfl_up_sync(kFull, k, 1);
         int pb = __shfl_up_sync(kFull, b, 1);
@@ -780,8 +791,8 @@ k1_packed(const __grid_constant__ K1cParams p) {
         ends += __popc(__ballot_sync(kFull, endp));
         if (head) {
             const int pos = h + __popc(mask & ltm);
-            p.run_m[row + pos] = m;
-            p.run_key[row + pos] = k;
+            rec_m[pos] = m;
+            rec_k[pos] = k;
             claim_cell(p, k);
         }
         if (lane == 0) meta[(m0 - 1) >> 5] = make_int2((int)mask, h);
@@ -796,7 +807,11 @@ k1_packed(const __grid_constant__ K1cParams p) {
 #ifndef TP_K1C_NOPD
     piece_deadlines<1>(p, g1, i, in, rb, nr + n_adm, nn, h, meta, reinterpret_cast<long long*>(sv), p.arr, lane);
 #endif
+#if TP_K1P_PERSIST
     }
+#else
+    } while (0);
+#endif
 }
 
 template <int WPI, bool FLAGGED = false>   // FLAGGED: the instances k1_packed handed over
@@ -882,33 +897,36 @@ int launch_packed(const K1cParams& p0, int32_t n_inst, int32_t H, cudaStream_t s
     p.arr = g.arr;
     const size_t per_warp = (size_t)g.arr * sizeof(int);
     if (per_warp > 200 * 1024) return TP_EINVAL;
-    const int wpb = (int)std::max<size_t>(1, std::min<size_t>(kWarpsPerCta, (100 * 1024) / per_warp));
+    const int wpb = (int)std::max<size_t>(1, std::min<size_t>(TP_K1P_WARPS, (100 * 1024) / per_warp));
     const size_t smem = (size_t)wpb * per_warp;
     int dev = 0;
     if (cudaGetDevice(&dev) != cudaSuccess) return TP_ECUDA;
-    static int attr_bytes[64] = {};
-    if (dev < 64 && attr_bytes[dev] < (int)smem) {
-        if (cudaFuncSetAttribute(k1_packed, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess)
-            return TP_EINVAL;
-        attr_bytes[dev] = (int)smem;
-    }
-    // persistent: as many CTAs as fit at once (the warps take instances from p.next)
-    static int occ_smem[64] = {}, occ_blocks[64] = {};
-    if (dev < 64 && occ_smem[dev] != (int)smem) {
-        int b = 0;
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, k1_packed, wpb * 32, smem);
-        occ_blocks[dev] = b > 0 ? b : 1;
-        occ_smem[dev] = (int)smem;
-    }
-    int sms = 148;
-    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-#ifdef TP_K1C_NOPERSIST
-    const int grid = (n_inst + wpb - 1) / wpb;
+    auto go = [&](auto kern, int li) {
+        static int attr_bytes[2][64] = {}, occ_smem[2][64] = {}, occ_blocks[2][64] = {};
+        if (dev < 64 && attr_bytes[li][dev] < (int)smem) {
+            if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess)
+                return TP_EINVAL;
+            attr_bytes[li][dev] = (int)smem;
+        }
+        // persistent: as many CTAs as fit at once (the warps take instances from p.next)
+        if (dev < 64 && occ_smem[li][dev] != (int)smem) {
+            int b = 0;
+            cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, kern, wpb * 32, smem);
+            occ_blocks[li][dev] = b > 0 ? b : 1;
+            occ_smem[li][dev] = (int)smem;
+        }
+        int sms = 148;
+        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+#if TP_K1P_PERSIST
+        const int grid = std::min((n_inst + wpb - 1) / wpb, sms * (dev < 64 ? occ_blocks[li][dev] : 1));
 #else
-    const int grid = std::min((n_inst + wpb - 1) / wpb, sms * (dev < 64 ? occ_blocks[dev] : 1));
+        const int grid = (n_inst + wpb - 1) / wpb;
 #endif
-    k1_packed<<<grid, wpb * 32, smem, s>>>(p);
-    if (cudaPeekAtLastError() != cudaSuccess) return TP_ECUDA;
+        kern<<<grid, wpb * 32, smem, s>>>(p);
+        return cudaPeekAtLastError() == cudaSuccess ? TP_OK : TP_ECUDA;
+    };
+    const int rc = go(k1_packed, 0);
+    if (rc != TP_OK) return rc;
     return launch_wpi<1, true>(p0, n_inst, H, s);
 }
 }  // namespace
