@@ -208,64 +208,178 @@ def slice_replay(data, i0, i1):
 
 def bench_replay(args, cfg, rank, world, local, dist, dist_test):
     """BASELINE configs[3]: 1M requests over 4,096 instance states, all re-decided every iteration.
-    A step = one round: decide every instance (tp_decide) + advance every instance one engine
-    iteration (tp_replay_advance), all on the GPU.  Instances are split over ranks."""
+    A round = decide every instance (tp_decide: K1c -> K2 -> K3c) + advance every instance one
+    engine iteration (tp_replay_advance), all on the GPU; instances are split over ranks.  The
+    WHOLE replay is timed (every round until every arrival is consumed and every request has
+    finished, or --replay-cap rounds): sustained decisions/s = instances x rounds / sum of round
+    times, per-round p50 / p90.  e2e: the same replay through the public API with the trace
+    uploaded from pinned host memory inside the timed region and every round's (level, status)
+    read back."""
     import torch
-    from paper_2408_05235_b200 import replay, shard, tp
+    from paper_2408_05235_b200 import replay, runner, shard, tp
     dev = torch.device("cuda", local)
     rc = W.ReplayConfig()
     data = W.gen_replay(rc)
     i0, i1 = shard.shard_range(rc.n_inst, rank, world)
     data = slice_replay(data, i0, i1)
-    model = tp.Gbdt(W.write_blob(W.config_ensemble(cfg)), local)
+    I = i1 - i0
+    blob = W.write_blob(W.config_ensemble(cfg))
+    model = tp.Gbdt(blob, local)
+    info = model.info()
     rp = replay.Replay(data, model, dev, admission=args.admission, search=args.search)
     stream = torch.cuda.current_stream(dev)
     sms = torch.cuda.get_device_properties(dev).multi_processor_count
-    for _ in range(max(args.warmup, 3)):
+    for _ in range(max(args.warmup, 3)):              # warm-up rounds (then back to the initial state)
         rp.round(stream)
+    rp.reset(stream)
     torch.cuda.synchronize(dev)
-    ev = [[torch.cuda.Event(enable_timing=True) for _ in range(3)] for _ in range(args.steps)]
+    cap = args.replay_cap
+
+    def whole(ev_pairs, readback=None):
+        """Rounds until drained, or until every arrival has been consumed and no request has
+        completed for 500 rounds (the rest are blocked for good: FIFO head-of-line requests whose
+        KV footprint exceeds their instance's capacity), or cap; checked every 100 rounds."""
+        r, last_done, still = 0, -1, 0
+        while r < cap:
+            n = min(100, cap - r)
+            for k in range(n):
+                a, b = ev_pairs[r + k]
+                a.record(stream)
+                rp.round(stream)
+                if readback is not None:
+                    readback.copy_(torch.stack([rp.level, rp.status]), non_blocking=True)
+                b.record(stream)
+            r += n
+            torch.cuda.synchronize(dev)
+            if rp.finished():
+                break
+            done = rp.stats_dict()["completed"]
+            still = still + 1 if (done == last_done and rp.arrivals_consumed()) else 0
+            last_done = done
+            if still >= 5:
+                break
+        return r
+
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(cap)]
     clocks = Clocks(local)
     if world > 1:
         dist.barrier()
     clocks.start()
     time.sleep(0.3)
-    for k in range(args.steps):
-        ev[k][0].record(stream)
-        rp.decide(stream)
-        ev[k][1].record(stream)
-        rp.advance(stream)
-        ev[k][2].record(stream)
-    torch.cuda.synchronize(dev)
+    rounds = whole(ev)
     clk = clocks.stop()
-    dec_ms = float(sum(e[0].elapsed_time(e[1]) for e in ev))
-    adv_ms = float(sum(e[1].elapsed_time(e[2]) for e in ev))
-    tot = torch.tensor([dec_ms + adv_ms, dec_ms], dtype=torch.float64, device=dev)
+    round_ms = np.array([a.elapsed_time(b) for a, b in ev[:rounds]])
+    stats = rp.stats_dict()
+    drained = rp.finished()
+    blocked = rp.in_flight()
+    # e2e: the trace uploaded from pinned host memory inside the timed region, every round's
+    # decisions read back to pinned host memory
+    out_h = torch.empty((2, max(I, 1)), dtype=torch.int32).pin_memory()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    torch.cuda.synchronize(dev)
+    e0.record(stream)
+    rp.reset(stream)
+    ev2 = [(torch.cuda.Event(enable_timing=False), torch.cuda.Event(enable_timing=False)) for _ in range(cap)]
+    rounds2 = whole(ev2, readback=out_h[:, :I])
+    e1.record(stream)
+    torch.cuda.synchronize(dev)
+    e2e_ms = e0.elapsed_time(e1) - 0.0
+    # per-kernel breakdown and rooflines on snapshots of the replay state (initial and mid-replay):
+    # the compact path's kernels on exactly those inputs, with events between the kernels
+    snaps = []
+    rp.reset(stream)
+    for target in (0, rounds // 2):
+        while rp.rounds < target:
+            rp.round(stream)
+        inst_h, req_h, td_h, _ = rp.state()
+        snaps.append(dict(inst=inst_h, req=req_h, t_dead=td_h, H=data["H"], freq=data["freq"],
+                          tbt_slo=data["tbt_slo"]))
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
+    kern_rows = []
+    for sn in snaps:
+        rnd = runner.Round(sn, dev, k2_mode="compact", model=model, search=args.search)
+        rnd.bkv = False
+        for _ in range(2):
+            rnd.run(model, stream)
+        evk = [[torch.cuda.Event(enable_timing=True) for _ in range(4)] for _ in range(10)]
+        for e in evk:
+            flush.zero_()
+            e[0].record(stream)
+            rnd.project(stream)
+            e[1].record(stream)
+            rnd.predict(model, stream)
+            e[2].record(stream)
+            rnd.select(stream)
+            e[3].record(stream)
+        torch.cuda.synchronize(dev)
+        k_ms = np.array([[e[j].elapsed_time(e[j + 1]) for j in range(3)] for e in evk]).mean(axis=0)
+        cs = tp.compact_stats(model, rnd.work, rnd.I, rnd.H, rnd.F)
+        nadm = rnd.n_adm[:rnd.I].cpu().numpy().astype(np.int64)
+        kern_rows.append((sn, k_ms, cs, int(sn["inst"]["n_run"].astype(np.int64).sum() + nadm.sum())))
+        del rnd
+    tot = torch.tensor([float(round_ms.sum()), e2e_ms], dtype=torch.float64, device=dev)
     if world > 1:
         c = tot.cpu() if dist_test else tot
         dist.all_reduce(c, op=dist.ReduceOp.MAX)
         tot = c.to(dev)
     if rank != 0:
         return
-    I = rc.n_inst
-    st = rp.stats_dict()
+    peaks = measured_peaks()
+    hbm = float(peaks.get("hbm_gbs", 6553.6))
+    smax = float(peaks.get("sm_max_mhz", 1965.0))
+    lds_peak = sms * 128 * smax * 1e6 / 1e9
+    per_row = info.n_trees * (info.depth + 1) * 4
+    snaps_out = []
+    for (sn, k_ms, cs, n_sched), tag in zip(kern_rows, ("initial state", f"state after {rounds // 2} rounds")):
+        n_req = int((sn["inst"]["n_run"].astype(np.int64) + sn["inst"]["n_queue"]).sum())
+        Is = len(sn["inst"])
+        k1b = 48 * Is + 16 * n_req + 8 * n_sched + 12 * Is + 16 * cs["pieces"]
+        k3b = 12 * Is + 16 * cs["pieces"]
+        kern = {"k1": roof("hbm", "K1c", k1b, k_ms[0], hbm, None, basis="as the C5 line"),
+                "k2": roof("smem", "k2_cells_phase", cs["cells"] * len(sn["freq"]) * per_row, k_ms[1], lds_peak,
+                           None, basis=f"{per_row} B per evaluated row"),
+                "k3": roof("hbm", "K3c", k3b, k_ms[2], hbm, None, basis="as the C5 line")}
+        snaps_out.append({"state": tag, "per_kernel": kern, "counts": dict(cs, instances=Is, requests=n_req)})
+    dom = max(snaps_out[0]["per_kernel"], key=lambda k: snaps_out[0]["per_kernel"][k]["ms"])
+    roofline = dict(snaps_out[0]["per_kernel"][dom], dominant=dom, snapshots=snaps_out)
+    cpu = None
+    if world == 1 and not args.no_cpu_baseline:
+        cpu = cpu_baseline(cfg, blob, snaps[0], search=args.search)
+        cpu["sample"] += " (instances of the replay's initial state)"
+    t_ms = float(tot[0])
     line = {
-        "metric": METRIC, "value": I * args.steps / (float(tot[0]) / 1e3), "unit": "decisions/s",
-        "n_gpus": world, "steps": args.steps, "warmup": max(args.warmup, 3),
-        "ms_per_step": float(tot[0]) / args.steps, "higher_is_better": True, "scaling": "strong",
+        "metric": METRIC, "value": I * world * rounds / (t_ms / 1e3), "unit": "decisions/s",
+        "n_gpus": world, "steps": rounds, "warmup": max(args.warmup, 3),
+        "ms_per_step": t_ms / rounds, "higher_is_better": True, "scaling": "strong",
         "vs_baseline": None, "dtype": "f32", "data": "synthetic",
-        "config": {"workload": DESCR["C4"], "name": "C4", "instances": I, "requests": rc.n_requests,
+        "config": {"workload": DESCR["C4"], "name": "C4", "instances": rc.n_inst, "requests": rc.n_requests,
                    "span_s": rc.span_s, "trees": cfg.n_trees, "depth": cfg.depth, "F": cfg.F, "H": cfg.H,
-                   "step": "decide all instances + advance all instances one iteration (GPU-resident replay)",
+                   "step": "one round: decide all instances + advance all instances one engine iteration "
+                           "(GPU-resident replay)",
+                   "timed": f"the whole replay: {rounds} rounds"
+                            + (" until drained" if drained else
+                               f" until every arrival was consumed and completions stopped for 500 rounds "
+                               f"({blocked} requests blocked for good by their instance's KV capacity)"
+                               if rounds < cap else f" (cap {cap}, not drained)"),
                    "admission": (f"full admission control (checks 1-3 at f_max, lost marking), q_max={args.admission}"
                                  if args.admission else "check 1 + batch cap gate"),
                    "search": args.search,
-                   "l2": "not flushed: the replay state (~20 MB) is re-used every round by design"},
-        "decisions_per_sec_decide_only": I * args.steps / (float(tot[1]) / 1e3),
-        "per_round_ms": {"decide": dec_ms / args.steps, "advance": adv_ms / args.steps},
-        "replay_stats_after_warmup_and_steps": st,
+                   "l2": "not flushed: the replay state (~60 MB) is re-used every round by design"},
+        "drained": drained,
+        "blocked_requests_at_end": blocked,
+        "round_ms_pctl": {"p10": float(np.percentile(round_ms, 10)), "p50": float(np.percentile(round_ms, 50)),
+                          "p90": float(np.percentile(round_ms, 90)), "max": float(round_ms.max())},
+        "replay_stats": stats,
+        "roofline": roofline,
+        "cpu_baseline": cpu,
+        "e2e": {"value": I * world * rounds2 / (float(tot[1]) / 1e3), "unit": "decisions/s",
+                "h2d_bytes_per_step": rp.host_bytes() / max(rounds2, 1), "d2h_bytes_per_step": 8 * I,
+                "api": "Replay.reset (trace + state uploaded from pinned host memory, timed) + every round "
+                       "tp_decide + tp_replay_advance + (level, status) read back to pinned host memory",
+                "rounds": rounds2},
+        # per round: K1c (+ its hand-over kernel at large batches), the K2 phases, K3c, the advance
         "gpu_launches": (None if args.admission else
-                         (3 + k2_phases(model.info()) + int((i1 - i0) * 2 > sms * 32)) * args.steps),
+                         (3 + k2_phases(info) + int(I * 2 > sms * 32)) * rounds),
         "clocks": clk,
     }
     print(json.dumps(line), flush=True)
@@ -286,6 +400,8 @@ def main():
                     help="override the workload's global instance count (tests; the line says so)")
     ap.add_argument("--dump-decisions", default=None,
                     help="rank 0 writes the gathered [2, I] (level, status) rows of the last step (.npy)")
+    ap.add_argument("--replay-cap", type=int, default=6000,
+                    help="C4: at most this many rounds (the replay normally drains before)")
     ap.add_argument("--admission", type=int, default=0,
                     help="C4 replay: run the paper's full admission control on up to N queued requests per instance")
     ap.add_argument("--search", default="exhaustive", choices=["exhaustive", "binary"],

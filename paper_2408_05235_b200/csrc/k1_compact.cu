@@ -17,7 +17,6 @@
 // (S a power of two >= 4); segments are padded by P = 4 words when S/4 is even so that 8
 // consecutive lanes' 128-bit accesses fall in distinct bank quads.
 #include <algorithm>
-#include <cstdio>
 #include <cstdlib>
 
 #include "tp_internal.cuh"
@@ -130,6 +129,12 @@ struct Group {
     }
 };
 
+// Admission-control mode: the number of queued requests forced in (tp_decide_admit's prefix
+// states), or -1 for the FIFO gate.
+__device__ __forceinline__ int forced_of(const K1cParams& p, int i, int nq) {
+    return p.force_adm ? min(max(p.force_adm[i], 0), nq) : -1;
+}
+
 // First claimant of a cell appends it to the cell list K2 evaluates (cell_count holds count - 1)
 // and zeroes its clamp mask.
 __device__ __forceinline__ void claim_cell(const K1cParams& p, uint32_t k) {
@@ -164,11 +169,7 @@ __device__ __forceinline__ void piece_deadlines(const K1cParams& p, Group<WPI>& 
     const size_t row = (size_t)i * p.H;
     const int C = (nn + 31) >> 5;
     long long* D = base + C;                         // behind meta[C] (8 bytes each)
-#ifdef TP_K1C_NOSMD
-    const bool sm = false;
-#else
     const bool sm = 2 * (C + h) <= words;
-#endif
     grp.sync();                                      // meta written by the whole group
     for (int k = gl; k < h; k += GL) {
         if (sm) D[k] = kNoDeadline;
@@ -629,21 +630,34 @@ k1_packed(const __grid_constant__ K1cParams p) {
         }
         continue;
     }
-#ifdef TP_K1C_FENCE
-    __threadfence_block();
-#endif
-    K1P_SYNC();
-#ifdef TP_K1C_DEBUG
-    {
-        int s0 = 0;
-        for (int k = lane; k < p.arr; k += 32) s0 += (k >= 1 && sv[k] != 0 && k < 2) ? 1 : 0;
-        if (lane == 0 && sv[0] != 0) printf("sv0 nonzero before m1 term: i=%d sv0=%d blk=%d w=%d\n", i, sv[0], (int)blockIdx.x, w);
-        if (lane == 0) {
-            const int old = atomicExch(&p.end_n[i], -7);
-            if (old == -7) printf("duplicate grab i=%d blk=%d w=%d\n", i, (int)blockIdx.x, w);
+    // Whole-queue admission: when the footprint of running + queued fits the capacity and the
+    // whole queue fits the batch cap, every FIFO candidate passes check 1 -- for any admitted
+    // prefix, max_m KV[m] <= sum of the requests' final block counts = foot <= kv_cap, and
+    // B[1] + c <= b1 + nq <= max_batch -- so the gate admits the whole queue: its requests go into
+    // the histogram with the running ones (one scan, no per-candidate window passes).  Same
+    // result as the one-at-a-time gate below, which handles every other case.
+    const bool allq = nq > 0 && forced_of(p, i, nq) < 0 && foot <= in.kv_cap && b1 + nq <= in.max_batch;
+    if (allq) {
+        int bq = 0, kvq = 0, lq = 0;
+        bool lostq = false;
+        for (int e = nr + lane; e < nr + nq; e += 32) {
+            const int4 r = __ldg(&p.req[rb + e]);     // a = 0 (validated)
+            const int q = r.y, l = r.z;
+            const int kv_end = (int)fdN.div((uint32_t)(q + l - 2)) + 1;
+            const int c1 = (int)fdN.div((uint32_t)(q - 1));
+            kvq += c1 + 1;
+            ++bq;
+            lq = max(lq, l);
+            lostq |= (r.w & TP_REQ_LOST) != 0;
+            for (int m = 2 + (c1 + 1) * N - q; m <= l; m += N) atomicAdd(&sv[ph(m)], 1);
+            atomicAdd(&sv[ph(l + 1)], -(65536 + kv_end));
         }
+        b1 += __reduce_add_sync(kFull, bq);
+        kv1 += __reduce_add_sync(kFull, kvq);
+        nloc = max(nloc, warp_max(lq));
+        lost |= __any_sync(kFull, lostq);
     }
-#endif
+    K1P_SYNC();
     if (lane == 0) sv[0] += b1 * 65536 + kv1;     // the m = 1 terms (index 0 gets no other event)
     K1P_SYNC();
 
@@ -675,20 +689,17 @@ k1_packed(const __grid_constant__ K1cParams p) {
         }
     }
     K1P_SYNC();
-#ifdef TP_K1C_DEBUG
-    for (int m = 1 + lane; m <= nloc; m += 32)
-        if (sv[ph(m)] < 0) printf("after scan neg: i=%d m=%d v=%d nloc=%d blk=%d w=%d\n", i, m, sv[ph(m)], nloc, (int)blockIdx.x, w);
-    if (lane == 0 && i < 4) printf("grab i=%d blk=%d w=%d nr=%d nloc=%d\n", i, (int)blockIdx.x, w, nr, nloc);
-#endif
     int kvb = warp_max(kvmax);
     uint32_t st = kvb > in.kv_cap ? TP_ST_KV_OVER : 0u;
 
     // ---- FIFO gate (as k1_compact: one candidate at a time over its window, exact bound shortcut) ----
-    int n_adm = 0;
-    const int forced = p.force_adm ? min(max(p.force_adm[i], 0), nq) : -1;
+    int n_adm = allq ? nq : 0;
+    const int forced = forced_of(p, i, nq);
     const uint32_t lmask = p.lost_mask ? p.lost_mask[i] : 0u;
-    const int ncand = forced >= 0 ? forced : nq;
-    if (forced < 0 && ncand > 0 && (st & TP_ST_KV_OVER)) {
+    const int ncand = allq ? 0 : forced >= 0 ? forced : nq;
+    if (allq) {
+        // the whole queue is in the histogram already
+    } else if (forced < 0 && ncand > 0 && (st & TP_ST_KV_OVER)) {
         st |= TP_ST_QUEUE_BLOCKED;
     } else {
         int B1 = sv[0] >> 16;
@@ -768,11 +779,6 @@ k1_packed(const __grid_constant__ K1cParams p) {
         if (m <= nn) {
             const int v = sv[ph(m)];
             b = v >> 16;
-#ifdef TP_K1C_DEBUG
-            if (b < 0)
-                printf("k1_packed neg B: i=%d m=%d nn=%d n=%d v=%d nr=%d nq=%d nadm=%d blk=%d w=%d\n", i, m, nn, n, v,
-                       nr, nq, n_adm, (int)blockIdx.x, w);
-#endif
             // b < 2^15, kv < 2^16 here (the packed check): the clamped table lookups are exact
             k = cell_base + (uint32_t)__ldg(tB + (uint32_t)min(b, lB1)) * nk1 +
                 __ldg(tKV + (uint32_t)min(v & 0xFFFF, lKV1));
@@ -793,7 +799,7 @@ k1_packed(const __grid_constant__ K1cParams p) {
             const int pos = h + __popc(mask & ltm);
             rec_m[pos] = m;
             rec_k[pos] = k;
-            claim_cell(p, k);
+            if (k != pk) claim_cell(p, k);            // (a piece cut only at an end repeats the cell)
         }
         if (lane == 0) meta[(m0 - 1) >> 5] = make_int2((int)mask, h);
         h += __popc(mask);
@@ -804,9 +810,7 @@ k1_packed(const __grid_constant__ K1cParams p) {
     }
     Group<1> g1;
     g1.bar = w + 1;
-#ifndef TP_K1C_NOPD
     piece_deadlines<1>(p, g1, i, in, rb, nr + n_adm, nn, h, meta, reinterpret_cast<long long*>(sv), p.arr, lane);
-#endif
 #if TP_K1P_PERSIST
     }
 #else

@@ -12,6 +12,12 @@ from . import tp
 from . import workload as W
 
 
+def _pin(a, dtype=None):
+    a = np.ascontiguousarray(a if dtype is None else a.astype(dtype))
+    t = torch.from_numpy(a.view(np.uint8).reshape(-1) if a.dtype.fields is not None else a)
+    return t.pin_memory()
+
+
 def _dev(a, dev, dtype=None):
     a = np.ascontiguousarray(a)
     if a.dtype.fields is not None:
@@ -27,6 +33,10 @@ class Replay:
         """admission = q_max > 0: each round runs the paper's full admission control (tp_decide_admit)
         on at most q_max queued requests per instance before the throttle."""
         dev = torch.device(device)
+        # pinned host copies of the initial state and the arrival stream (reset() uploads them)
+        self.host = {k: _pin(data[k], np.float64 if k in ("t_dead", "arr_t", "arr_dead") else
+                             np.int64 if k == "arr_off" else None)
+                     for k in ("inst", "req", "t_dead", "arr_t", "arr_req", "arr_dead", "arr_off")}
         self.dev, self.model = dev, model
         self.I = len(data["inst"])
         self.cap = int(data["slot_cap"])
@@ -56,6 +66,29 @@ class Replay:
             self.adm_lost = torch.zeros(self.I, dtype=torch.int32, device=dev)
         self.cur = 0
         self.rounds = 0
+
+    def reset(self, stream=None):
+        """Back to the initial state: host -> device copies of the state and the arrival stream
+        (pinned, asynchronous on ``stream``), counters cleared."""
+        st = stream if stream is not None else torch.cuda.current_stream(self.dev)
+        with torch.cuda.stream(st):
+            self.inst.copy_(self.host["inst"], non_blocking=True)
+            self.req[0].copy_(self.host["req"], non_blocking=True)
+            self.t_dead[0].copy_(self.host["t_dead"], non_blocking=True)
+            self.arr_t.copy_(self.host["arr_t"], non_blocking=True)
+            self.arr_req.copy_(self.host["arr_req"], non_blocking=True)
+            self.arr_dead.copy_(self.host["arr_dead"], non_blocking=True)
+            self.arr_off.copy_(self.host["arr_off"], non_blocking=True)
+            self.arr_next.copy_(self.arr_off[:-1])
+            self.stats.zero_()
+            if self.adm_lost is not None:
+                self.adm_lost.zero_()
+        self.cur = 0
+        self.rounds = 0
+
+    def host_bytes(self) -> int:
+        """Bytes reset() copies host -> device."""
+        return int(sum(t.numel() * t.element_size() for t in self.host.values()))
 
     def decide(self, stream=None):
         if self.admission:
@@ -89,6 +122,14 @@ class Replay:
         inst = self.inst.cpu().numpy().view(W.INST_DTYPE)
         return bool((inst["n_run"] + inst["n_queue"]).sum() == 0 and
                     torch.equal(self.arr_next, self.arr_off[1:]))
+
+    def arrivals_consumed(self) -> bool:
+        return bool(torch.equal(self.arr_next, self.arr_off[1:]))
+
+    def in_flight(self) -> int:
+        """Requests running or queued over all instances (synchronises)."""
+        inst = self.inst.cpu().numpy().view(W.INST_DTYPE)
+        return int((inst["n_run"].astype(np.int64) + inst["n_queue"]).sum())
 
     def stats_dict(self):
         return dict(zip(self.STATS, (int(x) for x in self.stats.cpu().numpy())))
