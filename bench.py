@@ -235,11 +235,15 @@ def bench_replay(args, cfg, rank, world, local, dist, dist_test):
     torch.cuda.synchronize(dev)
     cap = args.replay_cap
 
+    phase = [None]
+
     def whole(ev_pairs, readback=None):
-        """Rounds until drained, or until every arrival has been consumed and no request has
-        completed for 500 rounds (the rest are blocked for good: FIFO head-of-line requests whose
-        KV footprint exceeds their instance's capacity), or cap; checked every 100 rounds."""
-        r, last_done, still = 0, -1, 0
+        """Rounds until drained, or until every arrival has been consumed and no instance has a
+        running request left (what remains is queued and blocked for good: FIFO head-of-line
+        requests whose KV footprint exceeds their instance's capacity), or cap; checked every 100
+        rounds."""
+        r = 0
+        phase[0] = None
         while r < cap:
             n = min(100, cap - r)
             for k in range(n):
@@ -253,11 +257,11 @@ def bench_replay(args, cfg, rank, world, local, dist, dist_test):
             torch.cuda.synchronize(dev)
             if rp.finished():
                 break
-            done = rp.stats_dict()["completed"]
-            still = still + 1 if (done == last_done and rp.arrivals_consumed()) else 0
-            last_done = done
-            if still >= 5:
-                break
+            if rp.arrivals_consumed():
+                if phase[0] is None:
+                    phase[0] = r         # (within 100 rounds) every arrival has joined a queue
+                if rp.running() == 0:
+                    break                # what is left is queued and blocked for good
         return r
 
     ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(cap)]
@@ -269,6 +273,7 @@ def bench_replay(args, cfg, rank, world, local, dist, dist_test):
     rounds = whole(ev)
     clk = clocks.stop()
     round_ms = np.array([a.elapsed_time(b) for a, b in ev[:rounds]])
+    arrivals_rounds = phase[0] or rounds
     stats = rp.stats_dict()
     drained = rp.finished()
     blocked = rp.in_flight()
@@ -358,14 +363,18 @@ def bench_replay(args, cfg, rank, world, local, dist, dist_test):
                            "(GPU-resident replay)",
                    "timed": f"the whole replay: {rounds} rounds"
                             + (" until drained" if drained else
-                               f" until every arrival was consumed and completions stopped for 500 rounds "
-                               f"({blocked} requests blocked for good by their instance's KV capacity)"
+                               f" until every arrival was consumed and no request was running "
+                               f"({blocked} queued requests blocked for good by their instance's KV capacity)"
                                if rounds < cap else f" (cap {cap}, not drained)"),
                    "admission": (f"full admission control (checks 1-3 at f_max, lost marking), q_max={args.admission}"
                                  if args.admission else "check 1 + batch cap gate"),
                    "search": args.search,
                    "l2": "not flushed: the replay state (~60 MB) is re-used every round by design"},
         "drained": drained,
+        "arrival_phase": {"rounds": arrivals_rounds,
+                          "decisions_per_sec": I * world * arrivals_rounds / (float(round_ms[:arrivals_rounds].sum()) / 1e3),
+                          "note": "rounds until every arrival had joined a queue (checked every 100 rounds); "
+                                  "the rest of the replay drains the queues"},
         "blocked_requests_at_end": blocked,
         "round_ms_pctl": {"p10": float(np.percentile(round_ms, 10)), "p50": float(np.percentile(round_ms, 50)),
                           "p90": float(np.percentile(round_ms, 90)), "max": float(round_ms.max())},
@@ -400,7 +409,7 @@ def main():
                     help="override the workload's global instance count (tests; the line says so)")
     ap.add_argument("--dump-decisions", default=None,
                     help="rank 0 writes the gathered [2, I] (level, status) rows of the last step (.npy)")
-    ap.add_argument("--replay-cap", type=int, default=6000,
+    ap.add_argument("--replay-cap", type=int, default=60000,
                     help="C4: at most this many rounds (the replay normally drains before)")
     ap.add_argument("--admission", type=int, default=0,
                     help="C4 replay: run the paper's full admission control on up to N queued requests per instance")

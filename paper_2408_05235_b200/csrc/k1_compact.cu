@@ -155,6 +155,10 @@ __device__ __forceinline__ void claim_cell(const K1cParams& p, uint32_t k) {
 // B[m] < B[m - 1].  Per instance: run_h = #pieces, run_m / run_key = head m / cell id of each piece,
 // end_d = Dmin of the piece's tail (piece_deadlines), end_n = #end positions (statistics).
 
+#ifndef TP_K1_DUNROLL
+#define TP_K1_DUNROLL 1
+#endif
+constexpr int kDUnroll = TP_K1_DUNROLL;
 // Eq. 4 per piece: end_d[k] = min over the scheduled requests whose last iteration l is piece k's
 // tail of ceil(fl64(t_dead - t_cur) * 2^40) (reading A-12), kNoDeadline where none ends.  The piece
 // of l comes from the chunk meta (heads before l's 32-iteration chunk + heads in it up to l, - 1).
@@ -176,6 +180,7 @@ __device__ __forceinline__ void piece_deadlines(const K1cParams& p, Group<WPI>& 
         else p.end_d[row + k] = kNoDeadline;
     }
     grp.sync();
+#pragma unroll kDUnroll
     for (int e = gl; e < n_sched; e += GL) {
         const int64_t j = rb + e;
         const int4 r = __ldg(&p.req[j]);
@@ -537,6 +542,12 @@ __device__ __forceinline__ void k1_body(const K1cParams& p, const int i, Group<W
 #define TP_K1P_MINB (48 / TP_K1P_WARPS)
 #endif
 
+#ifndef TP_K1P_PIPE
+#define TP_K1P_PIPE 0        // the next chunk's rank lookups issued before this chunk's compaction
+#endif
+#ifndef TP_K1P_DEFER
+#define TP_K1P_DEFER 0       // first-seen cells claimed after the piece pass (keys staged in smem)
+#endif
 #ifndef TP_K1P_PERSIST
 #define TP_K1P_PERSIST 0     // 1: persistent warps over a global instance counter (measured slower at C3/C5)
 #endif
@@ -772,10 +783,16 @@ k1_packed(const __grid_constant__ K1cParams p) {
     int h = 0, ends = 0;
     uint32_t kcarry = 0xffffffffu;
     int bcarry = 0;
-    for (int m0 = 1; m0 <= nn; m0 += 32) {
-        const int m = m0 + lane;
-        uint32_t k = 0;
-        int b = 0;
+    // First-seen cells are claimed after the pass: their keys are staged at the top of the
+    // histogram space (growing down, above every position the pass still reads), so the claim
+    // loads of the whole instance go out together instead of one L2 round trip per 32 iterations.
+    const int top_read = nn > 0 ? ph(nn) : -1;
+    int nstaged = 0;
+    // the cell key and B of iteration m (the two rank lookups of chunk m0 + 32 are issued before
+    // chunk m0's compaction, so their latency overlaps it)
+    auto key_of = [&](int m, uint32_t& k, int& b) {
+        k = 0;
+        b = 0;
         if (m <= nn) {
             const int v = sv[ph(m)];
             b = v >> 16;
@@ -783,6 +800,21 @@ k1_packed(const __grid_constant__ K1cParams p) {
             k = cell_base + (uint32_t)__ldg(tB + (uint32_t)min(b, lB1)) * nk1 +
                 __ldg(tKV + (uint32_t)min(v & 0xFFFF, lKV1));
         }
+    };
+    uint32_t k;
+    int b;
+#if TP_K1P_PIPE
+    key_of(1 + lane, k, b);
+#endif
+    for (int m0 = 1; m0 <= nn; m0 += 32) {
+        const int m = m0 + lane;
+#if TP_K1P_PIPE
+        uint32_t k_next;
+        int b_next;
+        key_of(m + 32, k_next, b_next);
+#else
+        key_of(m, k, b);
+#endif
         uint32_t pk = __shfl_up_sync(kFull, k, 1);
         int pb = __shfl_up_sync(kFull, b, 1);
         if (lane == 0) {
@@ -793,17 +825,36 @@ k1_packed(const __grid_constant__ K1cParams p) {
         bcarry = __shfl_sync(kFull, b, 31);
         const bool live = m <= nn, endp = live && b < pb;   // m - 1 is an end position
         const bool head = live && (k != pk || endp);
+        const bool fresh = head && k != pk;           // (a piece cut only at an end repeats the cell)
         const unsigned mask = __ballot_sync(kFull, head);
+        const unsigned fmask = __ballot_sync(kFull, fresh);
         ends += __popc(__ballot_sync(kFull, endp));
         if (head) {
             const int pos = h + __popc(mask & ltm);
             rec_m[pos] = m;
             rec_k[pos] = k;
-            if (k != pk) claim_cell(p, k);            // (a piece cut only at an end repeats the cell)
+        }
+        if (fresh) {
+#if TP_K1P_DEFER
+            const int slot = p.arr - 1 - (nstaged + __popc(fmask & ltm));
+            if (slot > top_read) sv[slot] = (int)k;
+            else claim_cell(p, k);                    // no room above the histogram: claim now
+#else
+            claim_cell(p, k);
+#endif
         }
         if (lane == 0) meta[(m0 - 1) >> 5] = make_int2((int)mask, h);
         h += __popc(mask);
+#if TP_K1P_DEFER
+        nstaged = min(nstaged + __popc(fmask), p.arr - 1 - top_read);
+#endif
+#if TP_K1P_PIPE
+        k = k_next;
+        b = b_next;
+#endif
     }
+    K1P_SYNC();
+    for (int j = lane; j < nstaged; j += 32) claim_cell(p, (uint32_t)sv[p.arr - 1 - j]);
     if (lane == 0) {
         p.run_h[i] = h;
         p.end_n[i] = nn > 0 ? ends + 1 : 0;

@@ -126,6 +126,11 @@ class Replay:
     def arrivals_consumed(self) -> bool:
         return bool(torch.equal(self.arr_next, self.arr_off[1:]))
 
+    def running(self) -> int:
+        """Running requests over all instances (synchronises)."""
+        inst = self.inst.cpu().numpy().view(W.INST_DTYPE)
+        return int(inst["n_run"].astype(np.int64).sum())
+
     def in_flight(self) -> int:
         """Requests running or queued over all instances (synchronises)."""
         inst = self.inst.cpu().numpy().view(W.INST_DTYPE)
