@@ -386,9 +386,10 @@ def bench_replay(args, cfg, rank, world, local, dist, dist_test):
                 "api": "Replay.reset (trace + state uploaded from pinned host memory, timed) + every round "
                        "tp_decide + tp_replay_advance + (level, status) read back to pinned host memory",
                 "rounds": rounds2},
-        # per round: K1c (+ its hand-over kernel at large batches), the K2 phases, K3c, the advance
+        # per round: K1c (+ its hand-over kernel at large batches), the cell-list collector, the K2
+        # phases, K3c, the advance
         "gpu_launches": (None if args.admission else
-                         (3 + k2_phases(info) + int(I * 2 > sms * 32)) * rounds),
+                         (4 + k2_phases(info) + int(I * 2 > sms * 32)) * rounds),
         "clocks": clk,
     }
     print(json.dumps(line), flush=True)
@@ -675,8 +676,9 @@ def main():
         "cpu_baseline": cpu,
         "e2e": e2e,
         # our kernels per step: K1c (k1_packed + the hand-over k1_compact<1,1> at one warp per
-        # instance, i.e. when the batch exceeds 16 warps per SM), the K2 phases, K3c
-        "gpu_launches": (2 + k2_phases(info) + int(I * 2 > sms * 32)) * args.steps,
+        # instance, i.e. when the batch exceeds 16 warps per SM), the cell-list collector, the K2
+        # phases, K3c
+        "gpu_launches": (3 + k2_phases(info) + int(I * 2 > sms * 32)) * args.steps,
         "clocks": clk,
         "dist": dist_info,
         "paper_context": "paper controller on host CPU (A100 box): projection <2 ms, model ~3 ms per call, "

@@ -74,7 +74,8 @@ struct K1cParams {
     int32_t* end_n;
     long long* end_d;
     int32_t tick_shift;      // Dmin in units of 2^tick_shift ticks (K2Params::tick_shift)
-    int32_t* next;           // k1_packed's persistent warps: next instance (count - 1)
+    int32_t* next;           // (unused by K1c; reset with K3c's counters)
+    int32_t tab_words;       // k1_packed<true>: 32-bit words of the rank tables staged in shared memory
     int32_t* flag_count;     // k1_packed -> wide fallback hand-over (count - 1)
     int32_t* flag_list;
 };
@@ -135,15 +136,13 @@ __device__ __forceinline__ int forced_of(const K1cParams& p, int i, int nq) {
     return p.force_adm ? min(max(p.force_adm[i], 0), nq) : -1;
 }
 
-// First claimant of a cell appends it to the cell list K2 evaluates (cell_count holds count - 1)
-// and zeroes its clamp mask.
+// A piece's cell is marked SEEN in the dense cell table: cell_tab[k] &= 0x7fffffff, a fire-and-
+// forget reduction (no L2 round trip on the warp's path, idempotent, and a cell already listed --
+// index >= 0 -- keeps its index).  -1 (absent, the launch's memset) becomes kCellSeen; after K1c,
+// k1_cells_collect appends every seen cell to the list K2 evaluates and gives it its index.
+constexpr int32_t kCellSeen = 0x7fffffff;
 __device__ __forceinline__ void claim_cell(const K1cParams& p, uint32_t k) {
-    if (__ldcg(p.cell_tab + k) == -1 && atomicCAS(p.cell_tab + k, -1, -2) == -1) {
-        const int idx = atomicAdd(p.cell_count, 1) + 1;
-        p.cell_list[idx] = k;
-        p.cell_clamp[k] = 0u;
-        p.cell_tab[k] = idx;
-    }
+    atomicAnd(ptr_at(reinterpret_cast<unsigned*>(p.cell_tab), k), (unsigned)kCellSeen);
 }
 
 // piece_rules.  K3c accumulates T_R (Eq. 3) piece by piece and checks Eq. 4 at
@@ -536,52 +535,73 @@ __device__ __forceinline__ void k1_body(const K1cParams& p, const int i, Group<W
 // Eq. 4 table is built in windows of the histogram space.  Instances the check rejects are handed
 // to k1_compact<1, true> through the flag list.
 #ifndef TP_K1P_WARPS
-#define TP_K1P_WARPS 4       // warps (instances in flight) per CTA
+#define TP_K1P_WARPS 14      // warps (instances in flight) per CTA (named barriers 1..15)
 #endif
 #ifndef TP_K1P_MINB
-#define TP_K1P_MINB (48 / TP_K1P_WARPS)
+#define TP_K1P_MINB 3        // CTAs per SM: 3 x (14 x 4.6 KB + 9 KB of tables) at H = 1024
 #endif
 
-#ifndef TP_K1P_PIPE
-#define TP_K1P_PIPE 0        // the next chunk's rank lookups issued before this chunk's compaction
-#endif
-#ifndef TP_K1P_DEFER
-#define TP_K1P_DEFER 0       // first-seen cells claimed after the piece pass (keys staged in smem)
-#endif
-#ifndef TP_K1P_PERSIST
-#define TP_K1P_PERSIST 0     // 1: persistent warps over a global instance counter (measured slower at C3/C5)
-#endif
-// one warp's named barrier (see Group::sync)
-#define K1P_SYNC() warp_bar(w + 1)
+// one warp's named barrier (see Group::sync); the id is a register (k1_packed uses up to 15 of them
+// anyway: one per warp of its CTA), a switch over immediate ids costs ~10 instructions per barrier
+#define K1P_SYNC() asm volatile("bar.sync %0, 32;" ::"r"(w + 1) : "memory")
+// +1 at every m = m1, m1 + N, ... <= l (the block increments of one request, Eq. 1) in the padded
+// layout ph(m) = m - 1 + P * ((m - 1) >> SL); when N is a multiple of the segment length 2^SL the
+// physical stride is the constant N + P * N / 2^SL
+__device__ __forceinline__ void block_events(int* sv, int m1, int l, int N, int SL, int P) {
+    if (m1 > l) return;
+    if ((N & ((1 << SL) - 1)) == 0) {
+        const int step = N + P * (N >> SL);
+        int pi = (m1 - 1) + P * ((m1 - 1) >> SL);
+        #pragma unroll 1
+        for (int m = m1; m <= l; m += N, pi += step) atomicAdd(&sv[pi], 1);
+    } else {
+        #pragma unroll 1
+        for (int m = m1; m <= l; m += N) atomicAdd(&sv[(m - 1) + P * ((m - 1) >> SL)], 1);
+    }
+}
+// ST: the B / KV rank tables staged in shared memory (p.tab_words 32-bit words in front of the
+// warps' histograms; every lookup an LDS), else read through L1 from global memory.  Persistent:
+// the CTAs that fit at once, warp w of CTA b takes instances b * wpb + w, + gridDim.x * wpb, ...
+template <bool ST>
 __global__ void __launch_bounds__(TP_K1P_WARPS * 32, TP_K1P_MINB)
 k1_packed(const __grid_constant__ K1cParams p) {
     extern __shared__ __align__(16) int smem[];
-    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-    int* sv = smem + (size_t)w * p.arr;
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, wpb = (int)(blockDim.x >> 5);
+    int* sv = smem + (ST ? p.tab_words : 0) + (size_t)w * p.arr;
     const int lB1 = p.rtab_len[0] - 1, lKV1 = p.rtab_len[1] - 1;   // tables end past the last cut
-    const uint16_t* tB = p.rtab + p.rtab_off[0];
-    const uint16_t* tKV = p.rtab + p.rtab_off[1];
+    const uint16_t* tB;
+    const uint16_t* tKV;
+    if (lane == 0 && blockIdx.x * wpb + w < p.n_inst) {   // the first instance's request table -> L2
+        const int4 f = __ldg(reinterpret_cast<const int4*>(p.inst + blockIdx.x * wpb + w) + 1);
+        if (f.y > 0 && f.z >= 0 && f.x >= 0 && (int64_t)f.x + f.y + f.z <= (int64_t)p.n_req)
+            prefetch_l2_bulk(p.req + f.x, (uint32_t)(f.y + f.z) * 16u);
+    }
+    if constexpr (ST) {
+        for (int k = threadIdx.x; k < p.tab_words; k += blockDim.x)
+            smem[k] = __ldg(reinterpret_cast<const int*>(p.rtab) + k);
+        __syncthreads();
+        tB = reinterpret_cast<const uint16_t*>(smem) + p.rtab_off[0];
+        tKV = reinterpret_cast<const uint16_t*>(smem) + p.rtab_off[1];
+    } else {
+        tB = p.rtab + p.rtab_off[0];
+        tKV = p.rtab + p.rtab_off[1];
+    }
     const int SL = p.S_log2, S = 1 << SL, P = p.P, H = p.H;
     auto ph = [&](int m) { return (m - 1) + P * ((m - 1) >> SL); };   // physical index of m >= 1
-#if TP_K1P_PERSIST
-    // persistent warps: each takes the next instance from a global counter (instances differ a
-    // lot in length; a static assignment leaves warps idle behind the longest one of their CTA)
-    for (;;) {
-    int i = 0;
-    if (lane == 0) i = atomicAdd(p.next, 1) + 1;     // next holds count - 1 (reset by the launch's memset)
-    i = __shfl_sync(kFull, i, 0);
-    if (i >= p.n_inst) break;                         // warp-uniform
+#pragma unroll 1
+    for (int i = blockIdx.x * wpb + w; i < p.n_inst; i += gridDim.x * wpb) {
     K1P_SYNC();                                       // the previous instance's reads of sv are done
-#else
-    do {                                              // one instance per warp
-    const int i = blockIdx.x * (int)(blockDim.x >> 5) + w;
-    if (i >= p.n_inst) break;
-#endif
 
     const tp_inst in = p.inst[i];
     const int64_t rb = in.req_begin;
     const int nr = in.n_run, nq = in.n_queue, N = in.N;
     const FastDiv fdN((uint32_t)(N > 0 ? N : 1));
+    // the warp's next instance: {req_begin, n_run, n_queue, N}, for the L2 prefetch of its request
+    // table below (its loads are then L2 hits instead of HBM round trips)
+    const int inext = i + gridDim.x * wpb;
+    int4 nx = make_int4(0, 0, 0, 0);
+    if (lane == 0 && inext < p.n_inst) nx = __ldg(reinterpret_cast<const int4*>(p.inst + inext) + 1);
+    #pragma unroll 1
     for (int k = lane * 4; k + 3 < p.arr; k += 128) *reinterpret_cast<int4*>(sv + k) = make_int4(0, 0, 0, 0);
     K1P_SYNC();
 
@@ -591,6 +611,7 @@ k1_packed(const __grid_constant__ K1cParams p) {
     int nloc = 0, b1 = 0, kv1 = 0;
     bool lost = false;
     if (!bad) {
+        #pragma unroll 1
         for (int e = lane; e < nr + nq; e += 32) {
             const int4 r = __ldg(&p.req[rb + e]);
             const int64_t l64 = (int64_t)r.z - r.x;
@@ -608,7 +629,7 @@ k1_packed(const __grid_constant__ K1cParams p) {
                 const int c1 = (int)fdN.div((uint32_t)(aq - 1));                    // ceil(aq / N) - 1
                 kv1 += c1 + 1;
                 ++b1;
-                for (int m = 2 + (c1 + 1) * N - aq; m <= l; m += N) atomicAdd(&sv[ph(m)], 1);
+                block_events(sv, 2 + (c1 + 1) * N - aq, l, N, SL, P);
                 atomicAdd(&sv[ph(l + 1)], -(65536 + kv_end));                       // B -1 and KV -kv_end
             }
         }
@@ -627,6 +648,7 @@ k1_packed(const __grid_constant__ K1cParams p) {
     if (bad) {
         if (p.B) {
             const int lim = p.bkv_rows ? H : 1;
+            #pragma unroll 1
             for (int m = lane; m < lim; m += 32) {
                 p.B[(int64_t)i * H + m] = 0;
                 p.KV[(int64_t)i * H + m] = 0;
@@ -651,6 +673,7 @@ k1_packed(const __grid_constant__ K1cParams p) {
     if (allq) {
         int bq = 0, kvq = 0, lq = 0;
         bool lostq = false;
+        #pragma unroll 1
         for (int e = nr + lane; e < nr + nq; e += 32) {
             const int4 r = __ldg(&p.req[rb + e]);     // a = 0 (validated)
             const int q = r.y, l = r.z;
@@ -660,7 +683,7 @@ k1_packed(const __grid_constant__ K1cParams p) {
             ++bq;
             lq = max(lq, l);
             lostq |= (r.w & TP_REQ_LOST) != 0;
-            for (int m = 2 + (c1 + 1) * N - q; m <= l; m += N) atomicAdd(&sv[ph(m)], 1);
+            block_events(sv, 2 + (c1 + 1) * N - q, l, N, SL, P);
             atomicAdd(&sv[ph(l + 1)], -(65536 + kv_end));
         }
         b1 += __reduce_add_sync(kFull, bq);
@@ -674,10 +697,10 @@ k1_packed(const __grid_constant__ K1cParams p) {
 
     // ---- inclusive scan of the packed words over the lane segments ----
     int* seg = sv + lane * (S + P);
-    const int lo = 1 + lane * S;
     int kvmax = 0;
     {
         int sum = 0;
+        #pragma unroll 1
         for (int k = 0; k < S; k += 4) {
             const int4 v = *reinterpret_cast<const int4*>(seg + k);
             sum += v.x + v.y + v.z + v.w;
@@ -689,17 +712,23 @@ k1_packed(const __grid_constant__ K1cParams p) {
             if (lane >= o) x += y;
         }
         int pre = x - sum;
+        #pragma unroll 1
         for (int k = 0; k < S; k += 4) {
             int4 v = *reinterpret_cast<const int4*>(seg + k);
             v.x += pre; v.y += v.x; v.z += v.y; v.w += v.z;
             pre = v.w;
             *reinterpret_cast<int4*>(seg + k) = v;
-            const int m = lo + k;
-            kvmax = max(kvmax, max(max(m <= H ? (v.x & 0xFFFF) : 0, m + 1 <= H ? (v.y & 0xFFFF) : 0),
-                                   max(m + 2 <= H ? (v.z & 0xFFFF) : 0, m + 3 <= H ? (v.w & 0xFFFF) : 0)));
+            // KV[m] = 0 past every request's last iteration, so positions past H need no mask
+            kvmax = max(kvmax, max(max(v.x & 0xFFFF, v.y & 0xFFFF), max(v.z & 0xFFFF, v.w & 0xFFFF)));
         }
     }
     K1P_SYNC();
+    if (lane == 0 && nx.y > 0 && nx.z >= 0 && nx.x >= 0 && (int64_t)nx.x + nx.y + nx.z <= (int64_t)p.n_req) {
+        const int64_t e0 = nx.x, e1 = e0 + nx.y + nx.z;
+        prefetch_l2_bulk(p.req + e0, (uint32_t)(e1 - e0) * 16u);
+        const int64_t d0 = e0 & ~1LL, d1 = min((e1 + 1) & ~1LL, (int64_t)p.n_req & ~1LL);   // 16-byte units
+        if (d1 > d0) prefetch_l2_bulk(p.t_dead + d0, (uint32_t)(d1 - d0) * 8u);
+    }
     int kvb = warp_max(kvmax);
     uint32_t st = kvb > in.kv_cap ? TP_ST_KV_OVER : 0u;
 
@@ -714,6 +743,7 @@ k1_packed(const __grid_constant__ K1cParams p) {
         st |= TP_ST_QUEUE_BLOCKED;
     } else {
         int B1 = sv[0] >> 16;
+        #pragma unroll 1
         for (int c = 0; c < ncand; ++c) {
             const int4 r = __ldg(&p.req[rb + nr + c]);
             const int q = r.y, lc = r.z;
@@ -722,7 +752,7 @@ k1_packed(const __grid_constant__ K1cParams p) {
                 bool admit = B1 + 1 <= in.max_batch;
                 if (admit && kvb + kvc_top > in.kv_cap) {
                     int mx = 0;
-#pragma unroll 4
+#pragma unroll 1
                     for (int m = 1 + lane; m <= lc; m += 32)
                         mx = max(mx, (sv[ph(m)] & 0xFFFF) + (int)fdN.div((uint32_t)(m + q - 2)) + 1);
                     mx = warp_max(mx);
@@ -738,7 +768,7 @@ k1_packed(const __grid_constant__ K1cParams p) {
             } else {
                 kvb += kvc_top;
             }
-#pragma unroll 4
+#pragma unroll 1
             for (int m = 1 + lane; m <= lc; m += 32) sv[ph(m)] += 65536 + (int)fdN.div((uint32_t)(m + q - 2)) + 1;
             K1P_SYNC();
             ++B1;
@@ -757,6 +787,7 @@ k1_packed(const __grid_constant__ K1cParams p) {
         int* Bo = p.B + (int64_t)i * H;
         int* Ko = p.KV + (int64_t)i * H;
         const int lim = p.bkv_rows ? H : 1;
+        #pragma unroll 1
         for (int m = 1 + lane; m <= lim; m += 32) {
             const int v = sv[ph(m)];
             Bo[m - 1] = v >> 16;
@@ -769,104 +800,115 @@ k1_packed(const __grid_constant__ K1cParams p) {
         p.status[i] = st;
     }
     const int nn = (st & p.skip) ? 0 : n;
-    const unsigned ltm = (1u << lane) - 1u;
     const size_t row = (size_t)i * H;
 
-    // ---- pieces (piece_rules), records straight from the ballot compaction, claims ----
-    const int nKV = p.cut_off[3] - p.cut_off[2];
-    const uint32_t rtp = rank_of(p.cuts + p.cut_off[0], p.cut_off[1] - p.cut_off[0], (float)in.tp);
-    const uint32_t nk1 = (uint32_t)nKV + 1;
-    const uint32_t cell_base = rtp * (uint32_t)(p.cut_off[2] - p.cut_off[1] + 1) * nk1;
-    int2* meta = reinterpret_cast<int2*>(sv);       // [chunk] (head mask, heads before the chunk)
-    int32_t* const rec_m = p.run_m + row;
-    uint32_t* const rec_k = p.run_key + row;
+    // ---- pieces (piece_rules) in lane segments: lane t walks m in [1 + t S2, 1 + (t+1) S2) ----
+    // Pass A: the cell key (two rank-table lookups) and the head / end flags of each m, left in
+    // place of the histogram word as key | head << 30 | fresh << 31 (keys < kMaxCells = 2^22);
+    // a warp scan of the per-lane head counts gives every lane its first piece index; pass B writes
+    // the piece records (first m, cell id), marks the fresh cells, and leaves in place of each m the
+    // index of its piece -- which is what the Eq. 4 pass below looks up at every request's end.
     int h = 0, ends = 0;
-    uint32_t kcarry = 0xffffffffu;
-    int bcarry = 0;
-    // First-seen cells are claimed after the pass: their keys are staged at the top of the
-    // histogram space (growing down, above every position the pass still reads), so the claim
-    // loads of the whole instance go out together instead of one L2 round trip per 32 iterations.
-    const int top_read = nn > 0 ? ph(nn) : -1;
-    int nstaged = 0;
-    // the cell key and B of iteration m (the two rank lookups of chunk m0 + 32 are issued before
-    // chunk m0's compaction, so their latency overlaps it)
-    auto key_of = [&](int m, uint32_t& k, int& b) {
-        k = 0;
-        b = 0;
-        if (m <= nn) {
-            const int v = sv[ph(m)];
-            b = v >> 16;
-            // b < 2^15, kv < 2^16 here (the packed check): the clamped table lookups are exact
-            k = cell_base + (uint32_t)__ldg(tB + (uint32_t)min(b, lB1)) * nk1 +
-                __ldg(tKV + (uint32_t)min(v & 0xFFFF, lKV1));
+    if (nn > 0) {
+        const int nKV = p.cut_off[3] - p.cut_off[2];
+        const uint32_t nk1 = (uint32_t)nKV + 1;
+        const uint32_t rtp = rank_of(p.cuts + p.cut_off[0], p.cut_off[1] - p.cut_off[0], (float)in.tp);
+        const uint32_t cell_base = rtp * (uint32_t)(p.cut_off[2] - p.cut_off[1] + 1) * nk1;
+        // b < 2^15, kv < 2^16 here (the packed check): the clamped table lookups are exact
+        auto key_of = [&](int v) -> uint32_t {
+            if constexpr (ST) return (uint32_t)tB[min(v >> 16, lB1)] * nk1 + tKV[min(v & 0xFFFF, lKV1)];
+            return (uint32_t)__ldg(ptr_at(tB, (unsigned)min(v >> 16, lB1))) * nk1 +
+                   __ldg(ptr_at(tKV, (unsigned)min(v & 0xFFFF, lKV1)));
+        };
+        // S2: a multiple of 4 (odd multiples preferred: conflict-free 128-bit accesses at lane stride
+        // S2), so each lane's segment starts 4-aligned and every 4-iteration batch is one aligned
+        // int4 of the padded layout (segments of the scan layout are multiples of 4 long)
+        int S2 = (((nn + 31) >> 5) + 3) & ~3;
+        if ((S2 & 4) == 0 && 32 * (S2 - 4) < nn) S2 += 4;
+        const int mlo = 1 + lane * S2, mhi = min(mlo + S2 - 1, nn);     // empty when mlo > nn
+        uint32_t pk = 0xffffffffu;                   // key / B of m - 1 (m = 1 always starts a piece)
+        int pb = 0;
+        if (mlo >= 2 && mlo <= nn) {
+            const int v = sv[ph(mlo - 1)];
+            pb = v >> 16;
+            pk = key_of(v);
         }
-    };
-    uint32_t k;
-    int b;
-#if TP_K1P_PIPE
-    key_of(1 + lane, k, b);
-#endif
-    for (int m0 = 1; m0 <= nn; m0 += 32) {
-        const int m = m0 + lane;
-#if TP_K1P_PIPE
-        uint32_t k_next;
-        int b_next;
-        key_of(m + 32, k_next, b_next);
-#else
-        key_of(m, k, b);
-#endif
-        uint32_t pk = __shfl_up_sync(kFull, k, 1);
-        int pb = __shfl_up_sync(kFull, b, 1);
-        if (lane == 0) {
-            pk = kcarry;
-            pb = bcarry;
+        K1P_SYNC();                                   // every neighbour read before the in-place writes
+        int cnt = 0, e = 0;
+        #pragma unroll 1
+        for (int m0 = mlo; m0 <= mhi; m0 += 4) {
+            int4* const q = reinterpret_cast<int4*>(sv + ph(m0));
+            int4 v = *q;
+            const uint32_t k0 = key_of(v.x), k1 = key_of(v.y), k2 = key_of(v.z), k3 = key_of(v.w);
+            auto flag = [&](int& x, uint32_t k, bool live) {     // x: the histogram word of m
+                const int b = x >> 16;
+                const bool endp = live && b < pb;     // m - 1 is an end position
+                const bool fresh = live && k != pk;   // (a piece cut only at an end repeats the cell)
+                const bool head = fresh || endp;
+                cnt += head;
+                e += endp;
+                x = (int)(k | (head ? 1u << 30 : 0u) | (fresh ? 1u << 31 : 0u));
+                pk = k;
+                pb = b;
+            };
+            flag(v.x, k0, true);
+            flag(v.y, k1, m0 + 1 <= mhi);
+            flag(v.z, k2, m0 + 2 <= mhi);
+            flag(v.w, k3, m0 + 3 <= mhi);
+            *q = v;                                   // words past nn are never read again
         }
-        kcarry = __shfl_sync(kFull, k, 31);
-        bcarry = __shfl_sync(kFull, b, 31);
-        const bool live = m <= nn, endp = live && b < pb;   // m - 1 is an end position
-        const bool head = live && (k != pk || endp);
-        const bool fresh = head && k != pk;           // (a piece cut only at an end repeats the cell)
-        const unsigned mask = __ballot_sync(kFull, head);
-        const unsigned fmask = __ballot_sync(kFull, fresh);
-        ends += __popc(__ballot_sync(kFull, endp));
-        if (head) {
-            const int pos = h + __popc(mask & ltm);
-            rec_m[pos] = m;
-            rec_k[pos] = k;
+        int x = cnt;                                  // inclusive scan of the head counts
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const int y = __shfl_up_sync(kFull, x, o);
+            if (lane >= o) x += y;
         }
-        if (fresh) {
-#if TP_K1P_DEFER
-            const int slot = p.arr - 1 - (nstaged + __popc(fmask & ltm));
-            if (slot > top_read) sv[slot] = (int)k;
-            else claim_cell(p, k);                    // no room above the histogram: claim now
-#else
-            claim_cell(p, k);
-#endif
+        h = __shfl_sync(kFull, x, 31);
+        ends = __reduce_add_sync(kFull, e);
+        int pos = x - cnt;                            // this lane's first piece
+        int32_t* const rec_m = p.run_m + row;
+        uint32_t* const rec_k = p.run_key + row;
+        #pragma unroll 1
+        for (int m0 = mlo; m0 <= mhi; m0 += 4) {
+            int4* const q = reinterpret_cast<int4*>(sv + ph(m0));
+            int4 v = *q;
+            auto piece = [&](int& x, int m) {
+                const uint32_t w = (uint32_t)x;
+                if (w & (1u << 30)) {                 // (words past mhi carry no head bit)
+                    const uint32_t k = cell_base + (w & 0x3fffffffu);
+                    *ptr_at(rec_m, (unsigned)pos) = m;
+                    *ptr_at(rec_k, (unsigned)pos) = k;
+                    if (w >> 31) claim_cell(p, k);
+                    ++pos;
+                }
+                x = pos - 1;                          // the piece of m
+            };
+            piece(v.x, m0);
+            piece(v.y, m0 + 1);
+            piece(v.z, m0 + 2);
+            piece(v.w, m0 + 3);
+            *q = v;
         }
-        if (lane == 0) meta[(m0 - 1) >> 5] = make_int2((int)mask, h);
-        h += __popc(mask);
-#if TP_K1P_DEFER
-        nstaged = min(nstaged + __popc(fmask), p.arr - 1 - top_read);
-#endif
-#if TP_K1P_PIPE
-        k = k_next;
-        b = b_next;
-#endif
+        // Eq. 4 per piece (piece_deadlines): end_d[k] = min over the scheduled requests whose last
+        // iteration l is piece k's tail of ceil(fl64(t_dead - t_cur) * 2^40) (reading A-12).
+        long long* const D = p.end_d + row;
+        #pragma unroll 1
+        for (int k = lane; k < h; k += 32) D[k] = kNoDeadline;
+        K1P_SYNC();                                   // piece indices and the initial minima in place
+        const int n_sched = nr + n_adm;
+        #pragma unroll 1
+        for (int j = lane; j < n_sched; j += 32) {
+            const int4 r = __ldg(&p.req[rb + j]);
+            const int l = r.z - r.x;                  // 1 <= l <= nn (validated; n = max l)
+            const long long d = slack_ticks(__ldg(&p.t_dead[rb + j]) - in.t_cur, p.tick_shift);
+            if (d != kNoDeadline) atomicMin(ptr_at(D, (unsigned)sv[ph(l)]), d);   // fire-and-forget RED.MIN.S64
+        }
     }
-    K1P_SYNC();
-    for (int j = lane; j < nstaged; j += 32) claim_cell(p, (uint32_t)sv[p.arr - 1 - j]);
     if (lane == 0) {
         p.run_h[i] = h;
-        p.end_n[i] = nn > 0 ? ends + 1 : 0;
+        p.end_n[i] = nn > 0 ? ends + 1 : 0;           // + m = nn, always an end
     }
-    Group<1> g1;
-    g1.bar = w + 1;
-    piece_deadlines<1>(p, g1, i, in, rb, nr + n_adm, nn, h, meta, reinterpret_cast<long long*>(sv), p.arr, lane);
-#if TP_K1P_PERSIST
     }
-#else
-    } while (0);
-#endif
 }
 
 template <int WPI, bool FLAGGED = false>   // FLAGGED: the instances k1_packed handed over
@@ -895,6 +937,27 @@ k1_compact(const __grid_constant__ K1cParams p) {
     const int i = blockIdx.x * gpb + g;
     if (i >= p.n_inst) return;                         // group-uniform
     k1_body<WPI>(p, i, grp, sB, sKV, gl, lane);
+}
+
+// After K1c: every cell marked seen (claim_cell) gets the next index of the cell list K2 evaluates
+// (cell_count holds count - 1; the order of the list is immaterial: K2 and K3c address the LUT by
+// cell id) and a zero clamp mask.  Cells listed by an earlier launch on the same workspace keep
+// their index.
+__global__ void __launch_bounds__(256) k1_cells_collect(int32_t* cell_tab, int32_t n_cells, uint32_t* cell_list,
+                                                        int32_t* cell_count, uint32_t* cell_clamp) {
+    const int k = blockIdx.x * blockDim.x + threadIdx.x, lane = threadIdx.x & 31;
+    const bool seen = k < n_cells && cell_tab[k] == kCellSeen;
+    const unsigned b = __ballot_sync(kFull, seen);
+    if (!b) return;                                    // warp-uniform
+    int base = 0;
+    if (lane == 0) base = atomicAdd(cell_count, __popc(b)) + 1;
+    base = __shfl_sync(kFull, base, 0);
+    if (seen) {
+        const int idx = base + __popc(b & ((1u << lane) - 1u));
+        cell_list[idx] = (uint32_t)k;
+        cell_tab[k] = idx;
+        cell_clamp[k] = 0u;
+    }
 }
 
 }  // namespace
@@ -952,35 +1015,39 @@ int launch_packed(const K1cParams& p0, int32_t n_inst, int32_t H, cudaStream_t s
     p.arr = g.arr;
     const size_t per_warp = (size_t)g.arr * sizeof(int);
     if (per_warp > 200 * 1024) return TP_EINVAL;
-    const int wpb = (int)std::max<size_t>(1, std::min<size_t>(TP_K1P_WARPS, (100 * 1024) / per_warp));
-    const size_t smem = (size_t)wpb * per_warp;
+    // rank tables in shared memory when they are small next to the histograms (the model's cut sets)
+    const int tab_entries = p.rtab_off[1] + p.rtab_len[1];
+    const size_t tab_bytes = ((size_t)tab_entries * 2 + 15) & ~(size_t)15;
+    constexpr size_t kCtaSmem = 75 * 1024;            // TP_K1P_MINB CTAs per SM
+    const bool st = tab_bytes <= 32 * 1024 && tab_bytes + per_warp <= kCtaSmem;
+    p.tab_words = st ? (int32_t)(tab_bytes / 4) : 0;
+    const size_t room = st ? kCtaSmem - tab_bytes : (size_t)100 * 1024;
+    const int wpb = (int)std::max<size_t>(1, std::min<size_t>(TP_K1P_WARPS, room / per_warp));
+    const size_t smem = (st ? tab_bytes : 0) + (size_t)wpb * per_warp;
     int dev = 0;
     if (cudaGetDevice(&dev) != cudaSuccess) return TP_ECUDA;
     auto go = [&](auto kern, int li) {
-        static int attr_bytes[2][64] = {}, occ_smem[2][64] = {}, occ_blocks[2][64] = {};
+        static int attr_bytes[2][64] = {}, occ_smem[2][64] = {}, occ_blocks[2][64] = {}, occ_wpb[2][64] = {};
         if (dev < 64 && attr_bytes[li][dev] < (int)smem) {
             if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess)
                 return TP_EINVAL;
             attr_bytes[li][dev] = (int)smem;
         }
-        // persistent: as many CTAs as fit at once (the warps take instances from p.next)
-        if (dev < 64 && occ_smem[li][dev] != (int)smem) {
+        // persistent: as many CTAs as fit at once
+        if (dev < 64 && (occ_smem[li][dev] != (int)smem || occ_wpb[li][dev] != wpb)) {
             int b = 0;
             cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, kern, wpb * 32, smem);
             occ_blocks[li][dev] = b > 0 ? b : 1;
             occ_smem[li][dev] = (int)smem;
+            occ_wpb[li][dev] = wpb;
         }
         int sms = 148;
         cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-#if TP_K1P_PERSIST
-        const int grid = std::min((n_inst + wpb - 1) / wpb, sms * (dev < 64 ? occ_blocks[li][dev] : 1));
-#else
-        const int grid = (n_inst + wpb - 1) / wpb;
-#endif
+        const int grid = (int)std::min<int64_t>((n_inst + wpb - 1) / wpb, (int64_t)sms * (dev < 64 ? occ_blocks[li][dev] : 1));
         kern<<<grid, wpb * 32, smem, s>>>(p);
         return cudaPeekAtLastError() == cudaSuccess ? TP_OK : TP_ECUDA;
     };
-    const int rc = go(k1_packed, 0);
+    const int rc = st ? go(k1_packed<true>, 1) : go(k1_packed<false>, 0);
     if (rc != TP_OK) return rc;
     return launch_wpi<1, true>(p0, n_inst, H, s);
 }
@@ -1040,12 +1107,18 @@ int launch_project_compact(const K2Params& w, const tp_inst* inst, int32_t n_ins
     const int64_t slots = (int64_t)sms * 32;    // C2 (1,024 instances): 4 warps each; C3: one
     const int wpi = wpi_env ? wpi_env : ((int64_t)n_inst * 4 <= slots ? 4 : (int64_t)n_inst * 2 <= slots ? 2 : 1);
     static const bool packed = env_int_k1("TP_K1C_PACKED", 1) != 0;
+    int rc;
     switch (wpi) {
-        case 8: return launch_wpi<8>(p, n_inst, H, s);
-        case 4: return launch_wpi<4>(p, n_inst, H, s);
-        case 2: return launch_wpi<2>(p, n_inst, H, s);
-        default: return packed ? launch_packed(p, n_inst, H, s) : launch_wpi<1>(p, n_inst, H, s);
+        case 8: rc = launch_wpi<8>(p, n_inst, H, s); break;
+        case 4: rc = launch_wpi<4>(p, n_inst, H, s); break;
+        case 2: rc = launch_wpi<2>(p, n_inst, H, s); break;
+        default: rc = packed ? launch_packed(p, n_inst, H, s) : launch_wpi<1>(p, n_inst, H, s); break;
     }
+    if (rc != TP_OK) return rc;
+    constexpr int kCollectThreads = 256;
+    k1_cells_collect<<<(w.n_cells + kCollectThreads - 1) / kCollectThreads, kCollectThreads, 0, s>>>(
+        w.cell_tab, w.n_cells, w.cell_list, w.cell_count, w.cell_clamp);
+    return cudaPeekAtLastError() == cudaSuccess ? TP_OK : TP_ECUDA;
 }
 
 }  // namespace tp

@@ -171,6 +171,7 @@ int load_impl(const void* host_blob, size_t nbytes, int device, tp_gbdt** out) {
             rtab.push_back((uint16_t)(std::upper_bound(c.begin(), c.end(), (float)x) - c.begin()));
     }
     rtab.push_back(0);
+    while (rtab.size() % 8) rtab.push_back(0);   // whole 16-byte words (K1c copies the tables to shared memory in 32-bit words)
 
     int prev = 0;
     if (cudaGetDevice(&prev) != cudaSuccess || cudaSetDevice(device) != cudaSuccess) {

@@ -160,8 +160,8 @@ cudaError_t launch_pdl(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t sme
     return cudaLaunchKernelEx(&cfg, kern, std::forward<Args>(args)...);
 }
 
-// One warp's own hardware barrier (named barrier `id` in [1, 8], 32 threads).  Used where a
-// warp hands data to itself through shared memory inside a persistent loop: a __syncwarp() that
+// One warp's own hardware barrier (named barrier `id` in [1, 15], 32 threads).  Used where a
+// warp hands data to itself through shared memory inside a persistent loop (ids 1..15): a __syncwarp() that
 // the compiler considers redundant is emitted as nothing, and the lanes are then not reliably
 // reconverged (measured on B200: stale shared-memory reads).  The ids are immediates so that ptxas
 // reserves only the barriers actually used (a register id reserves all 16 and caps occupancy).
@@ -174,8 +174,29 @@ __device__ __forceinline__ void warp_bar(int id) {
         case 5: asm volatile("bar.sync 5, 32;" ::: "memory"); break;
         case 6: asm volatile("bar.sync 6, 32;" ::: "memory"); break;
         case 7: asm volatile("bar.sync 7, 32;" ::: "memory"); break;
-        default: asm volatile("bar.sync 8, 32;" ::: "memory"); break;
+        case 8: asm volatile("bar.sync 8, 32;" ::: "memory"); break;
+        case 9: asm volatile("bar.sync 9, 32;" ::: "memory"); break;
+        case 10: asm volatile("bar.sync 10, 32;" ::: "memory"); break;
+        case 11: asm volatile("bar.sync 11, 32;" ::: "memory"); break;
+        case 12: asm volatile("bar.sync 12, 32;" ::: "memory"); break;
+        case 13: asm volatile("bar.sync 13, 32;" ::: "memory"); break;
+        case 14: asm volatile("bar.sync 14, 32;" ::: "memory"); break;
+        default: asm volatile("bar.sync 15, 32;" ::: "memory"); break;
     }
+}
+
+// &base[idx] for a 32-bit unsigned index as ONE IMAD.WIDE.U32 (nvcc otherwise often widens the
+// index and adds it with carries, 3-5 instructions per address)
+template <typename T>
+__device__ __forceinline__ T* ptr_at(T* base, unsigned idx) {
+    T* a;
+    asm("mad.wide.u32 %0, %1, %2, %3;" : "=l"(a) : "r"(idx), "n"((int)sizeof(T)), "l"(base));
+    return a;
+}
+
+// Bulk L2 prefetch of [p, p + bytes) (p 16-byte aligned, bytes a multiple of 16): one instruction
+__device__ __forceinline__ void prefetch_l2_bulk(const void* p, uint32_t bytes) {
+    asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(p), "r"(bytes) : "memory");
 }
 
 constexpr long long kNoDeadline = 0x7fffffffffffffffLL;
