@@ -824,7 +824,7 @@ k1_packed(const __grid_constant__ K1cParams p) {
         // S2), so each lane's segment starts 4-aligned and every 4-iteration batch is one aligned
         // int4 of the padded layout (segments of the scan layout are multiples of 4 long)
         int S2 = (((nn + 31) >> 5) + 3) & ~3;
-        if ((S2 & 4) == 0 && 32 * (S2 - 4) < nn) S2 += 4;
+        if ((S2 & 4) == 0 && 32 * (S2 - 4) < nn && S2 + 4 <= 32) S2 += 4;
         const int mlo = 1 + lane * S2, mhi = min(mlo + S2 - 1, nn);     // empty when mlo > nn
         uint32_t pk = 0xffffffffu;                   // key / B of m - 1 (m = 1 always starts a piece)
         int pb = 0;
@@ -834,74 +834,143 @@ k1_packed(const __grid_constant__ K1cParams p) {
             pk = key_of(v);
         }
         K1P_SYNC();                                   // every neighbour read before the in-place writes
-        int cnt = 0, e = 0;
-        #pragma unroll 1
-        for (int m0 = mlo; m0 <= mhi; m0 += 4) {
-            int4* const q = reinterpret_cast<int4*>(sv + ph(m0));
-            int4 v = *q;
-            const uint32_t k0 = key_of(v.x), k1 = key_of(v.y), k2 = key_of(v.z), k3 = key_of(v.w);
-            auto flag = [&](int& x, uint32_t k, bool live) {     // x: the histogram word of m
-                const int b = x >> 16;
-                const bool endp = live && b < pb;     // m - 1 is an end position
-                const bool fresh = live && k != pk;   // (a piece cut only at an end repeats the cell)
-                const bool head = fresh || endp;
-                cnt += head;
-                e += endp;
-                x = (int)(k | (head ? 1u << 30 : 0u) | (fresh ? 1u << 31 : 0u));
-                pk = k;
-                pb = b;
-            };
-            flag(v.x, k0, true);
-            flag(v.y, k1, m0 + 1 <= mhi);
-            flag(v.z, k2, m0 + 2 <= mhi);
-            flag(v.w, k3, m0 + 3 <= mhi);
-            *q = v;                                   // words past nn are never read again
-        }
-        int x = cnt;                                  // inclusive scan of the head counts
-#pragma unroll
-        for (int o = 1; o < 32; o <<= 1) {
-            const int y = __shfl_up_sync(kFull, x, o);
-            if (lane >= o) x += y;
-        }
-        h = __shfl_sync(kFull, x, 31);
-        ends = __reduce_add_sync(kFull, e);
-        int pos = x - cnt;                            // this lane's first piece
         int32_t* const rec_m = p.run_m + row;
         uint32_t* const rec_k = p.run_key + row;
-        #pragma unroll 1
-        for (int m0 = mlo; m0 <= mhi; m0 += 4) {
-            int4* const q = reinterpret_cast<int4*>(sv + ph(m0));
-            int4 v = *q;
-            auto piece = [&](int& x, int m) {
-                const uint32_t w = (uint32_t)x;
-                if (w & (1u << 30)) {                 // (words past mhi carry no head bit)
-                    const uint32_t k = cell_base + (w & 0x3fffffffu);
-                    *ptr_at(rec_m, (unsigned)pos) = m;
-                    *ptr_at(rec_k, (unsigned)pos) = k;
-                    if (w >> 31) claim_cell(p, k);
-                    ++pos;
-                }
-                x = pos - 1;                          // the piece of m
-            };
-            piece(v.x, m0);
-            piece(v.y, m0 + 1);
-            piece(v.z, m0 + 2);
-            piece(v.w, m0 + 3);
-            *q = v;
-        }
-        // Eq. 4 per piece (piece_deadlines): end_d[k] = min over the scheduled requests whose last
-        // iteration l is piece k's tail of ceil(fl64(t_dead - t_cur) * 2^40) (reading A-12).
         long long* const D = p.end_d + row;
-        #pragma unroll 1
-        for (int k = lane; k < h; k += 32) D[k] = kNoDeadline;
-        K1P_SYNC();                                   // piece indices and the initial minima in place
         const int n_sched = nr + n_adm;
-        #pragma unroll 1
-        for (int j = lane; j < n_sched; j += 32) {
-            const int4 r = __ldg(&p.req[rb + j]);
-            const int l = r.z - r.x;                  // 1 <= l <= nn (validated; n = max l)
-            const long long d = slack_ticks(__ldg(&p.t_dead[rb + j]) - in.t_cur, p.tick_shift);
-            if (d != kNoDeadline) atomicMin(ptr_at(D, (unsigned)sv[ph(l)]), d);   // fire-and-forget RED.MIN.S64
+        int cnt = 0, e = 0;
+        if (S2 <= 32) {
+            // Mask form (n <= 1024): pass A leaves each iteration's cell key in place and sets bit
+            // m - mlo of the lane's head mask; pass B visits only the set bits (one record per head,
+            // not a pass per iteration), and the piece of an iteration l is base[t] + popc(mask[t]
+            // up to l) - 1 (t the lane owning l), both left in the first 64 words for Eq. 4.
+            uint32_t mask = 0;
+            #pragma unroll 1
+            for (int m0 = mlo; m0 <= mhi; m0 += 4) {
+                int4* const q = reinterpret_cast<int4*>(sv + ph(m0));
+                int4 v = *q;
+                const uint32_t bit = 1u << (m0 - mlo);
+                auto flag = [&](int& x, uint32_t bu, bool live) {   // x: the histogram word of m
+                    const uint32_t k = key_of(x);
+                    const int b = x >> 16;
+                    const bool endp = live && b < pb;         // m - 1 is an end position
+                    const bool head = live && (k != pk || endp);
+                    mask |= head ? bu : 0u;
+                    e += endp;
+                    x = (int)k;
+                    pk = k;
+                    pb = b;
+                };
+                flag(v.x, bit, true);
+                flag(v.y, bit << 1, m0 + 1 <= mhi);
+                flag(v.z, bit << 2, m0 + 2 <= mhi);
+                flag(v.w, bit << 3, m0 + 3 <= mhi);
+                *q = v;                                   // words past nn are never read again
+            }
+            cnt = __popc(mask);
+            int x = cnt;                              // inclusive scan of the head counts
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+                const int y = __shfl_up_sync(kFull, x, o);
+                if (lane >= o) x += y;
+            }
+            h = __shfl_sync(kFull, x, 31);
+            ends = __reduce_add_sync(kFull, e);
+            const int base = x - cnt;                 // this lane's first piece
+            int pos = base;
+            #pragma unroll 1
+            for (uint32_t mm = mask; mm; mm &= mm - 1, ++pos) {
+                const int m = mlo + __ffs(mm) - 1;
+                const uint32_t k = cell_base + (uint32_t)sv[ph(m)];
+                *ptr_at(rec_m, (unsigned)pos) = m;
+                *ptr_at(rec_k, (unsigned)pos) = k;
+                claim_cell(p, k);                     // (also where a piece only repeats the cell)
+            }
+            #pragma unroll 1
+            for (int k = lane; k < h; k += 32) D[k] = kNoDeadline;
+            K1P_SYNC();                               // every lane's keys read
+            sv[lane] = base;
+            sv[32 + lane] = (int)mask;
+            K1P_SYNC();                               // bases, masks and the initial minima in place
+            // Eq. 4 per piece (piece_deadlines): end_d[k] = min over the scheduled requests whose
+            // last iteration l is piece k's tail of ceil(fl64(t_dead - t_cur) * 2^40) (A-12), by a
+            // fire-and-forget RED.MIN.S64 (a shared 64-bit atomicMin is a CAS loop)
+            const uint32_t inv = ((1u << 20) + (uint32_t)S2 - 1) / (uint32_t)S2;   // (l-1)/S2, l-1 < 1024
+            #pragma unroll 1
+            for (int j = lane; j < n_sched; j += 32) {
+                const int4 r = __ldg(&p.req[rb + j]);
+                const int l1 = r.z - r.x - 1;         // 0 <= l - 1 < nn (validated; n = max l)
+                const long long d = slack_ticks(__ldg(&p.t_dead[rb + j]) - in.t_cur, p.tick_shift);
+                const int t = (int)(((uint32_t)l1 * inv) >> 20);
+                const int jj = l1 - t * S2;
+                const int k = sv[t] + __popc((uint32_t)sv[32 + t] & (0xffffffffu >> (31 - jj))) - 1;
+                if (d != kNoDeadline) atomicMin(ptr_at(D, (unsigned)k), d);
+            }
+        } else {
+            // Per-iteration form (long horizons): pass A leaves key | head << 30 | fresh << 31 in
+            // place, pass B writes the records and leaves each iteration's piece index in place.
+            #pragma unroll 1
+            for (int m0 = mlo; m0 <= mhi; m0 += 4) {
+                int4* const q = reinterpret_cast<int4*>(sv + ph(m0));
+                int4 v = *q;
+                const uint32_t k0 = key_of(v.x), k1 = key_of(v.y), k2 = key_of(v.z), k3 = key_of(v.w);
+                auto flag = [&](int& x, uint32_t k, bool live) {
+                    const int b = x >> 16;
+                    const bool endp = live && b < pb;
+                    const bool fresh = live && k != pk;
+                    const bool head = fresh || endp;
+                    cnt += head;
+                    e += endp;
+                    x = (int)(k | (head ? 1u << 30 : 0u) | (fresh ? 1u << 31 : 0u));
+                    pk = k;
+                    pb = b;
+                };
+                flag(v.x, k0, true);
+                flag(v.y, k1, m0 + 1 <= mhi);
+                flag(v.z, k2, m0 + 2 <= mhi);
+                flag(v.w, k3, m0 + 3 <= mhi);
+                *q = v;                               // words past nn are never read again
+            }
+            int x = cnt;
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+                const int y = __shfl_up_sync(kFull, x, o);
+                if (lane >= o) x += y;
+            }
+            h = __shfl_sync(kFull, x, 31);
+            ends = __reduce_add_sync(kFull, e);
+            int pos = x - cnt;
+            #pragma unroll 1
+            for (int m0 = mlo; m0 <= mhi; m0 += 4) {
+                int4* const q = reinterpret_cast<int4*>(sv + ph(m0));
+                int4 v = *q;
+                auto piece = [&](int& x, int m) {
+                    const uint32_t w = (uint32_t)x;
+                    if (w & (1u << 30)) {
+                        const uint32_t k = cell_base + (w & 0x3fffffffu);
+                        *ptr_at(rec_m, (unsigned)pos) = m;
+                        *ptr_at(rec_k, (unsigned)pos) = k;
+                        if (w >> 31) claim_cell(p, k);
+                        ++pos;
+                    }
+                    x = pos - 1;
+                };
+                piece(v.x, m0);
+                piece(v.y, m0 + 1);
+                piece(v.z, m0 + 2);
+                piece(v.w, m0 + 3);
+                *q = v;
+            }
+            #pragma unroll 1
+            for (int k = lane; k < h; k += 32) D[k] = kNoDeadline;
+            K1P_SYNC();
+            #pragma unroll 1
+            for (int j = lane; j < n_sched; j += 32) {
+                const int4 r = __ldg(&p.req[rb + j]);
+                const int l = r.z - r.x;
+                const long long d = slack_ticks(__ldg(&p.t_dead[rb + j]) - in.t_cur, p.tick_shift);
+                if (d != kNoDeadline) atomicMin(ptr_at(D, (unsigned)sv[ph(l)]), d);
+            }
         }
     }
     if (lane == 0) {

@@ -11,9 +11,10 @@
 //    mbarrier completion), double-buffered in chunks when the model exceeds the smem budget;
 //    every CTA streams the chunks in the same fixed order, so the per-row fp32 sums are formed in
 //    tree order.
-//  * One tree level costs 4 instructions per row: LDS (word), PRMT (pick the split feature's rank
-//    into the upper half), IADD3 with carry-out (rank + 0xFFFF - j overflows <=> go right) and
-//    IADD3.X (idx = 2*idx + carry).  No branches, no divergence.
+//  * One tree level costs 5 instructions per row: LDS (word), PRMT (pick the split feature's rank
+//    into the upper half), IADD3 with carry-out (rank + 0xFFFF - j overflows <=> go right),
+//    IADD3.X (idx = 2*idx + carry) and the IMAD that turns idx into the next word's shared-memory
+//    address.  No branches, no divergence.
 //  * Persistent-style grid (#SMs x occupancy CTAs); tiles are split evenly over CTAs by a
 //    per-CTA scan of the per-instance tile counts.
 #include <algorithm>
