@@ -81,6 +81,22 @@ __device__ __forceinline__ const TV* tab_at(const TV* col, unsigned off) {
     asm("mad.wide.u32 %0, %1, %2, %3;" : "=l"(a) : "r"(off), "n"((int)sizeof(TV)), "l"(col));
     return a;
 }
+// T' table loads through L1 (default: hot cells are shared by many instances, C5 K3c 527 -> 497 us)
+// or L2 only (TP_K3C_LDG=0)
+#ifndef TP_K3C_LDG
+#define TP_K3C_LDG 1
+#endif
+#ifndef TP_K3C_CARVE
+#define TP_K3C_CARVE -1      // preferred shared-memory carveout in percent (-1: the driver's choice)
+#endif
+template <typename TV>
+__device__ __forceinline__ TV lut_load(const TV* a) {
+#if TP_K3C_LDG
+    return __ldg(a);
+#else
+    return __ldcg(a);
+#endif
+}
 // the 32-bit table (units of 2^8 ticks): one 32 x 32 -> 64-bit multiply-add
 __device__ __forceinline__ unsigned long long mad_len(unsigned long long T, unsigned len, unsigned t) {
     return T + (unsigned long long)len * t;
@@ -178,7 +194,7 @@ k3_compact(const __grid_constant__ K3cParams p) {
 #pragma unroll
             for (int j = 0; j < PD; ++j) {
                 const int4 r = buf[j];
-                rt[j] = __ldcg(tab_at(col, (unsigned)r.x));
+                rt[j] = lut_load(tab_at(col, (unsigned)r.x));
                 rl[j] = (unsigned)r.y;
                 rd[j] = ((unsigned long long)(unsigned)r.w << 32) | (unsigned)r.z;
             }
@@ -189,7 +205,7 @@ k3_compact(const __grid_constant__ K3cParams p) {
                     TV tn = 0;
                     if constexpr (decltype(more)::value) {
                         r = buf[q0 + PD + j];         // broadcast: the record PD pieces ahead
-                        tn = __ldcg(tab_at(col, (unsigned)r.x));
+                        tn = lut_load(tab_at(col, (unsigned)r.x));
                     }
                     T = mad_len(T, rl[j], rt[j]);     // T_R at this piece's tail (Eq. 3)
                     if (W == 1) ok &= T < rd[j];      // Eq. 4, strict (Dmin >= 0: unsigned compare)
@@ -223,7 +239,7 @@ k3_compact(const __grid_constant__ K3cParams p) {
 #pragma unroll
         for (int j = 0; j < PD; ++j) {
             const int4 r = s_rec[warp][0][j];
-            rt[j] = __ldcg(tab_at(col, (unsigned)r.x));
+            rt[j] = lut_load(tab_at(col, (unsigned)r.x));
             rl[j] = (unsigned)r.y;
             rd[j] = ((unsigned long long)(unsigned)r.w << 32) | (unsigned)r.z;
         }
@@ -243,7 +259,7 @@ k3_compact(const __grid_constant__ K3cParams p) {
 #pragma unroll
                 for (int j = 0; j < PD; ++j) {
                     const int4 r = ahead[j];          // broadcast: the record PD pieces ahead
-                    const TV tn = __ldcg(tab_at(col, (unsigned)r.x));
+                    const TV tn = lut_load(tab_at(col, (unsigned)r.x));
                     T = mad_len(T, rl[j], rt[j]);     // T_R at this piece's tail (Eq. 3)
                     if (W == 1) ok &= T < rd[j];      // Eq. 4, strict (Dmin >= 0: unsigned compare)
                     else M = min(M, (long long)rd[j] - (long long)T);
@@ -359,6 +375,7 @@ int launch_select_compact(const K2Params& w, int32_t n_inst, const int32_t* n, i
             static int per_sm[2][64] = {};
             const int li = w.tick_shift == 8;
             if (dev < 64 && per_sm[li][dev] == 0) {
+                if (TP_K3C_CARVE >= 0) cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout, TP_K3C_CARVE);
                 int b = 0;
                 cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, kern, kWarpsPerCta * 32, 0);
                 per_sm[li][dev] = b > 0 ? b : 1;
