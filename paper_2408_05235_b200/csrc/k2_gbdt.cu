@@ -527,6 +527,9 @@ k2_gbdt(const __grid_constant__ K2Params p, int TC, int nchunks) {
 // base score, the last one clamps, writes the tick LUT and the clamp masks), so every row's leaves
 // are still added one by one in tree order (reading A-7).
 constexpr int kPhaseChunkTrees = 8;
+#ifndef TP_K2_TPAIR
+#define TP_K2_TPAIR 1
+#endif
 constexpr int kMaxPhaseChunks = 64;
 constexpr int kPhaseThreads = 1024;
 
@@ -603,9 +606,50 @@ k2_cells_phase(const __grid_constant__ K2Params p, int t_begin, int t_count, int
 #pragma unroll
                 for (int r = 0; r < RR; ++r) acc[r] = __fadd_rn(acc[r], __uint_as_float(tw[idx[r]]));
             };
-            if (nt == kPhaseChunkTrees) {
+            // TP_K2_TPAIR: two trees' descents interleaved level by level (2 x RR independent
+            // dependent-load chains per thread), then their leaves added in tree order -- the same
+            // fp32 sum, more latency hidden when there are few rows per SM
+            auto tree2 = [&](int tt) {
+                const uint32_t* ta = cw + tt * TW;
+                const uint32_t* tb = ta + TW;
+                uint32_t ia[RR], ib[RR];
+                if constexpr (D >= 2) {
+                    const uint32_t a1 = ta[1], b1 = tb[1];
+                    const uint2 a23 = *reinterpret_cast<const uint2*>(ta + 2);
+                    const uint2 b23 = *reinterpret_cast<const uint2*>(tb + 2);
 #pragma unroll
-                for (int tt = 0; tt < kPhaseChunkTrees; ++tt) tree(tt);
+                    for (int r = 0; r < RR; ++r) {
+                        const bool ca = prmt(xlo, xhi[r], a1) > ~a1;
+                        const bool cb = prmt(xlo, xhi[r], b1) > ~b1;
+                        ia[r] = step_from(ca ? 6u : 4u, ca ? a23.y : a23.x, xlo, xhi[r]);
+                        ib[r] = step_from(cb ? 6u : 4u, cb ? b23.y : b23.x, xlo, xhi[r]);
+                    }
+                } else {
+#pragma unroll
+                    for (int r = 0; r < RR; ++r) ia[r] = ib[r] = 1u;
+                }
+#pragma unroll
+                for (int d = (D >= 2 ? 2 : 0); d < D; ++d) {
+#pragma unroll
+                    for (int r = 0; r < RR; ++r) {
+                        ia[r] = descend(ia[r], ta[ia[r]], xlo, xhi[r]);
+                        ib[r] = descend(ib[r], tb[ib[r]], xlo, xhi[r]);
+                    }
+                }
+#pragma unroll
+                for (int r = 0; r < RR; ++r) {
+                    acc[r] = __fadd_rn(acc[r], __uint_as_float(ta[ia[r]]));
+                    acc[r] = __fadd_rn(acc[r], __uint_as_float(tb[ib[r]]));
+                }
+            };
+            if (nt == kPhaseChunkTrees) {
+                if constexpr (TP_K2_TPAIR) {
+#pragma unroll
+                    for (int tt = 0; tt < kPhaseChunkTrees; tt += 2) tree2(tt);
+                } else {
+#pragma unroll
+                    for (int tt = 0; tt < kPhaseChunkTrees; ++tt) tree(tt);
+                }
             } else {
                 for (int tt = 0; tt < nt; ++tt) tree(tt);
             }

@@ -8,6 +8,7 @@ timeout 900 python -m pytest tests -m gpu -x -q -k "$PK" > $o/pytest.log 2>&1; e
 tail -2 $o/pytest.log
 WL=C5 bash tools/sweep_r02.sh "$@" 2>&1 | tee $o/sweep_c5.txt
 WL=C3 bash tools/sweep_r02.sh "$@" 2>&1 | tee $o/sweep_c3.txt
+WL=C2 bash tools/sweep_r02.sh "$@" 2>&1 | tee $o/sweep_c2.txt
 if [ "$RX" != "none" ]; then
 B="python bench.py --workload C5 --steps 1 --warmup 3 --no-cpu-baseline --e2e-steps 0 --no-graph"
 timeout 900 ncu --set full --clock-control none --import-source on -k regex:"$RX" -s 3 -c 1 -o $o/full $B > $o/ncu.log 2>&1
