@@ -10,7 +10,8 @@ already resident in HBM when the timed region starts.
   python bench.py [--gpus N] [--steps K] [--warmup W] [--workload C5] [--impl ours|reference]
 
 Default workload C5 = BASELINE.json configs[4], the configuration the metric is quoted on: 262,144
-instances sharded over the N GPUs (strong scaling: rank r decides its contiguous 262,144/N).  N > 1
+instances sharded over the N GPUs (strong scaling: rank r decides 262,144/N of them, grouped by
+engine size, shard.shard_by_engine).  N > 1
 runs under torchrun, one process per GPU, NCCL.  --workload C2/C3 time the other configs (C2: weak
 scaling, 1,024 instances per GPU); --workload C4 is the trace replay.
 """
@@ -48,6 +49,16 @@ def env_int(k, d):
         return int(os.environ.get(k, d))
     except ValueError:
         return d
+
+
+def parse_emulate(s):
+    """'R/N' -> (R, N); None -> (0, 1)."""
+    if not s:
+        return 0, 1
+    r, n = (int(x) for x in s.split("/"))
+    if not (0 <= r < n):
+        raise SystemExit(f"--emulate-shard {s}: need 0 <= R < N")
+    return r, n
 
 
 def shard_of(cfg, rank, world):
@@ -408,6 +419,9 @@ def main():
                     help="reference arm: instances the oracle decides per step (default per workload)")
     ap.add_argument("--instances", type=int, default=None,
                     help="override the workload's global instance count (tests; the line says so)")
+    ap.add_argument("--emulate-shard", default=None,
+                    help="R/N: one process decides rank R's shard of an N-way C5 sweep (no gather; a "
+                         "per-rank step time for DESIGN.md's scaling projection, not a multi-GPU number)")
     ap.add_argument("--dump-decisions", default=None,
                     help="rank 0 writes the gathered [2, I] (level, status) rows of the last step (.npy)")
     ap.add_argument("--replay-cap", type=int, default=60000,
@@ -465,7 +479,19 @@ def main():
         return
     i0, i1, I_glob = shard_of(cfg, rank, world)
     blob = W.write_blob(W.config_ensemble(cfg))
-    inputs = W.config_inputs(dataclasses_replace(cfg, I_glob), i0, i1)
+    em_r, em_n = parse_emulate(args.emulate_shard)
+    shard_ix, perm = None, None
+    if cfg.name != "C2" and (world > 1 or em_n > 1):
+        # strong scaling grouped by engine size (shard.shard_by_engine): every rank generates the
+        # global round (untimed) and keeps its instances
+        cfg_g = dataclasses_replace(cfg, I_glob)
+        tpv = W.tp_of(cfg_g)
+        r_, n_ = (rank, world) if world > 1 else (em_r, em_n)
+        shard_ix = shard.shard_by_engine(tpv, r_, n_)
+        perm = np.concatenate([shard.shard_by_engine(tpv, r, n_) for r in range(n_)])
+        inputs = W.select_instances(W.config_inputs(cfg_g), shard_ix)
+    else:
+        inputs = W.config_inputs(dataclasses_replace(cfg, I_glob), i0, i1)
     I, R = len(inputs["inst"]), len(inputs["req"])
     model = tp.Gbdt(blob, local)
     info = model.info()
@@ -529,9 +555,13 @@ def main():
     step_ms = np.array([a.elapsed_time(b) for a, b in evs])            # ms, the K timed steps
     t_total = float(step_ms.sum())
     if args.dump_decisions:
-        res = gather.result() if gather is not None else rows[:, :I]
+        res = (gather.result() if gather is not None else rows[:, :I]).cpu().numpy()
+        if gather is not None and perm is not None:      # engine-grouped shards -> global order
+            glob = np.zeros_like(res)
+            glob[:, perm] = res
+            res = glob
         if rank == 0:
-            np.save(args.dump_decisions, res.cpu().numpy())
+            np.save(args.dump_decisions, res)
     # per-kernel breakdown (the kernel times of the rooflines): a second pass of K steps kernel by
     # kernel with events between the kernels, same inputs, same L2 flushes
     evk = [[torch.cuda.Event(enable_timing=True) for _ in range(5)] for _ in range(args.steps)]
@@ -653,7 +683,10 @@ def main():
         "config": {"workload": DESCR[cfg.name], "name": cfg.name, "instances_per_gpu": I,
                    "global_instances": int(inst_all), "H": cfg.H, "F": cfg.F, "trees": info.n_trees,
                    "depth": info.depth,
-                   "parallelism": f"instance-sharded x{world}" + (" + NCCL all-gather" if world > 1 else ""),
+                   "parallelism": f"instance-sharded x{world}"
+                                  + (", grouped by engine size" if shard_ix is not None and world > 1 else "")
+                                  + (" + NCCL all-gather" if world > 1 else ""),
+                   "emulated_shard": args.emulate_shard,
                    "l2": "flushed between timed steps (256 MiB device write, untimed)",
                    "path": "compact: K1c -> K2 cell phases -> K3c (B/KV on chip), PDL, "
                            + ("one CUDA graph per step" if args.graph else "kernel by kernel"),

@@ -16,6 +16,21 @@ def shard_range(n_total: int, rank: int, world: int) -> tuple[int, int]:
     return n_total * rank // world, n_total * (rank + 1) // world
 
 
+def shard_by_engine(tp, rank: int, world: int):
+    """Strong scaling, grouped by engine size: the global indices of ``rank``'s instances.
+
+    The instances are ordered by (tp, index) and cut into ``world`` contiguous equal-count (+-1)
+    chunks.  The model is evaluated once per distinct cell (rank_tp, rank_B, rank_KV) a rank's
+    instances touch, and tp is one coordinate of the cell, so a rank that holds one or two engine
+    sizes evaluates a quarter or a half of the cells a mixed shard touches -- the K2 work that
+    does not shrink with N under index-contiguous sharding.  The decisions are the
+    same; only who decides which instance changes."""
+    import numpy as np
+    order = np.argsort(np.asarray(tp), kind="stable")
+    i0, i1 = shard_range(len(order), rank, world)
+    return order[i0:i1]
+
+
 def shard_counts(n_total: int, world: int) -> list[int]:
     return [b - a for a, b in (shard_range(n_total, r, world) for r in range(world))]
 

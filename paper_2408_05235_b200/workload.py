@@ -164,6 +164,30 @@ def _gen_block(cfg: Config, block: int, n: int):
     return inst, req, t_dead.astype(np.float64)
 
 
+def tp_of(cfg: Config) -> np.ndarray:
+    """Engine size (tp) of every instance of ``cfg``, without generating the requests: the first
+    draw of each block's generator (as `_gen_block`)."""
+    out = np.empty(cfg.n_inst, np.int64)
+    for b in range((cfg.n_inst + BLOCK - 1) // BLOCK):
+        b0 = b * BLOCK
+        nb = min(BLOCK, cfg.n_inst - b0)
+        out[b0:b0 + nb] = np.random.default_rng([cfg.seed, b]).choice(np.array([1, 2, 4, 8]), size=nb)
+    return out
+
+
+def select_instances(inputs: dict, idx) -> dict:
+    """The instances ``idx`` (in that order) of a round's inputs as a self-contained round: request
+    rows gathered, ``req_begin`` rebased.  Input plumbing only."""
+    idx = np.asarray(idx, np.int64)
+    inst = inputs["inst"][idx].copy()
+    cnt = (inst["n_run"] + inst["n_queue"]).astype(np.int64)
+    begin = inst["req_begin"].astype(np.int64)
+    off = np.concatenate([[0], np.cumsum(cnt)[:-1]]) if len(idx) else np.zeros(0, np.int64)
+    rows = np.repeat(begin - off, cnt) + np.arange(int(cnt.sum()))
+    inst["req_begin"] = off
+    return dict(inputs, inst=inst, req=inputs["req"][rows], t_dead=inputs["t_dead"][rows])
+
+
 def gen_instances(cfg: Config, i0: int = 0, i1: int | None = None):
     """Instances [i0, i1) of ``cfg`` (default: all) -> (inst, req, t_dead).
 

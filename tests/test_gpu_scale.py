@@ -115,6 +115,15 @@ def test_bench_path_c5_stratified_and_shards(gpu, oracle_mod):
         part = bench_decisions(gpu, blob, W.config_inputs(cfg, i0, i1), replays=1)
         for k in part:
             assert np.array_equal(part[k], got[k][i0:i1]), f"shard {N - 1}/{N} {k}"
+    # the engine-grouped shards bench.py's ranks decide at N > 1 (shard.shard_by_engine): the first
+    # and last rank of each sweep, every decision equal to the single-GPU run's
+    tpv = W.tp_of(cfg)
+    for N in (2, 4, 8):
+        for r in (0, N - 1):
+            ix = shard.shard_by_engine(tpv, r, N)
+            part = bench_decisions(gpu, blob, W.select_instances(inputs, ix), replays=1)
+            for k in part:
+                assert np.array_equal(part[k], got[k][ix]), f"engine shard {r}/{N} {k}"
 
 
 def test_bench_path_c4_generator(gpu, oracle_mod):
