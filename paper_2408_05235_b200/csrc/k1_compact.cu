@@ -537,6 +537,9 @@ __device__ __forceinline__ void k1_body(const K1cParams& p, const int i, Group<W
 #ifndef TP_K1P_WARPS
 #define TP_K1P_WARPS 14      // warps (instances in flight) per CTA (named barriers 1..15)
 #endif
+#ifndef TP_K1P_RTP
+#define TP_K1P_RTP 1         // engine-size ranks from a per-CTA table (0: a binary search per instance)
+#endif
 #ifndef TP_K1P_MINB
 #define TP_K1P_MINB 3        // CTAs per SM: 3 x (14 x 4.6 KB + 9 KB of tables) at H = 1024
 #endif
@@ -576,6 +579,10 @@ k1_packed(const __grid_constant__ K1cParams p) {
         if (f.y > 0 && f.z >= 0 && f.x >= 0 && (int64_t)f.x + f.y + f.z <= (int64_t)p.n_req)
             prefetch_l2_bulk(p.req + f.x, (uint32_t)(f.y + f.z) * 16u);
     }
+    // rank of every engine size tp < 64 among the tp cuts (one binary search per CTA, not per instance)
+    __shared__ uint16_t s_rtp[64];
+    if (threadIdx.x < 64) s_rtp[threadIdx.x] = (uint16_t)rank_of(p.cuts + p.cut_off[0], p.cut_off[1] - p.cut_off[0],
+                                                                 (float)threadIdx.x);
     if constexpr (ST) {
         for (int k = threadIdx.x; k < p.tab_words; k += blockDim.x)
             smem[k] = __ldg(reinterpret_cast<const int*>(p.rtab) + k);
@@ -583,6 +590,7 @@ k1_packed(const __grid_constant__ K1cParams p) {
         tB = reinterpret_cast<const uint16_t*>(smem) + p.rtab_off[0];
         tKV = reinterpret_cast<const uint16_t*>(smem) + p.rtab_off[1];
     } else {
+        __syncthreads();
         tB = p.rtab + p.rtab_off[0];
         tKV = p.rtab + p.rtab_off[1];
     }
@@ -812,7 +820,8 @@ k1_packed(const __grid_constant__ K1cParams p) {
     if (nn > 0) {
         const int nKV = p.cut_off[3] - p.cut_off[2];
         const uint32_t nk1 = (uint32_t)nKV + 1;
-        const uint32_t rtp = rank_of(p.cuts + p.cut_off[0], p.cut_off[1] - p.cut_off[0], (float)in.tp);
+        const uint32_t rtp = TP_K1P_RTP && (uint32_t)in.tp < 64u ? s_rtp[in.tp]
+                                                     : rank_of(p.cuts + p.cut_off[0], p.cut_off[1] - p.cut_off[0], (float)in.tp);
         const uint32_t cell_base = rtp * (uint32_t)(p.cut_off[2] - p.cut_off[1] + 1) * nk1;
         // b < 2^15, kv < 2^16 here (the packed check): the clamped table lookups are exact
         auto key_of = [&](int v) -> uint32_t {
