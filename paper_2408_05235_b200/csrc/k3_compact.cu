@@ -160,7 +160,8 @@ k3_compact(const __grid_constant__ K3cParams p) {
         // this lane's column of the T' table (by cell id; lanes >= F read column F-1 -- ignored)
         const TV* col = reinterpret_cast<const TV*>(p.lut_ticks) + min(lane, F - 1);
         // piece k's record, lane-parallel: {cell id * F, len, Dmin lo, Dmin hi}; padding past kz
-        // (table offset 0, len 0, no deadline) walks as a no-op
+        // (len 0, no deadline; the T' row of the chunk's first piece, so every T' load reads a row
+        // K2 wrote) walks as a no-op
         int s0 = 0, s1 = 0;
         uint32_t key = 0;
         long long d = kNoDeadline;
@@ -175,8 +176,10 @@ k3_compact(const __grid_constant__ K3cParams p) {
             }
         };
         auto stage = [&](int4* buf) {
-            buf[lane] = v ? make_int4((int)(key * (uint32_t)F), s1 - s0, (int)(unsigned)d, (int)(d >> 32))
-                          : make_int4(0, 0, -1, 0x7fffffff);
+            const int off = (int)(key * (uint32_t)F);
+            const int off0 = __shfl_sync(kFull, off, 0);          // lane 0's piece is always real
+            buf[lane] = v ? make_int4(off, s1 - s0, (int)(unsigned)d, (int)(d >> 32))
+                          : make_int4(off0, 0, -1, 0x7fffffff);
             if (v) cm |= __ldcg(p.cell_clamp + key);
         };
 #if TP_K3C_SINGLE

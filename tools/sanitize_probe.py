@@ -26,4 +26,15 @@ for name, n_inst in [("P2", 40), ("C2", 24), ("C1", 3)]:
     ctx.decide(model, r.inst, I, r.req, R, r.t_dead, inputs["freq"], inputs["tbt_slo"], r.level, r.status)
     torch.cuda.synchronize()
     print(name, "levels", r.level[:8].cpu().numpy())
+# the large-batch K1c (k1_packed: one warp per instance, persistent CTAs) needs > 2 * 148 * 32 / 4
+# instances; a C3-shaped round of 2,600 takes it (plus its hand-over kernel)
+cfg = dataclasses.replace(W.CONFIGS["C3"], n_inst=2600)
+blob = W.write_blob(W.config_ensemble(cfg))
+inputs = W.config_inputs(cfg)
+model = tp.Gbdt(blob, 0)
+r = runner.Round(inputs, "cuda:0", k2_mode="compact", model=model)
+r.bkv = False
+r.run(model)
+torch.cuda.synchronize()
+print("C3 packed levels", r.level[:8].cpu().numpy())
 print("sanitize probe done")
