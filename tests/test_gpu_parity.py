@@ -7,6 +7,7 @@ therefore met with margin 0); T_R ticks bit-exact (exact integer sums).
 from __future__ import annotations
 
 import dataclasses
+import os
 
 import numpy as np
 import pytest
@@ -377,3 +378,31 @@ def test_compact_packed_fallback(gpu, oracle_mod):
     ref = run_oracle(oracle_mod, blob, inputs, want_tr=False)
     assert_parity(got, ref)
     assert int(got["KV"][5].max()) >= 65536
+
+
+def test_compact_packed_long_horizon(gpu, oracle_mod):
+    """Large batches (one warp per instance, packed histograms) whose horizon exceeds 1,024
+    iterations: the lane segments of the piece pass are then longer than 32 iterations, so K1c
+    takes its per-iteration piece form instead of the per-lane head masks -- both bit-exact, in
+    the same launch (instances with n <= 1,024 keep the mask form)."""
+    cfg = dataclasses.replace(W.CONFIGS["P2"], n_inst=2600, H=2048, seed=8777)
+    blob = W.write_blob(W.config_ensemble(cfg))
+    inputs = W.config_inputs(cfg)
+    inst, req = inputs["inst"].copy(), inputs["req"].copy()
+    long_ix = np.arange(3, cfg.n_inst, 7)
+    for i in long_ix:                          # one running request with l = 1,100 .. 2,048
+        b, nr = int(inst[i]["req_begin"]), int(inst[i]["n_run"])
+        if nr:
+            a = int(req["a"][b])
+            req["r"][b] = a + 1100 + (int(i) * 37) % 949
+    inputs = dict(inputs, inst=inst, req=req)
+    got = run_gpu(gpu, blob, inputs, want_tr=False, mode="compact")
+    assert int((got["n"] > 1024).sum()) >= 200
+    idx = np.union1d(long_ix[::3], np.arange(0, cfg.n_inst, 11))
+    ref = run_oracle(oracle_mod, blob, cases.subset_inputs(inputs, idx), want_tr=False, want_grid=False,
+                     threads=os.cpu_count() or 8)
+    for k in ["level", "n", "n_adm"]:
+        assert np.array_equal(got[k][idx].astype(np.int64), ref[k].astype(np.int64)), k
+    assert np.array_equal(got["status"][idx].astype(np.uint32), ref["status"].astype(np.uint32)), "status"
+    for k in ["B", "KV"]:
+        assert np.array_equal(got[k][idx], ref[k]), k
