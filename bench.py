@@ -659,9 +659,12 @@ def main():
         "k3": roof("hbm", "k3_compact<W> (K3c: exact T_R per piece, Eq. 4, TBT, ballot argmin)",
                    k3_bytes, k_ms[2], hbm, traffic.get("k3"),
                    basis="12 + 16 pieces bytes per instance (LUT reads are L2 traffic)",
-                   extra={"lut_bytes_l2": 8 * rnd.F * cs["pieces"],
+                   extra={"lut_bytes_l2": (4 if info.tick_shift == 8 else 8) * rnd.F * cs["pieces"],
                           "tick_updates_per_s": rnd.F * cs["pieces"] / (k_ms[2] / 1e3)}),
     }
+    for k, v in load_traffic(cfg.name, "ncu_limiters").items():
+        if k in kern:
+            kern[k]["ncu_limiters"] = v
     dom = max(kern, key=lambda k: kern[k]["ms"])
     roofline = dict(kern[dom], dominant=dom, per_kernel=kern)
     if d_ms is not None:
@@ -732,12 +735,13 @@ def roof(bound, kernel, algo_bytes, ms, peak_gbs, traffic, basis, extra=None):
     return r
 
 
-def load_traffic(name):
-    """ncu dram__bytes (read + write) per launch of each kernel, from the committed capture of
-    this workload (profiles/traffic_<name>.json), or {}."""
+def load_traffic(name, key="dram_bytes_per_launch"):
+    """ncu dram__bytes (read + write) per launch of each kernel (or, key="ncu_limiters", its issue /
+    L1 data-pipe / DRAM / warp utilisation), from the committed capture of this workload
+    (profiles/traffic_<name>.json), or {}."""
     try:
         with open(os.path.join(ROOT, "profiles", f"traffic_{name}.json")) as f:
-            return json.load(f).get("dram_bytes_per_launch", {})
+            return json.load(f).get(key, {})
     except (OSError, ValueError):
         return {}
 
