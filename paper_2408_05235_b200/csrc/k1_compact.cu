@@ -540,6 +540,21 @@ __device__ __forceinline__ void k1_body(const K1cParams& p, const int i, Group<W
 #ifndef TP_K1P_RTP
 #define TP_K1P_RTP 1         // engine-size ranks from a per-CTA table (0: a binary search per instance)
 #endif
+#ifndef TP_K1P_REQPF
+#define TP_K1P_REQPF 1       // request loop: the lane's next record loaded one iteration ahead
+#endif
+#ifndef TP_K1P_EQ4PF
+#define TP_K1P_EQ4PF 1       // Eq. 4 pass: the lane's first record + deadline loaded before the piece passes
+#endif
+#ifndef TP_K1P_BATCHQ
+#define TP_K1P_BATCHQ 1      // the bound-covered prefix of the FIFO queue admitted as events before the scan
+#endif
+#ifndef TP_K1P_EQ4B
+#define TP_K1P_EQ4B 1        // Eq. 4 pass: records per lane loaded together (1: one ahead)
+#endif
+#ifndef TP_K1P_MAXREG
+#define TP_K1P_MAXREG 48     // > 0: register cap instead of the CTAs-per-SM launch bound (48 x 42 warps fill the file)
+#endif
 #ifndef TP_K1P_MINB
 #define TP_K1P_MINB 3        // CTAs per SM: 3 x (14 x 4.6 KB + 9 KB of tables) at H = 1024
 #endif
@@ -566,7 +581,11 @@ __device__ __forceinline__ void block_events(int* sv, int m1, int l, int N, int 
 // warps' histograms; every lookup an LDS), else read through L1 from global memory.  Persistent:
 // the CTAs that fit at once, warp w of CTA b takes instances b * wpb + w, + gridDim.x * wpb, ...
 template <bool ST>
+#if TP_K1P_MAXREG
+__global__ void __maxnreg__(TP_K1P_MAXREG)
+#else
 __global__ void __launch_bounds__(TP_K1P_WARPS * 32, TP_K1P_MINB)
+#endif
 k1_packed(const __grid_constant__ K1cParams p) {
     extern __shared__ __align__(16) int smem[];
     const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, wpb = (int)(blockDim.x >> 5);
@@ -604,9 +623,15 @@ k1_packed(const __grid_constant__ K1cParams p) {
     const int64_t rb = in.req_begin;
     const int nr = in.n_run, nq = in.n_queue, N = in.N;
     const FastDiv fdN((uint32_t)(N > 0 ? N : 1));
+    // one request's Eq. 1 events: its block increments and the end event at l + 1
+    auto req_events = [&](int m1, int l, int kv_end) {
+        block_events(sv, m1, l, N, SL, P);
+        atomicAdd(&sv[ph(l + 1)], -(65536 + kv_end));                           // B -1 and KV -kv_end
+    };
     // the warp's next instance: {req_begin, n_run, n_queue, N}, for the L2 prefetch of its request
     // table below (its loads are then L2 hits instead of HBM round trips)
     const int inext = i + gridDim.x * wpb;
+    const bool first = i == blockIdx.x * wpb + w;
     int4 nx = make_int4(0, 0, 0, 0);
     if (lane == 0 && inext < p.n_inst) nx = __ldg(reinterpret_cast<const int4*>(p.inst + inext) + 1);
     #pragma unroll 1
@@ -619,16 +644,36 @@ k1_packed(const __grid_constant__ K1cParams p) {
     int nloc = 0, b1 = 0, kv1 = 0;
     bool lost = false;
     if (!bad) {
+        const int ne = nr + nq;
+#if TP_K1P_REQPF
+        // the next record of this lane is loaded before the current one's events (one load in flight
+        // behind the shared atomics instead of a full round trip per iteration)
+        int4 rn = lane < ne ? __ldg(&p.req[rb + lane]) : make_int4(0, 0, 0, 0);
+#if TP_K1P_REQPF > 1
+        int4 rn2 = lane + 32 < ne ? __ldg(&p.req[rb + lane + 32]) : make_int4(0, 0, 0, 0);
+#endif
+#endif
         #pragma unroll 1
-        for (int e = lane; e < nr + nq; e += 32) {
+        for (int e = lane; e < ne; e += 32) {
+#if TP_K1P_REQPF
+            const int4 r = rn;
+#if TP_K1P_REQPF > 1
+            rn = rn2;
+            if (e + 64 < ne) rn2 = __ldg(&p.req[rb + e + 64]);
+#else
+            if (e + 32 < ne) rn = __ldg(&p.req[rb + e + 32]);
+#endif
+#else
             const int4 r = __ldg(&p.req[rb + e]);
+#endif
             const int64_t l64 = (int64_t)r.z - r.x;
             const bool eb = r.x < 0 || r.y < 1 || r.z < 1 || r.x >= kFeatLimit || r.y >= kFeatLimit || l64 < 1 ||
                             l64 > H || (e >= nr && r.x != 0);
             bad |= eb;
             if (eb) continue;
             const int a = r.x, q = r.y, l = (int)l64, aq = a + q;
-            asm volatile("prefetch.global.L2 [%0];" ::"l"(p.t_dead + rb + e));
+            // the warp's later instances had their deadlines bulk-prefetched by the previous one
+            if (first) asm volatile("prefetch.global.L2 [%0];" ::"l"(p.t_dead + rb + e));
             const int kv_end = (int)fdN.div((uint32_t)(aq + l - 2)) + 1;           // ceil((a+l-1+q)/N)
             foot += kv_end;
             if (e < nr) {
@@ -637,8 +682,7 @@ k1_packed(const __grid_constant__ K1cParams p) {
                 const int c1 = (int)fdN.div((uint32_t)(aq - 1));                    // ceil(aq / N) - 1
                 kv1 += c1 + 1;
                 ++b1;
-                block_events(sv, 2 + (c1 + 1) * N - aq, l, N, SL, P);
-                atomicAdd(&sv[ph(l + 1)], -(65536 + kv_end));                       // B -1 and KV -kv_end
+                req_events(2 + (c1 + 1) * N - aq, l, kv_end);
             }
         }
     }
@@ -691,8 +735,7 @@ k1_packed(const __grid_constant__ K1cParams p) {
             ++bq;
             lq = max(lq, l);
             lostq |= (r.w & TP_REQ_LOST) != 0;
-            block_events(sv, 2 + (c1 + 1) * N - q, l, N, SL, P);
-            atomicAdd(&sv[ph(l + 1)], -(65536 + kv_end));
+            req_events(2 + (c1 + 1) * N - q, l, kv_end);
         }
         b1 += __reduce_add_sync(kFull, bq);
         kv1 += __reduce_add_sync(kFull, kvq);
@@ -704,10 +747,10 @@ k1_packed(const __grid_constant__ K1cParams p) {
     K1P_SYNC();
 
     // ---- inclusive scan of the packed words over the lane segments ----
+    // (write = false: only the lane's max of KV, the array is left as it is)
     int* seg = sv + lane * (S + P);
-    int kvmax = 0;
-    {
-        int sum = 0;
+    auto scan = [&](bool write) {
+        int kvm = 0, sum = 0;
         #pragma unroll 1
         for (int k = 0; k < S; k += 4) {
             const int4 v = *reinterpret_cast<const int4*>(seg + k);
@@ -725,11 +768,54 @@ k1_packed(const __grid_constant__ K1cParams p) {
             int4 v = *reinterpret_cast<const int4*>(seg + k);
             v.x += pre; v.y += v.x; v.z += v.y; v.w += v.z;
             pre = v.w;
-            *reinterpret_cast<int4*>(seg + k) = v;
+            if (write) *reinterpret_cast<int4*>(seg + k) = v;
             // KV[m] = 0 past every request's last iteration, so positions past H need no mask
-            kvmax = max(kvmax, max(max(v.x & 0xFFFF, v.y & 0xFFFF), max(v.z & 0xFFFF, v.w & 0xFFFF)));
+            kvm = max(kvm, max(max(v.x & 0xFFFF, v.y & 0xFFFF), max(v.z & 0xFFFF, v.w & 0xFFFF)));
+        }
+        return kvm;
+    };
+    const int forced = forced_of(p, i, nq);
+    const uint32_t lmask = p.lost_mask ? p.lost_mask[i] : 0u;
+    int c0 = 0;                                    // candidates admitted by the bound below
+#if TP_K1P_BATCHQ
+    // Bound prefix of the FIFO gate: with kvb0 = max_m KV[m] of the running set, candidate c is
+    // admitted by check 1 whenever kvb0 + sum_{c' <= c} ceil((q_c' + l_c' - 1) / N) <= kv_cap and
+    // B[1] + c + 1 <= max_batch (each admitted request adds at most its final block count at any
+    // m), so that prefix of the queue is admitted exactly as the one-at-a-time gate admits it and
+    // goes into the difference array as events (one read-only scan instead of a per-iteration add
+    // pass per candidate); the gate below continues at the first candidate the bound does not cover.
+    if (!allq && nq > 0 && forced < 0) {
+        const int kvb0 = warp_max(scan(false));
+        if (kvb0 <= in.kv_cap) {
+            const bool has = lane < nq;
+            const int4 r = has ? __ldg(&p.req[rb + nr + lane]) : make_int4(0, 1, 1, 0);   // a = 0 (validated)
+            const int q = r.y, l = r.z;
+            const int top = has ? (int)fdN.div((uint32_t)(q + l - 2)) + 1 : 0;
+            int cum = top;
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+                const int y = __shfl_up_sync(kFull, cum, o);
+                if (lane >= o) cum += y;
+            }
+            const bool okc = has && (int64_t)kvb0 + cum <= in.kv_cap && b1 + lane + 1 <= in.max_batch;
+            const uint32_t nok = ~__ballot_sync(kFull, okc);
+            c0 = nok ? __ffs(nok) - 1 : 32;
+            if (c0 > 0) {
+                K1P_SYNC();                            // every lane's read-only scan is done
+                const bool adm = lane < c0;
+                if (adm) {
+                    const int c1 = (int)fdN.div((uint32_t)(q - 1));
+                    req_events(2 + (c1 + 1) * N - q, l, top);
+                    atomicAdd(&sv[0], 65536 + c1 + 1);
+                }
+                nloc = max(nloc, warp_max(adm ? l : 0));
+                lost |= __any_sync(kFull, adm && ((r.w & TP_REQ_LOST) || ((lmask >> lane) & 1u)));
+                K1P_SYNC();
+            }
         }
     }
+#endif
+    const int kvmax = scan(true);
     K1P_SYNC();
     if (lane == 0 && nx.y > 0 && nx.z >= 0 && nx.x >= 0 && (int64_t)nx.x + nx.y + nx.z <= (int64_t)p.n_req) {
         const int64_t e0 = nx.x, e1 = e0 + nx.y + nx.z;
@@ -741,9 +827,7 @@ k1_packed(const __grid_constant__ K1cParams p) {
     uint32_t st = kvb > in.kv_cap ? TP_ST_KV_OVER : 0u;
 
     // ---- FIFO gate (as k1_compact: one candidate at a time over its window, exact bound shortcut) ----
-    int n_adm = allq ? nq : 0;
-    const int forced = forced_of(p, i, nq);
-    const uint32_t lmask = p.lost_mask ? p.lost_mask[i] : 0u;
+    int n_adm = allq ? nq : c0;
     const int ncand = allq ? 0 : forced >= 0 ? forced : nq;
     if (allq) {
         // the whole queue is in the histogram already
@@ -752,7 +836,7 @@ k1_packed(const __grid_constant__ K1cParams p) {
     } else {
         int B1 = sv[0] >> 16;
         #pragma unroll 1
-        for (int c = 0; c < ncand; ++c) {
+        for (int c = c0; c < ncand; ++c) {
             const int4 r = __ldg(&p.req[rb + nr + c]);
             const int q = r.y, lc = r.z;
             const int kvc_top = (int)fdN.div((uint32_t)(lc + q - 2)) + 1;
@@ -818,6 +902,16 @@ k1_packed(const __grid_constant__ K1cParams p) {
     // index of its piece -- which is what the Eq. 4 pass below looks up at every request's end.
     int h = 0, ends = 0;
     if (nn > 0) {
+        const int n_sched = nr + n_adm;
+#if TP_K1P_EQ4PF
+        // the Eq. 4 pass's first record and deadline of this lane, in flight during the piece passes
+        int2 qa = make_int2(0, 0);
+        double qt = 0.0;
+        if (lane < n_sched) {
+            qa = make_int2(__ldg(&p.req[rb + lane].x), __ldg(&p.req[rb + lane].z));
+            qt = __ldg(&p.t_dead[rb + lane]);
+        }
+#endif
         const int nKV = p.cut_off[3] - p.cut_off[2];
         const uint32_t nk1 = (uint32_t)nKV + 1;
         const uint32_t rtp = TP_K1P_RTP && (uint32_t)in.tp < 64u ? s_rtp[in.tp]
@@ -846,7 +940,6 @@ k1_packed(const __grid_constant__ K1cParams p) {
         int32_t* const rec_m = p.run_m + row;
         uint32_t* const rec_k = p.run_key + row;
         long long* const D = p.end_d + row;
-        const int n_sched = nr + n_adm;
         int cnt = 0, e = 0;
         if (S2 <= 32) {
             // Mask form (n <= 1024): pass A leaves each iteration's cell key in place and sets bit
@@ -905,16 +998,58 @@ k1_packed(const __grid_constant__ K1cParams p) {
             // last iteration l is piece k's tail of ceil(fl64(t_dead - t_cur) * 2^40) (A-12), by a
             // fire-and-forget RED.MIN.S64 (a shared 64-bit atomicMin is a CAS loop)
             const uint32_t inv = ((1u << 20) + (uint32_t)S2 - 1) / (uint32_t)S2;   // (l-1)/S2, l-1 < 1024
+#if TP_K1P_EQ4PF && TP_K1P_EQ4B > 1
+            // batches of TP_K1P_EQ4B records per lane: the batch's loads are issued together (the
+            // first one was loaded before the piece passes)
+            #pragma unroll 1
+            for (int j0 = lane; j0 < n_sched; j0 += 32 * TP_K1P_EQ4B) {
+                int2 ab[TP_K1P_EQ4B];
+                double tb[TP_K1P_EQ4B];
+#pragma unroll
+                for (int u = 0; u < TP_K1P_EQ4B; ++u) {
+                    const int j = j0 + 32 * u;
+                    ab[u] = make_int2(0, 1);
+                    tb[u] = 0.0;
+                    if (u == 0 && j0 == lane) {
+                        ab[0] = qa;
+                        tb[0] = qt;
+                    } else if (j < n_sched) {
+                        ab[u] = make_int2(__ldg(&p.req[rb + j].x), __ldg(&p.req[rb + j].z));
+                        tb[u] = __ldg(&p.t_dead[rb + j]);
+                    }
+                }
+#pragma unroll
+                for (int u = 0; u < TP_K1P_EQ4B; ++u) {
+                    if (j0 + 32 * u >= n_sched) break;
+                    const int l1 = ab[u].y - ab[u].x - 1;   // 0 <= l - 1 < nn (validated; n = max l)
+                    const long long d = slack_ticks(tb[u] - in.t_cur, p.tick_shift);
+                    const int t = (int)(((uint32_t)l1 * inv) >> 20);
+                    const int jj = l1 - t * S2;
+                    const int k = sv[t] + __popc((uint32_t)sv[32 + t] & (0xffffffffu >> (31 - jj))) - 1;
+                    if (d != kNoDeadline) atomicMin(ptr_at(D, (unsigned)k), d);
+                }
+            }
+#else
             #pragma unroll 1
             for (int j = lane; j < n_sched; j += 32) {
+#if TP_K1P_EQ4PF
+                const int l1 = qa.y - qa.x - 1;       // 0 <= l - 1 < nn (validated; n = max l)
+                const long long d = slack_ticks(qt - in.t_cur, p.tick_shift);
+                if (j + 32 < n_sched) {
+                    qa = make_int2(__ldg(&p.req[rb + j + 32].x), __ldg(&p.req[rb + j + 32].z));
+                    qt = __ldg(&p.t_dead[rb + j + 32]);
+                }
+#else
                 const int4 r = __ldg(&p.req[rb + j]);
                 const int l1 = r.z - r.x - 1;         // 0 <= l - 1 < nn (validated; n = max l)
                 const long long d = slack_ticks(__ldg(&p.t_dead[rb + j]) - in.t_cur, p.tick_shift);
+#endif
                 const int t = (int)(((uint32_t)l1 * inv) >> 20);
                 const int jj = l1 - t * S2;
                 const int k = sv[t] + __popc((uint32_t)sv[32 + t] & (0xffffffffu >> (31 - jj))) - 1;
                 if (d != kNoDeadline) atomicMin(ptr_at(D, (unsigned)k), d);
             }
+#endif
         } else {
             // Per-iteration form (long horizons): pass A leaves key | head << 30 | fresh << 31 in
             // place, pass B writes the records and leaves each iteration's piece index in place.
