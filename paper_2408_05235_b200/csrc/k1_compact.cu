@@ -535,7 +535,10 @@ __device__ __forceinline__ void k1_body(const K1cParams& p, const int i, Group<W
 // Eq. 4 table is built in windows of the histogram space.  Instances the check rejects are handed
 // to k1_compact<1, true> through the flag list.
 #ifndef TP_K1P_WARPS
-#define TP_K1P_WARPS 14      // warps (instances in flight) per CTA (named barriers 1..15)
+// warps (instances in flight) per CTA (named barriers 1..15).  12: three CTAs of 12 warps at 48
+// registers fill each SM sub-partition's 16 K registers with 9 warps (36 per SM); 13 or 14 put
+// 4 warps of every CTA on sub-partition 0, so only two CTAs fit (26-28 warps)
+#define TP_K1P_WARPS 12
 #endif
 #ifndef TP_K1P_RTP
 #define TP_K1P_RTP 1         // engine-size ranks from a per-CTA table (0: a binary search per instance)
@@ -545,6 +548,9 @@ __device__ __forceinline__ void k1_body(const K1cParams& p, const int i, Group<W
 #endif
 #ifndef TP_K1P_EQ4PF
 #define TP_K1P_EQ4PF 1       // Eq. 4 pass: the lane's first record + deadline loaded before the piece passes
+#endif
+#ifndef TP_K1P_ST
+#define TP_K1P_ST 1          // rank tables staged in shared memory when they fit (0: read through L1)
 #endif
 #ifndef TP_K1P_BATCHQ
 #define TP_K1P_BATCHQ 1      // the bound-covered prefix of the FIFO queue admitted as events before the scan
@@ -556,7 +562,7 @@ __device__ __forceinline__ void k1_body(const K1cParams& p, const int i, Group<W
 #define TP_K1P_MAXREG 48     // > 0: register cap instead of the CTAs-per-SM launch bound (48 x 42 warps fill the file)
 #endif
 #ifndef TP_K1P_MINB
-#define TP_K1P_MINB 3        // CTAs per SM: 3 x (14 x 4.6 KB + 9 KB of tables) at H = 1024
+#define TP_K1P_MINB 3        // CTAs per SM when TP_K1P_MAXREG = 0 (3 x (12 x 4.6 KB + 9 KB of tables) at H = 1024)
 #endif
 
 // one warp's named barrier (see Group::sync); the id is a register (k1_packed uses up to 15 of them
@@ -1231,8 +1237,8 @@ int launch_packed(const K1cParams& p0, int32_t n_inst, int32_t H, cudaStream_t s
     // rank tables in shared memory when they are small next to the histograms (the model's cut sets)
     const int tab_entries = p.rtab_off[1] + p.rtab_len[1];
     const size_t tab_bytes = ((size_t)tab_entries * 2 + 15) & ~(size_t)15;
-    constexpr size_t kCtaSmem = 75 * 1024;            // TP_K1P_MINB CTAs per SM
-    const bool st = tab_bytes <= 32 * 1024 && tab_bytes + per_warp <= kCtaSmem;
+    constexpr size_t kCtaSmem = 75 * 1024;            // three CTAs per SM
+    const bool st = TP_K1P_ST && tab_bytes <= 32 * 1024 && tab_bytes + per_warp <= kCtaSmem;
     p.tab_words = st ? (int32_t)(tab_bytes / 4) : 0;
     const size_t room = st ? kCtaSmem - tab_bytes : (size_t)100 * 1024;
     const int wpb = (int)std::max<size_t>(1, std::min<size_t>(TP_K1P_WARPS, room / per_warp));
