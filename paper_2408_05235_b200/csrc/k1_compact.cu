@@ -552,6 +552,15 @@ __device__ __forceinline__ void k1_body(const K1cParams& p, const int i, Group<W
 #ifndef TP_K1P_ST
 #define TP_K1P_ST 1          // rank tables staged in shared memory when they fit (0: read through L1)
 #endif
+#ifndef TP_K1P_BCACHE
+#define TP_K1P_BCACHE 0      // B rank looked up only where B changes (predicated shared load)
+#endif
+#ifndef TP_K1P_ZDIRTY
+#define TP_K1P_ZDIRTY 1      // clear only the prefix of the histogram the previous instance wrote
+#endif
+#ifndef TP_K1P_MERGE
+#define TP_K1P_MERGE 1       // scan + pass A in one pass when no FIFO candidate is left for the gate
+#endif
 #ifndef TP_K1P_BATCHQ
 #define TP_K1P_BATCHQ 1      // the bound-covered prefix of the FIFO queue admitted as events before the scan
 #endif
@@ -621,6 +630,7 @@ k1_packed(const __grid_constant__ K1cParams p) {
     }
     const int SL = p.S_log2, S = 1 << SL, P = p.P, H = p.H;
     auto ph = [&](int m) { return (m - 1) + P * ((m - 1) >> SL); };   // physical index of m >= 1
+    int zhi = p.arr;                                  // words of sv to clear for the next instance
 #pragma unroll 1
     for (int i = blockIdx.x * wpb + w; i < p.n_inst; i += gridDim.x * wpb) {
     K1P_SYNC();                                       // the previous instance's reads of sv are done
@@ -641,7 +651,7 @@ k1_packed(const __grid_constant__ K1cParams p) {
     int4 nx = make_int4(0, 0, 0, 0);
     if (lane == 0 && inext < p.n_inst) nx = __ldg(reinterpret_cast<const int4*>(p.inst + inext) + 1);
     #pragma unroll 1
-    for (int k = lane * 4; k + 3 < p.arr; k += 128) *reinterpret_cast<int4*>(sv + k) = make_int4(0, 0, 0, 0);
+    for (int k = lane * 4; k + 3 < zhi; k += 128) *reinterpret_cast<int4*>(sv + k) = make_int4(0, 0, 0, 0);
     K1P_SYNC();
 
     bool bad = N < 1 || in.tp < 1 || (int64_t)in.tp >= kFeatLimit || nr < 0 || nq < 0 || in.kv_cap < 0 ||
@@ -701,6 +711,7 @@ k1_packed(const __grid_constant__ K1cParams p) {
     bad = bad || foot >= kFeatLimit;
     if (!bad && (nr + nq >= 32768 || foot >= 65536)) {       // does not fit the packed words
         if (lane == 0) p.flag_list[atomicAdd(p.flag_count, 1) + 1] = i;   // flag_count holds count - 1
+        zhi = p.arr;
         continue;
     }
     if (bad) {
@@ -719,6 +730,7 @@ k1_packed(const __grid_constant__ K1cParams p) {
             if (p.run_h) p.run_h[i] = 0;
             if (p.end_n) p.end_n[i] = 0;
         }
+        zhi = p.arr;
         continue;
     }
     // Whole-queue admission: when the footprint of running + queued fits the capacity and the
@@ -783,6 +795,7 @@ k1_packed(const __grid_constant__ K1cParams p) {
     const int forced = forced_of(p, i, nq);
     const uint32_t lmask = p.lost_mask ? p.lost_mask[i] : 0u;
     int c0 = 0;                                    // candidates admitted by the bound below
+    int kvb0 = -1;                                 // max_m KV[m] of the running set (bound prefix)
 #if TP_K1P_BATCHQ
     // Bound prefix of the FIFO gate: with kvb0 = max_m KV[m] of the running set, candidate c is
     // admitted by check 1 whenever kvb0 + sum_{c' <= c} ceil((q_c' + l_c' - 1) / N) <= kv_cap and
@@ -791,7 +804,7 @@ k1_packed(const __grid_constant__ K1cParams p) {
     // goes into the difference array as events (one read-only scan instead of a per-iteration add
     // pass per candidate); the gate below continues at the first candidate the bound does not cover.
     if (!allq && nq > 0 && forced < 0) {
-        const int kvb0 = warp_max(scan(false));
+        kvb0 = warp_max(scan(false));
         if (kvb0 <= in.kv_cap) {
             const bool has = lane < nq;
             const int4 r = has ? __ldg(&p.req[rb + nr + lane]) : make_int4(0, 1, 1, 0);   // a = 0 (validated)
@@ -821,7 +834,106 @@ k1_packed(const __grid_constant__ K1cParams p) {
         }
     }
 #endif
-    const int kvmax = scan(true);
+    // cell key of a histogram word (b < 2^15, kv < 2^16 here, the packed check: the clamped table
+    // lookups are exact) and the piece-pass segment length S2 for n iterations: a multiple of 4
+    // (odd multiples preferred: conflict-free 128-bit accesses at lane stride S2), so each lane's
+    // segment starts 4-aligned and every 4-iteration batch is one aligned int4 of the padded layout
+    // (segments of the scan layout are multiples of 4 long)
+    const uint32_t nk1 = (uint32_t)(p.cut_off[3] - p.cut_off[2]) + 1;
+    auto key_of = [&](int v) -> uint32_t {
+        if constexpr (ST) return (uint32_t)tB[min(v >> 16, lB1)] * nk1 + tKV[min(v & 0xFFFF, lKV1)];
+        return (uint32_t)__ldg(ptr_at(tB, (unsigned)min(v >> 16, lB1))) * nk1 +
+               __ldg(ptr_at(tKV, (unsigned)min(v & 0xFFFF, lKV1)));
+    };
+    // B rank of a batch size (the rank of m - 1 is kept: B changes only at end positions, so the
+    // lookup is predicated off in most lanes -- fewer shared wavefronts)
+    auto rank_b = [&](int b) -> uint32_t {
+        if constexpr (ST) return tB[min(b, lB1)];
+        return __ldg(ptr_at(tB, (unsigned)min(b, lB1)));
+    };
+    auto key_next = [&](int w, int b, int pb, uint32_t& prB) -> uint32_t {
+#if TP_K1P_BCACHE
+        if (b != pb) prB = rank_b(b);
+        if constexpr (ST) return prB * nk1 + tKV[min(w & 0xFFFF, lKV1)];
+        return prB * nk1 + __ldg(ptr_at(tKV, (unsigned)min(w & 0xFFFF, lKV1)));
+#else
+        (void)b; (void)pb; (void)prB;
+        return key_of(w);
+#endif
+    };
+    auto s2_of = [](int nn) {
+        int S2 = (((nn + 31) >> 5) + 3) & ~3;
+        if ((S2 & 4) == 0 && 32 * (S2 - 4) < nn && S2 + 4 <= 32) S2 += 4;
+        return S2;
+    };
+    // Merged scan + pass A: when no FIFO candidate is left for the gate below (no queue, the whole
+    // queue admitted, the bound prefix covering it, or the queue blocked by KV_OVER), n is final
+    // before the scan, so the scan runs over the piece-pass segments (lane t: m in
+    // [1 + t S2, (t+1) S2], n <= 1024) and its second pass computes the keys and head / end flags
+    // of pass A on the scanned words in registers: one read + write of each word instead of two,
+    // and the neighbour's last word is the lane's exclusive prefix (no shared read).  Values past n
+    // are 0 (every request has ended), so the KV max needs no mask.  Not with full B/KV rows out.
+    int kvmax = 0, v1 = 0;                         // v1: the word of m = 1 (merged)
+    uint32_t mmask = 0;                            // merged: the lane's head mask and end count
+    int me = 0;
+#if TP_K1P_MERGE
+    const bool merged = !(p.B && p.bkv_rows) && s2_of(nloc) <= 32 &&
+                        (nq == 0 || allq || (forced < 0 && (kvb0 > in.kv_cap || c0 >= nq)));
+#else
+    const bool merged = false;
+#endif
+    if (merged) {
+        const int S2 = s2_of(nloc);
+        const int mlo = 1 + lane * S2, mhi = min(mlo + S2 - 1, nloc);   // empty when mlo > n
+        int sum = 0;
+        #pragma unroll 1
+        for (int m0 = mlo; m0 <= mhi; m0 += 4) {
+            const int4 v = *reinterpret_cast<const int4*>(sv + ph(m0));
+            sum += v.x + v.y + v.z + v.w;
+        }
+        int x = sum;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const int y = __shfl_up_sync(kFull, x, o);
+            if (lane >= o) x += y;
+        }
+        int pre = x - sum;                         // the word of mlo - 1
+        uint32_t pk = 0xffffffffu;                 // key / B of m - 1 (m = 1 always starts a piece)
+        int pb = 0;
+        if (mlo >= 2 && mlo <= nloc) {
+            pb = pre >> 16;
+            pk = key_of(pre);
+        }
+        uint32_t prB = rank_b(pb);                 // B rank of m - 1
+        #pragma unroll 1
+        for (int m0 = mlo; m0 <= mhi; m0 += 4) {
+            int4* const q = reinterpret_cast<int4*>(sv + ph(m0));
+            int4 v = *q;
+            v.x += pre; v.y += v.x; v.z += v.y; v.w += v.z;
+            pre = v.w;
+            kvmax = max(kvmax, max(max(v.x & 0xFFFF, v.y & 0xFFFF), max(v.z & 0xFFFF, v.w & 0xFFFF)));
+            if (m0 == 1) v1 = v.x;
+            const uint32_t bit = 1u << (m0 - mlo);
+            auto flag = [&](int& w, uint32_t bu, bool live) {   // as pass A below
+                const int b = w >> 16;
+                const uint32_t k = key_next(w, b, pb, prB);
+                const bool endp = live && b < pb;
+                const bool head = live && (k != pk || endp);
+                mmask |= head ? bu : 0u;
+                me += endp;
+                w = (int)k;
+                pk = k;
+                pb = b;
+            };
+            flag(v.x, bit, true);
+            flag(v.y, bit << 1, m0 + 1 <= mhi);
+            flag(v.z, bit << 2, m0 + 2 <= mhi);
+            flag(v.w, bit << 3, m0 + 3 <= mhi);
+            *q = v;
+        }
+    } else {
+        kvmax = scan(true);
+    }
     K1P_SYNC();
     if (lane == 0 && nx.y > 0 && nx.z >= 0 && nx.x >= 0 && (int64_t)nx.x + nx.y + nx.z <= (int64_t)p.n_req) {
         const int64_t e0 = nx.x, e1 = e0 + nx.y + nx.z;
@@ -887,7 +999,7 @@ k1_packed(const __grid_constant__ K1cParams p) {
         const int lim = p.bkv_rows ? H : 1;
         #pragma unroll 1
         for (int m = 1 + lane; m <= lim; m += 32) {
-            const int v = sv[ph(m)];
+            const int v = merged ? v1 : sv[ph(m)];    // merged: lim = 1, lane 0 holds m = 1
             Bo[m - 1] = v >> 16;
             Ko[m - 1] = v & 0xFFFF;
         }
@@ -918,30 +1030,19 @@ k1_packed(const __grid_constant__ K1cParams p) {
             qt = __ldg(&p.t_dead[rb + lane]);
         }
 #endif
-        const int nKV = p.cut_off[3] - p.cut_off[2];
-        const uint32_t nk1 = (uint32_t)nKV + 1;
         const uint32_t rtp = TP_K1P_RTP && (uint32_t)in.tp < 64u ? s_rtp[in.tp]
                                                      : rank_of(p.cuts + p.cut_off[0], p.cut_off[1] - p.cut_off[0], (float)in.tp);
         const uint32_t cell_base = rtp * (uint32_t)(p.cut_off[2] - p.cut_off[1] + 1) * nk1;
-        // b < 2^15, kv < 2^16 here (the packed check): the clamped table lookups are exact
-        auto key_of = [&](int v) -> uint32_t {
-            if constexpr (ST) return (uint32_t)tB[min(v >> 16, lB1)] * nk1 + tKV[min(v & 0xFFFF, lKV1)];
-            return (uint32_t)__ldg(ptr_at(tB, (unsigned)min(v >> 16, lB1))) * nk1 +
-                   __ldg(ptr_at(tKV, (unsigned)min(v & 0xFFFF, lKV1)));
-        };
-        // S2: a multiple of 4 (odd multiples preferred: conflict-free 128-bit accesses at lane stride
-        // S2), so each lane's segment starts 4-aligned and every 4-iteration batch is one aligned
-        // int4 of the padded layout (segments of the scan layout are multiples of 4 long)
-        int S2 = (((nn + 31) >> 5) + 3) & ~3;
-        if ((S2 & 4) == 0 && 32 * (S2 - 4) < nn && S2 + 4 <= 32) S2 += 4;
+        const int S2 = s2_of(nn);
         const int mlo = 1 + lane * S2, mhi = min(mlo + S2 - 1, nn);     // empty when mlo > nn
         uint32_t pk = 0xffffffffu;                   // key / B of m - 1 (m = 1 always starts a piece)
         int pb = 0;
-        if (mlo >= 2 && mlo <= nn) {
+        if (!merged && mlo >= 2 && mlo <= nn) {
             const int v = sv[ph(mlo - 1)];
             pb = v >> 16;
             pk = key_of(v);
         }
+        uint32_t prB = rank_b(pb);                   // B rank of m - 1
         K1P_SYNC();                                   // every neighbour read before the in-place writes
         int32_t* const rec_m = p.run_m + row;
         uint32_t* const rec_k = p.run_key + row;
@@ -952,15 +1053,16 @@ k1_packed(const __grid_constant__ K1cParams p) {
             // m - mlo of the lane's head mask; pass B visits only the set bits (one record per head,
             // not a pass per iteration), and the piece of an iteration l is base[t] + popc(mask[t]
             // up to l) - 1 (t the lane owning l), both left in the first 64 words for Eq. 4.
-            uint32_t mask = 0;
+            uint32_t mask = mmask;                    // merged: pass A is done
+            e = me;
             #pragma unroll 1
-            for (int m0 = mlo; m0 <= mhi; m0 += 4) {
+            for (int m0 = mlo; m0 <= (merged ? 0 : mhi); m0 += 4) {
                 int4* const q = reinterpret_cast<int4*>(sv + ph(m0));
                 int4 v = *q;
                 const uint32_t bit = 1u << (m0 - mlo);
                 auto flag = [&](int& x, uint32_t bu, bool live) {   // x: the histogram word of m
-                    const uint32_t k = key_of(x);
                     const int b = x >> 16;
+                    const uint32_t k = key_next(x, b, pb, prB);
                     const bool endp = live && b < pb;         // m - 1 is an end position
                     const bool head = live && (k != pk || endp);
                     mask |= head ? bu : 0u;
@@ -1127,6 +1229,12 @@ k1_packed(const __grid_constant__ K1cParams p) {
         p.run_h[i] = h;
         p.end_n[i] = nn > 0 ? ends + 1 : 0;           // + m = nn, always an end
     }
+#if TP_K1P_ZDIRTY
+    // words this instance can have written: events at <= n + 1, in-place keys / piece indices of
+    // 4-iteration batches at <= n + 3, bases and masks in the first 64; everything past them is
+    // still 0 (the scanned words past n + 1 are 0), so the next instance clears only this prefix
+    zhi = min(p.arr, max(64, (ph(min(n + 4, H + 1)) + 4) & ~3));
+#endif
     }
 }
 
