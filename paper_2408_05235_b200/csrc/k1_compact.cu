@@ -552,9 +552,6 @@ __device__ __forceinline__ void k1_body(const K1cParams& p, const int i, Group<W
 #ifndef TP_K1P_ST
 #define TP_K1P_ST 1          // rank tables staged in shared memory when they fit (0: read through L1)
 #endif
-#ifndef TP_K1P_BCACHE
-#define TP_K1P_BCACHE 0      // B rank looked up only where B changes (predicated shared load)
-#endif
 #ifndef TP_K1P_ZDIRTY
 #define TP_K1P_ZDIRTY 1      // clear only the prefix of the histogram the previous instance wrote
 #endif
@@ -845,22 +842,6 @@ k1_packed(const __grid_constant__ K1cParams p) {
         return (uint32_t)__ldg(ptr_at(tB, (unsigned)min(v >> 16, lB1))) * nk1 +
                __ldg(ptr_at(tKV, (unsigned)min(v & 0xFFFF, lKV1)));
     };
-    // B rank of a batch size (the rank of m - 1 is kept: B changes only at end positions, so the
-    // lookup is predicated off in most lanes -- fewer shared wavefronts)
-    auto rank_b = [&](int b) -> uint32_t {
-        if constexpr (ST) return tB[min(b, lB1)];
-        return __ldg(ptr_at(tB, (unsigned)min(b, lB1)));
-    };
-    auto key_next = [&](int w, int b, int pb, uint32_t& prB) -> uint32_t {
-#if TP_K1P_BCACHE
-        if (b != pb) prB = rank_b(b);
-        if constexpr (ST) return prB * nk1 + tKV[min(w & 0xFFFF, lKV1)];
-        return prB * nk1 + __ldg(ptr_at(tKV, (unsigned)min(w & 0xFFFF, lKV1)));
-#else
-        (void)b; (void)pb; (void)prB;
-        return key_of(w);
-#endif
-    };
     auto s2_of = [](int nn) {
         int S2 = (((nn + 31) >> 5) + 3) & ~3;
         if ((S2 & 4) == 0 && 32 * (S2 - 4) < nn && S2 + 4 <= 32) S2 += 4;
@@ -904,7 +885,6 @@ k1_packed(const __grid_constant__ K1cParams p) {
             pb = pre >> 16;
             pk = key_of(pre);
         }
-        uint32_t prB = rank_b(pb);                 // B rank of m - 1
         #pragma unroll 1
         for (int m0 = mlo; m0 <= mhi; m0 += 4) {
             int4* const q = reinterpret_cast<int4*>(sv + ph(m0));
@@ -915,8 +895,8 @@ k1_packed(const __grid_constant__ K1cParams p) {
             if (m0 == 1) v1 = v.x;
             const uint32_t bit = 1u << (m0 - mlo);
             auto flag = [&](int& w, uint32_t bu, bool live) {   // as pass A below
+                const uint32_t k = key_of(w);
                 const int b = w >> 16;
-                const uint32_t k = key_next(w, b, pb, prB);
                 const bool endp = live && b < pb;
                 const bool head = live && (k != pk || endp);
                 mmask |= head ? bu : 0u;
@@ -1042,7 +1022,6 @@ k1_packed(const __grid_constant__ K1cParams p) {
             pb = v >> 16;
             pk = key_of(v);
         }
-        uint32_t prB = rank_b(pb);                   // B rank of m - 1
         K1P_SYNC();                                   // every neighbour read before the in-place writes
         int32_t* const rec_m = p.run_m + row;
         uint32_t* const rec_k = p.run_key + row;
@@ -1061,8 +1040,8 @@ k1_packed(const __grid_constant__ K1cParams p) {
                 int4 v = *q;
                 const uint32_t bit = 1u << (m0 - mlo);
                 auto flag = [&](int& x, uint32_t bu, bool live) {   // x: the histogram word of m
+                    const uint32_t k = key_of(x);
                     const int b = x >> 16;
-                    const uint32_t k = key_next(x, b, pb, prB);
                     const bool endp = live && b < pb;         // m - 1 is an end position
                     const bool head = live && (k != pk || endp);
                     mask |= head ? bu : 0u;
