@@ -552,6 +552,9 @@ __device__ __forceinline__ void k1_body(const K1cParams& p, const int i, Group<W
 #ifndef TP_K1P_ST
 #define TP_K1P_ST 1          // rank tables staged in shared memory when they fit (0: read through L1)
 #endif
+#ifndef TP_K1P_LINEAR
+#define TP_K1P_LINEAR 1      // unpadded histogram, scans over the S2 lane segments
+#endif
 #ifndef TP_K1P_ZDIRTY
 #define TP_K1P_ZDIRTY 1      // clear only the prefix of the histogram the previous instance wrote
 #endif
@@ -625,7 +628,10 @@ k1_packed(const __grid_constant__ K1cParams p) {
         tB = p.rtab + p.rtab_off[0];
         tKV = p.rtab + p.rtab_off[1];
     }
-    const int SL = p.S_log2, S = 1 << SL, P = p.P, H = p.H;
+    // TP_K1P_LINEAR: the histogram is unpadded (ph(m) = m - 1); every 128-bit pass walks the
+    // S2-word lane segments, S2 / 4 odd where possible, so 8 consecutive lanes hit 8 distinct
+    // 16-byte bank groups (the padded layout made the S2 passes 2-6-way conflicted)
+    const int SL = p.S_log2, S = 1 << SL, P = TP_K1P_LINEAR ? 0 : p.P, H = p.H;
     auto ph = [&](int m) { return (m - 1) + P * ((m - 1) >> SL); };   // physical index of m >= 1
     int zhi = p.arr;                                  // words of sv to clear for the next instance
 #pragma unroll 1
@@ -761,8 +767,48 @@ k1_packed(const __grid_constant__ K1cParams p) {
     if (lane == 0) sv[0] += b1 * 65536 + kv1;     // the m = 1 terms (index 0 gets no other event)
     K1P_SYNC();
 
+    // piece-pass segment length S2 for n iterations: a multiple of 4 (odd multiples preferred:
+    // conflict-free 128-bit accesses at lane stride S2), so each lane's segment starts 4-aligned
+    // and every 4-iteration batch is one aligned int4 (segments of the padded layout are
+    // multiples of 4 long); 32 S2 <= arr for n <= H
+    auto s2_of = [](int nn) {
+        int S2 = (((nn + 31) >> 5) + 3) & ~3;
+        if ((S2 & 4) == 0 && 32 * (S2 - 4) < nn && S2 + 4 <= 32) S2 += 4;
+        return S2;
+    };
     // ---- inclusive scan of the packed words over the lane segments ----
     // (write = false: only the lane's max of KV, the array is left as it is)
+#if TP_K1P_LINEAR
+    // over the S2 segments of min(n + 1, H) iterations: every event is at m <= n + 1, and the
+    // words past the segments are 0 (nothing was written there)
+    auto scan = [&](bool write) {
+        const int S2s = s2_of(min(nloc + 1, H));
+        int* const seg = sv + lane * S2s;
+        int kvm = 0, sum = 0;
+        #pragma unroll 1
+        for (int k = 0; k < S2s; k += 4) {
+            const int4 v = *reinterpret_cast<const int4*>(seg + k);
+            sum += v.x + v.y + v.z + v.w;
+        }
+        int x = sum;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const int y = __shfl_up_sync(kFull, x, o);
+            if (lane >= o) x += y;
+        }
+        int pre = x - sum;
+        #pragma unroll 1
+        for (int k = 0; k < S2s; k += 4) {
+            int4 v = *reinterpret_cast<const int4*>(seg + k);
+            v.x += pre; v.y += v.x; v.z += v.y; v.w += v.z;
+            pre = v.w;
+            if (write) *reinterpret_cast<int4*>(seg + k) = v;
+            // KV[m] = 0 past every request's last iteration, so positions past H need no mask
+            kvm = max(kvm, max(max(v.x & 0xFFFF, v.y & 0xFFFF), max(v.z & 0xFFFF, v.w & 0xFFFF)));
+        }
+        return kvm;
+    };
+#else
     int* seg = sv + lane * (S + P);
     auto scan = [&](bool write) {
         int kvm = 0, sum = 0;
@@ -789,6 +835,7 @@ k1_packed(const __grid_constant__ K1cParams p) {
         }
         return kvm;
     };
+#endif
     const int forced = forced_of(p, i, nq);
     const uint32_t lmask = p.lost_mask ? p.lost_mask[i] : 0u;
     int c0 = 0;                                    // candidates admitted by the bound below
@@ -841,11 +888,6 @@ k1_packed(const __grid_constant__ K1cParams p) {
         if constexpr (ST) return (uint32_t)tB[min(v >> 16, lB1)] * nk1 + tKV[min(v & 0xFFFF, lKV1)];
         return (uint32_t)__ldg(ptr_at(tB, (unsigned)min(v >> 16, lB1))) * nk1 +
                __ldg(ptr_at(tKV, (unsigned)min(v & 0xFFFF, lKV1)));
-    };
-    auto s2_of = [](int nn) {
-        int S2 = (((nn + 31) >> 5) + 3) & ~3;
-        if ((S2 & 4) == 0 && 32 * (S2 - 4) < nn && S2 + 4 <= 32) S2 += 4;
-        return S2;
     };
     // Merged scan + pass A: when no FIFO candidate is left for the gate below (no queue, the whole
     // queue admitted, the bound prefix covering it, or the queue blocked by KV_OVER), n is final
