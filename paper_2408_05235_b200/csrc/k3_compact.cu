@@ -32,7 +32,10 @@ constexpr unsigned kFull = 0xffffffffu;
 #define TP_K3C_PD 4         // pieces ahead: T' loads in flight per warp
 #endif
 #ifndef TP_K3C_MINB
-#define TP_K3C_MINB 5       // W = 1: CTAs (8 warps) per SM
+#define TP_K3C_MINB 6       // W = 1: CTAs (8 warps) per SM (40 registers with TP_K3C_RING: 12 warps per sub-partition)
+#endif
+#ifndef TP_K3C_RING
+#define TP_K3C_RING 1       // SINGLE: only the T' values in the prefetch ring (len / Dmin re-read from shared)
 #endif
 #ifndef TP_K3C_SINGLE
 #define TP_K3C_SINGLE 1     // one record buffer per warp (refilled per chunk) vs double-buffered
@@ -191,6 +194,26 @@ k3_compact(const __grid_constant__ K3cParams p) {
             stage(buf);
             wsync();
             const int cnt = min(32, kz - kb);
+#if TP_K3C_RING
+            // only the T' loads ride in registers; len and Dmin are re-read from the staged record
+            // when the piece is walked (a broadcast shared load): 16 registers fewer
+            TV rt[PD];
+#pragma unroll
+            for (int j = 0; j < PD; ++j) rt[j] = lut_load(tab_at(col, (unsigned)buf[j].x));
+            auto group = [&](int q0, auto more) {
+#pragma unroll
+                for (int j = 0; j < PD; ++j) {
+                    TV tn = 0;
+                    if constexpr (decltype(more)::value) tn = lut_load(tab_at(col, (unsigned)buf[q0 + PD + j].x));
+                    const int4 r = buf[q0 + j];
+                    const unsigned long long dd = ((unsigned long long)(unsigned)r.w << 32) | (unsigned)r.z;
+                    T = mad_len(T, (unsigned)r.y, rt[j]);   // T_R at this piece's tail (Eq. 3)
+                    if (W == 1) ok &= T < dd;                 // Eq. 4, strict (Dmin >= 0: unsigned compare)
+                    else M = min(M, (long long)dd - (long long)T);
+                    if constexpr (decltype(more)::value) rt[j] = tn;
+                }
+            };
+#else
             TV rt[PD];
             unsigned rl[PD];
             unsigned long long rd[PD];
@@ -220,6 +243,7 @@ k3_compact(const __grid_constant__ K3cParams p) {
                     }
                 }
             };
+#endif
             int q0 = 0;
             for (; q0 + PD < cnt; q0 += PD) group(q0, std::true_type{});
             group(q0, std::false_type{});             // the last group: padding past cnt is a no-op
