@@ -896,7 +896,7 @@ k1_packed(const __grid_constant__ K1cParams p) {
     // of pass A on the scanned words in registers: one read + write of each word instead of two,
     // and the neighbour's last word is the lane's exclusive prefix (no shared read).  Values past n
     // are 0 (every request has ended), so the KV max needs no mask.  Not with full B/KV rows out.
-    int kvmax = 0;
+    int kvmax = 0, v1 = 0;                         // v1: the word of m = 1 (merged)
     uint32_t mmask = 0;                            // merged: the lane's head mask and end count
     int me = 0;
 #if TP_K1P_MERGE
@@ -934,10 +934,7 @@ k1_packed(const __grid_constant__ K1cParams p) {
             v.x += pre; v.y += v.x; v.z += v.y; v.w += v.z;
             pre = v.w;
             kvmax = max(kvmax, max(max(v.x & 0xFFFF, v.y & 0xFFFF), max(v.z & 0xFFFF, v.w & 0xFFFF)));
-            if (p.B && m0 == 1) {                  // the m = 1 row (merged: lim = 1 below)
-                p.B[(int64_t)i * H] = v.x >> 16;
-                p.KV[(int64_t)i * H] = v.x & 0xFFFF;
-            }
+            if (m0 == 1) v1 = v.x;
             const uint32_t bit = 1u << (m0 - mlo);
             auto flag = [&](int& w, uint32_t bu, bool live) {   // as pass A below
                 const uint32_t k = key_of(w);
@@ -1018,13 +1015,13 @@ k1_packed(const __grid_constant__ K1cParams p) {
     else if (lost) st |= TP_ST_BYPASS_LOST;
     K1P_SYNC();
 
-    if (p.B && !merged) {                          // (merged: the m = 1 row is written)
+    if (p.B) {
         int* Bo = p.B + (int64_t)i * H;
         int* Ko = p.KV + (int64_t)i * H;
         const int lim = p.bkv_rows ? H : 1;
         #pragma unroll 1
         for (int m = 1 + lane; m <= lim; m += 32) {
-            const int v = sv[ph(m)];
+            const int v = merged ? v1 : sv[ph(m)];    // merged: lim = 1, lane 0 holds m = 1
             Bo[m - 1] = v >> 16;
             Ko[m - 1] = v & 0xFFFF;
         }
