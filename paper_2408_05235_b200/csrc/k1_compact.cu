@@ -555,6 +555,9 @@ __device__ __forceinline__ void k1_body(const K1cParams& p, const int i, Group<W
 #ifndef TP_K1P_LINEAR
 #define TP_K1P_LINEAR 1      // unpadded histogram, scans over the S2 lane segments
 #endif
+#ifndef TP_K1P_BALB
+#define TP_K1P_BALB 1        // pass B records distributed round-robin over the lanes
+#endif
 #ifndef TP_K1P_ZDIRTY
 #define TP_K1P_ZDIRTY 1      // clear only the prefix of the histogram the previous instance wrote
 #endif
@@ -1108,6 +1111,32 @@ k1_packed(const __grid_constant__ K1cParams p) {
             h = __shfl_sync(kFull, x, 31);
             ends = __reduce_add_sync(kFull, e);
             const int base = x - cnt;                 // this lane's first piece
+#if TP_K1P_BALB
+            // balanced pass B: heads cluster at small m (most requests end early), so piece kk goes
+            // to lane kk % 32 instead of the lane whose segment holds it; its owner t (the last lane
+            // with base_t <= kk, by a shuffle binary search) and its bit (the (kk - base_t)-th set
+            // bit of mask_t) give its m
+            K1P_SYNC();                               // every lane's keys are in place
+            #pragma unroll 1
+            for (int k0 = 0; k0 < h; k0 += 32) {
+                const int kk = k0 + lane;
+                int t = 0;
+#pragma unroll
+                for (int o = 16; o; o >>= 1) {
+                    const int bt = __shfl_sync(kFull, base, t + o);
+                    if (bt <= kk) t += o;
+                }
+                const uint32_t mt = (uint32_t)__shfl_sync(kFull, (int)mask, t);
+                const int jt = kk - __shfl_sync(kFull, base, t);
+                if (kk < h) {
+                    const int m = 1 + t * S2 + (int)__fns(mt, 0u, jt + 1);
+                    const uint32_t k = cell_base + (uint32_t)sv[ph(m)];
+                    *ptr_at(rec_m, (unsigned)kk) = m;
+                    *ptr_at(rec_k, (unsigned)kk) = k;
+                    claim_cell(p, k);                 // (also where a piece only repeats the cell)
+                }
+            }
+#else
             int pos = base;
             #pragma unroll 1
             for (uint32_t mm = mask; mm; mm &= mm - 1, ++pos) {
@@ -1117,6 +1146,7 @@ k1_packed(const __grid_constant__ K1cParams p) {
                 *ptr_at(rec_k, (unsigned)pos) = k;
                 claim_cell(p, k);                     // (also where a piece only repeats the cell)
             }
+#endif
             #pragma unroll 1
             for (int k = lane; k < h; k += 32) D[k] = kNoDeadline;
             K1P_SYNC();                               // every lane's keys read
