@@ -1390,8 +1390,17 @@ int launch_packed(const K1cParams& p0, int32_t n_inst, int32_t H, cudaStream_t s
     const SegGeom g = seg_geom(H, 32);
     p.S_log2 = g.S_log2;
     p.P = g.P;
-    p.arr = g.arr;
-    const size_t per_warp = (size_t)g.arr * sizeof(int);
+    int arr = g.arr;
+#if TP_K1P_LINEAR
+    {   // unpadded: the S2-segment passes touch words < 32 S2(H) (S2 is monotone in n), the events
+        // and the cleared prefix words <= H + 4
+        int S2 = (((H + 31) >> 5) + 3) & ~3;
+        if ((S2 & 4) == 0 && 32 * (S2 - 4) < H && S2 + 4 <= 32) S2 += 4;
+        arr = (std::max(32 * S2, H + 8) + 3) & ~3;
+    }
+#endif
+    p.arr = arr;
+    const size_t per_warp = (size_t)arr * sizeof(int);
     if (per_warp > 200 * 1024) return TP_EINVAL;
     // rank tables in shared memory when they are small next to the histograms (the model's cut sets)
     const int tab_entries = p.rtab_off[1] + p.rtab_len[1];
